@@ -1,0 +1,165 @@
+"""Validates the NEW BEM CPU oracle (oracle/bem_oracle.cpp; the reference has no
+BEM) against closed forms: Kelvin static limits, the Navier PDE
+residual by finite differences, traction = σ(U)·n by finite differences, the
+Taylor/direct branch continuity, and the analytic spherical cavity
+(SURVEY.md Appendix A.3). Also checks the oracle LU against LAPACK.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_1511_04355_b200 import mesh
+
+MU, NU, RHO = 1.0, 0.25, 1.0
+LAM = 2 * MU * NU / (1 - 2 * NU)
+
+
+def kelvin_U(rv):
+    r = np.linalg.norm(rv)
+    e = rv / r
+    return ((3 - 4 * NU) * np.eye(3) + np.outer(e, e)) / (16 * math.pi * MU * (1 - NU) * r)
+
+
+def kelvin_T(rv, n):
+    r = np.linalg.norm(rv)
+    e = rv / r
+    rn = e @ n
+    T = np.zeros((3, 3))
+    for i in range(3):
+        for j in range(3):
+            T[i, j] = -1 / (8 * math.pi * (1 - NU) * r * r) * (
+                rn * ((1 - 2 * NU) * (i == j) + 3 * e[i] * e[j]) - (1 - 2 * NU) * (e[i] * n[j] - e[j] * n[i]))
+    return T
+
+
+def test_static_limit_kelvin():
+    rv = np.array([0.3, -0.2, 0.5])
+    n = np.array([0.0, 0.6, 0.8])
+    U, T = O.kernel_ut(rv, n, 1e-7)
+    np.testing.assert_allclose(U.real, kelvin_U(rv), rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(T.real, kelvin_T(rv, n), rtol=1e-6, atol=1e-10)
+
+
+def _U(x, s):
+    U, _ = O.kernel_ut(x, np.array([0.0, 0.0, 1.0]), s)
+    return U
+
+
+def test_navier_pde_residual():
+    """mu ∇²U + (λ+μ) ∇(∇·U) − ρ s² U = 0 away from the source (O(h²) FD)."""
+    s = complex(0.7, 1.3)
+    x0 = np.array([0.4, 0.3, -0.5])
+    h = 2e-3
+    E = np.eye(3)
+
+    def lap(i):
+        return sum(_U(x0 + h * E[d], s)[i] - 2 * _U(x0, s)[i] + _U(x0 - h * E[d], s)[i] for d in range(3)) / h**2
+
+    for i in range(3):  # load direction i: displacement field U[i, :]
+        graddiv = np.zeros(3, complex)
+        for a in range(3):
+            for b in range(3):
+                if a == b:
+                    graddiv[a] += (_U(x0 + h * E[a], s)[i, b] - 2 * _U(x0, s)[i, b] + _U(x0 - h * E[a], s)[i, b]) / h**2
+                else:
+                    graddiv[a] += (_U(x0 + h * E[a] + h * E[b], s)[i, b] - _U(x0 + h * E[a] - h * E[b], s)[i, b]
+                                   - _U(x0 - h * E[a] + h * E[b], s)[i, b] + _U(x0 - h * E[a] - h * E[b], s)[i, b]) / (4 * h * h)
+        res = MU * lap(i) + (LAM + MU) * graddiv - RHO * s * s * _U(x0, s)[i]
+        assert np.max(np.abs(res)) < 2e-4 * np.max(np.abs(MU * lap(i)))
+
+
+def test_traction_is_stress_of_U():
+    s = complex(1.1, 2.5)
+    x0 = np.array([0.2, -0.35, 0.6])
+    n = np.array([1.0, 2.0, -2.0]) / 3.0
+    h = 1e-4
+    E = np.eye(3)
+    _, T = O.kernel_ut(x0, n, s)
+    for i in range(3):
+        grad = np.zeros((3, 3), complex)  # grad[j, k] = dU_ij/dy_k
+        for k in range(3):
+            grad[:, k] = (_U(x0 + h * E[k], s)[i] - _U(x0 - h * E[k], s)[i]) / (2 * h)
+        div = np.trace(grad)
+        sigma = LAM * div * np.eye(3) + MU * (grad + grad.T)
+        np.testing.assert_allclose(T[i], sigma @ n, rtol=1e-6, atol=1e-8)
+
+
+def test_series_direct_continuity():
+    for ang in np.linspace(0, 1.4, 6):
+        z_in = 0.29999 * np.exp(1j * ang)
+        z_out = 0.30001 * np.exp(1j * ang)
+        a, b = O.kernel_abcd(z_in), O.kernel_abcd(z_out)
+        assert np.max(np.abs(a - b)) < 1e-4 * 0.00002 / 0.0001 + 1e-12
+
+
+def test_series_matches_direct_formula():
+    """Direct closed form in Python at |z| = 0.29 (cancellation error ~ eps/|z|^2 ~ 3e-15)."""
+    k = 1 / math.sqrt(3)
+    for ang in (0.0, 0.5, 1.2, 1.57):
+        z = 0.29 * np.exp(1j * ang)
+        x1 = k * z
+        e2, e1 = np.exp(-z), np.exp(-x1)
+        A = (1 + 1 / z + 1 / z**2) * e2 - k * k * (1 / x1 + 1 / x1**2) * e1
+        B = (1 + 3 / z + 3 / z**2) * e2 - k * k * (1 + 3 / x1 + 3 / x1**2) * e1
+        C = -(z + 2 + 3 / z + 3 / z**2) * e2 + k * k * (1 + 3 / x1 + 3 / x1**2) * e1
+        D = -(z + 4 + 9 / z + 9 / z**2) * e2 + k * k * (x1 + 4 + 9 / x1 + 9 / x1**2) * e1
+        np.testing.assert_allclose(O.kernel_abcd(z), [A, B, C, D], rtol=0, atol=2e-13)
+
+
+def test_lu_matches_lapack():
+    rng = np.random.default_rng(3)
+    n = 60
+    A = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    np.testing.assert_allclose(O.lu_solve(A, b), np.linalg.solve(A, b), rtol=1e-10)
+
+
+@pytest.fixture(scope="module")
+def sphere320():
+    V, F = mesh.icosphere(2)
+    return V, F, O.Bem(V, F, mesh.pressure_traction(V, F))
+
+
+def test_sphere_mesh_counts():
+    for lvl, ne in ((2, 320), (3, 1280)):
+        V, F = mesh.icosphere(lvl)
+        assert F.shape[0] == ne
+        c, n, _ = mesh.element_geometry(V, F)
+        assert np.all(np.einsum("ij,ij->i", c, n) < 0)  # normals into the cavity
+    V, F = mesh.cube_cavity(4)
+    assert F.shape[0] == 12 * 16
+    c, n, a = mesh.element_geometry(V, F)
+    assert np.all(np.einsum("ij,ij->i", c - 0.5, n) < 0)
+    assert a.sum() == pytest.approx(6.0)
+
+
+def _sphere_err(level, s):
+    V, F = mesh.icosphere(level)
+    bem = O.Bem(V, F, mesh.pressure_traction(V, F))
+    _, n, _ = mesh.element_geometry(V, F)
+    u = bem.solve(s).reshape(-1, 3)
+    ur = -np.einsum("ij,ij->i", u, n)  # radial = -n (n points to the centre)
+    ref = mesh.sphere_radial_analytic(s)
+    ut = u + ur[:, None] * n
+    return np.max(np.abs(ur - ref)) / abs(ref), np.max(np.abs(ut)) / abs(ref)
+
+
+def test_sphere_cavity_matches_analytic():
+    """Constant flat elements converge ~O(h): 10.8% (80) -> 4.9% (320) -> 2.2% (1280 tris)."""
+    for s in (complex(0.9, 0.4), complex(0.25, 1.5)):
+        e80, _ = _sphere_err(1, s)
+        e320, t320 = _sphere_err(2, s)
+        assert e320 < 0.06
+        assert e320 < 0.6 * e80  # discretisation convergence
+        assert t320 < 2e-2  # tangential components vanish by symmetry
+
+
+def test_static_sphere_limit(sphere320):
+    V, F, bem = sphere320
+    _, n, _ = mesh.element_geometry(V, F)
+    s = complex(1e-3, 0.0)
+    u = bem.solve(s).reshape(-1, 3) * s  # s * U(s) -> static U = p a / (4 mu) = 0.25
+    ur = -np.einsum("ij,ij->i", u, n)
+    assert np.max(np.abs(ur - 0.25)) < 0.06 * 0.25  # same O(h) discretisation error

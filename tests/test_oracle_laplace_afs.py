@@ -1,0 +1,162 @@
+"""Pins the CPU oracle's Laplace-inversion restatement and the reference's own
+AFS driver (proj/src/afs.cpp, compiled unmodified into the oracle) to the
+SPEC.md examples — the reference's test_laplace.cpp / test_afs.cpp are absent
+(proj/tests/CMakeLists.txt:1-20), so the SPEC examples are the surviving pins.
+"""
+import json
+import math
+
+import numpy as np
+import pytest
+
+import pyoracle as O
+from helpers import ModalFixture, contour_points
+
+
+def test_damping_eta_spec_example():
+    assert O.damping_eta(3.0, 0.0155) == pytest.approx(445.66, abs=0.01)
+    assert O.damping_eta(0.0, 1.0) == 0.0
+
+
+def test_hanning_window_examples():
+    assert O.hanning_window(0, 16) == 1.0
+    assert O.hanning_window(8, 16) == pytest.approx(0.0, abs=1e-16)
+    for k in range(1, 16):
+        assert O.hanning_window(k, 16) == pytest.approx(O.hanning_window(16 - k, 16), abs=1e-15)
+
+
+def test_conjugate_fill_example():
+    out = O.conjugate_fill([1.0, 1j, 2.0])
+    np.testing.assert_array_equal(out, np.array([1.0, 1j, 2.0, -1j]))
+
+
+def test_fsm_grid_identities():  # SPEC.md FsmGrid invariants
+    dw, dt, wm, nc = O.fsm_grid(4.0, 512)
+    assert nc == 257
+    assert dw * dt * 512 == pytest.approx(2 * math.pi, rel=1e-15)
+    assert wm == pytest.approx(math.pi / dt, rel=1e-15)
+
+
+def _fsm_rms(ns):
+    T, a = 4.0, -5.0
+    eta = O.damping_eta(3.0, T)
+    dw = 2 * math.pi / T
+    s = eta + 1j * dw * np.arange(ns // 2 + 1)
+    h = O.fsm_invert(T, ns, eta, (1.0 / (s - a))[None, :])[0]
+    t = np.arange(ns) * T / ns
+    mask = t <= 0.9 * T
+    err = h[mask] - np.exp(a * t[mask])
+    return math.sqrt(np.mean(err ** 2)) / 1.0
+
+
+@pytest.mark.xfail(strict=True, reason=(
+    "SPEC.md:257/519 asks RMS <= 2% of peak on [0, 0.9T]; the specified FSM (Hanning, 1/T, full "
+    "k=0 weight) gives 2.439% at N_s=512 — the t=0 step of e^{-5t} reconstructs at ~0.5. An "
+    "independent numpy.fft restatement gives the same 0.024392554787831 (see DESIGN.md §7)."))
+def test_fsm_reconstructs_exponential_2pct():  # SPEC.md:257, acceptance #3
+    assert _fsm_rms(512) <= 0.02
+
+
+def test_fsm_reconstructs_exponential():  # SPEC.md:257, acceptance #3
+    r512 = _fsm_rms(512)
+    r256 = _fsm_rms(256)
+    assert r512 == pytest.approx(0.024392554787831, rel=1e-9)  # numpy.fft restatement value
+    assert r256 <= 2.0 * r512  # "halving N_s at most doubles the RMS"
+
+
+def test_fsm_zero_spectrum():
+    out = O.fsm_invert(1.0, 16, 0.5, np.zeros((2, 9), complex))
+    assert np.all(out == 0.0)
+
+
+def test_rational_invert_examples():
+    h = O.rational_invert([complex(-2, 0)], [[1.0 + 0j]], [0.0, 0.5])
+    assert h[0, 0] == 1.0
+    t = np.linspace(0, 2, 50)
+    h = O.rational_invert([complex(-1, 10), complex(-1, -10)], [[0.5 + 0j, 0.5 + 0j]], t)
+    np.testing.assert_allclose(h[0], np.exp(-t) * np.cos(10 * t), atol=1e-14)
+
+
+def test_rational_invert_errors():  # laplace.cpp:129-143
+    with pytest.raises(O.OracleError) as e:
+        O.rational_invert([complex(-1, 0)], [[1.0 + 0j]], [0.0, 0.0])
+    assert e.value.kind == "ValidationError"
+    with pytest.raises(O.OracleError) as e:
+        O.rational_invert([complex(1, 0)], [[1.0 + 0j]], [0.0, 800.0])
+    assert e.value.kind == "NumericError"
+
+
+def test_initial_frequencies_example():
+    s = O.initial_frequencies(3, 0.5, 10.0)
+    np.testing.assert_allclose(s.imag, [0.0, 10.0 * (1 - math.cos(math.pi / 4)), 10.0], rtol=1e-15)
+    assert np.all(s.real == 0.5)
+
+
+def test_fit_orders_examples():
+    assert O.fit_orders(32) == (16, 13)
+    assert O.fit_orders(16) == (8, 6)
+    assert O.fit_orders(5) == (2, 1)
+
+
+def test_channel_errors_examples():
+    poles = [complex(-1, 3), complex(-1, -3)]
+    res = [[complex(1, 1), complex(1, -1)]]
+    grid = contour_points(0.5, 10.0, 64)
+    assert O.channel_errors(poles, res, poles, res, grid)[0] == 0.0
+    assert O.channel_errors(poles, res, poles, [[0j, 0j]], grid)[0] == 1.0
+
+
+def _modal_system(channels=4):
+    fx = ModalFixture(channels)
+    return fx, O.System.from_json(fx.system_json())
+
+
+def test_afs_infinite_thresholds_gives_j0_plus_jc():
+    fx, sysm = _modal_system()
+    r = O.run_afs(sysm, omega_max=1.5 * fx.band, eta=0.35, period=20.0, orf=[0, 1], test=[2, 3],
+                  initial_count=8, e1_threshold=float("inf"), e2_threshold=float("inf"),
+                  validation_steps=3, grid_points=512, time_points=128)
+    assert r["converged"] and r["n_c"] == 8 + 3
+
+
+def test_afs_invariants_modal():  # SPEC.md:384-389, acceptance #6
+    # Default thresholds drive the 8-mode (exactly 16-pole) fixture to M_H > 16, where the
+    # reference's sigma LS is exactly rank-deficient and relocate_poles throws (vecfit.cpp:282);
+    # looser thresholds converge first.
+    fx, sysm = _modal_system(6)
+    kw = dict(omega_max=1.5 * fx.band, eta=0.35, period=20.0, orf=[0, 1, 2], test=[3, 4, 5],
+              initial_count=16, grid_points=1024, time_points=256, e1_threshold=1e-2, e2_threshold=5e-2)
+    r1 = O.run_afs(sysm, **kw)
+    r2 = O.run_afs(sysm, **kw)
+    assert r1["converged"]
+    assert r1["solver_calls"] == r1["n_c"] == len(r1["samples"])
+    np.testing.assert_array_equal(r1["samples"], r2["samples"])
+    J = r1["history"][:, 0]
+    assert np.all(np.diff(J) == 1)
+    jc = 3
+    tail = r1["history"][-(jc + 1):]
+    assert np.all(tail[:, 6] <= 1e-2) and np.all(tail[:, 7] <= 5e-2)
+    assert len(set(np.round(r1["samples"].imag, 12))) == r1["n_c"]
+
+
+def _rod_json():
+    st = [(3.0, "displacement", "p1_disp"), (0.0, "traction", "p2_trac"), (3.0, "displacement", "p3_disp"),
+          (0.0, "traction", "p4_trac"), (1.53, "displacement", "p5_disp"), (0.0, "traction", "p6_trac"),
+          (1.898, "displacement", "p7_disp")]
+    return json.dumps({"type": "rod", "length": 3.0, "youngs_modulus": 2.11e11, "density": 7.85e3,
+                       "load_amplitude": -1.0e6,
+                       "stations": [{"x": x, "quantity": q, "label": l} for x, q, l in st]})
+
+
+@pytest.mark.xfail(strict=True, raises=O.OracleError, reason=(
+    "SPEC.md acceptance #4 on the reference algorithm: at J=56 (M_H=28) the stacked sigma LS "
+    "reaches |R_ii| = 4.6e-15 < Eigen's rank threshold 5.8e-15 and relocate_poles throws "
+    "NumericError before the E1/E2 streak completes (DESIGN.md §7)."))
+def test_afs_rod_example1_acceptance():  # SPEC.md acceptance #4 (N_c <= 55 vs FSM 110)
+    sysr = O.System.from_json(_rod_json())
+    T, ns = 0.0155, 218
+    wmax = math.pi * ns / T
+    r = O.run_afs(sysr, omega_max=wmax, eta=O.damping_eta(3.0, T), period=T,
+                  orf=[0, 1, 2, 3, 4], test=[5, 6])
+    assert r["converged"]
+    assert r["n_c"] <= 55
