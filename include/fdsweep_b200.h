@@ -1,0 +1,205 @@
+/*
+ * fdsweep_b200 — C-ABI of the B200-native hot path behind the reference
+ * toolkit's solver/fitting/inversion API (arxiv 1511.04355, `fdsweep`).
+ *
+ * Plain pointers and sizes only; no CUDA or torch types. Complex numbers are
+ * `fds_c64` = two doubles (re, im), layout-identical to std::complex<double>
+ * (proj/include/fdsweep/types.hpp:10) so a C++ caller passes
+ * reinterpret_cast<const fds_c64*>(vec.data()).
+ *
+ * Status codes map one-to-one onto the reference's exception classes
+ * (proj/include/fdsweep/types.hpp:14-36): FDS_EVALIDATION -> ValidationError,
+ * FDS_ENUMERIC -> NumericError, FDS_EIO -> IoError, FDS_ECONVERGENCE ->
+ * ConvergenceError. FDS_ECUDA means the device path failed (no fallback
+ * exists). fds_last_error() returns the thread-local message of the last
+ * failing call on this thread.
+ *
+ * Host layouts follow the reference: samples are per-frequency AoS
+ * values[j*K + k] (FrequencySample::values, types.hpp:40-45), residues are
+ * channel-major res[k*M + m] (RationalModel::residues, vecfit.hpp:21-30),
+ * time series are channel-major out[k*T + n] (TimeSeries::values, types.hpp:48-56).
+ */
+#ifndef FDSWEEP_B200_H
+#define FDSWEEP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef struct {
+    double re, im;
+} fds_c64;
+
+enum {
+    FDS_OK = 0,
+    FDS_EVALIDATION = 1,
+    FDS_ENUMERIC = 2,
+    FDS_EIO = 3,
+    FDS_ECONVERGENCE = 4,
+    FDS_ECUDA = 5
+};
+
+const char* fds_last_error(void);
+/* Version string of the library ("fdsweep_b200 <semver> sm_100a"). */
+const char* fds_version(void);
+/* Select the CUDA device for subsequent calls on this thread. */
+int fds_set_device(int device);
+
+/* ------------------------------------------------------------------------
+ * BEM frequency system — replaces FrequencySystem::evaluate(Complex s)
+ * (proj/include/fdsweep/systems.hpp:34-42; called by run_afs at
+ * proj/src/afs.cpp:293 and by the FSM sweep).
+ * Laplace-domain 3D elastodynamic collocation BEM on constant flat
+ * triangles; unknowns element-major u[3e + {x,y,z}]; load = per-element
+ * traction vector x Heaviside factor 1/s. The handle is immutable after
+ * create; evaluate is deterministic (bit-identical for equal s) and
+ * reentrant (calls are serialised per handle on its own stream).
+ * ---------------------------------------------------------------------- */
+typedef struct fds_bem fds_bem;
+
+typedef struct {
+    int n_vertices;
+    const double* vertices;   /* [n_vertices][3] */
+    int n_elements;
+    const int* triangles;     /* [n_elements][3]; (v1-v0)x(v2-v0) = domain-outward normal */
+    double shear_modulus;     /* mu */
+    double poisson_ratio;     /* nu */
+    double density;           /* rho */
+    const double* traction;   /* [n_elements][3], multiplied by p(s) = 1/s */
+    int n_channels;           /* output DOFs; 0 => all 3*n_elements */
+    const int* channels;      /* DOF indices into u */
+    int max_batch;            /* frequencies solved concurrently; 0 => auto from free HBM */
+} fds_bem_desc;
+
+int fds_bem_create(const fds_bem_desc* desc, fds_bem** out);
+int fds_bem_destroy(fds_bem* bem);
+int fds_bem_channels(const fds_bem* bem);
+int fds_bem_unknowns(const fds_bem* bem);
+/* One solve: out[k] = u_channel_k(s). Host buffers. */
+int fds_bem_evaluate(fds_bem* bem, fds_c64 s, fds_c64* out);
+/* B independent solves (batched assembly + LU + solve): out[b*K + k]. Host buffers. */
+int fds_bem_evaluate_batch(fds_bem* bem, const fds_c64* s, int B, fds_c64* out);
+/* Same, device-resident result (pointer to B*K fds_c64 in HBM, valid until the
+ * next call on this handle); used by the bench to time the path without copies. */
+int fds_bem_evaluate_batch_device(fds_bem* bem, const fds_c64* s, int B, const fds_c64** dev_out);
+/* Debug / parity: assembled A(s) (column-major N x N) and b(s) to host. */
+int fds_bem_assemble_host(fds_bem* bem, fds_c64 s, fds_c64* A, fds_c64* b);
+/* Per-stage device times of the last evaluate_batch call (ms): assembly, LU, solve;
+ * and the number of kernel launches it issued. */
+int fds_bem_last_timing(const fds_bem* bem, double* assembly_ms, double* lu_ms, double* solve_ms,
+                        int* launches);
+
+/* Dense complex LU + solve on the device for caller-provided host matrices
+ * (column-major, B matrices of order n): x[b] = A[b]^{-1} rhs[b]. */
+int fds_zgesv_batch(int n, int B, const fds_c64* A, const fds_c64* rhs, fds_c64* x);
+/* Device-resident variant: A (planar: re plane then im plane,
+ * column-major, B consecutive matrices) is factored in place; returns ms. */
+int fds_lu_factor_device(int n, int B, double* A_planar, int* ipiv, int* info, double* ms);
+
+/* ------------------------------------------------------------------------
+ * Vector fitting — replaces proj/src/vecfit.cpp (vecfit.hpp:48-86).
+ * ---------------------------------------------------------------------- */
+/* relocate_poles (vecfit.cpp:188-354): samples restricted to K channels. */
+int fds_vf_relocate(int J, int K, const fds_c64* s, const fds_c64* values, int M,
+                    const fds_c64* poles_in, fds_c64* poles_out, double* per_channel_rms,
+                    double* movement);
+/* identify_residues for K channels at once (vecfit.cpp:356-408 applied per channel;
+ * the LS matrix is shared): res[k*M + m], rms[k] (may be NULL). */
+int fds_vf_identify_residues(int J, int K, const fds_c64* s, const fds_c64* values, int M,
+                             const fds_c64* poles, fds_c64* residues, double* rms);
+/* vector_fit (vecfit.cpp:410-488). report_i = {iterations_used, unstable_pole_count},
+ * report_d = {pole_movement}; per_channel_rms[K], relocation_rms[n_orf] may be NULL. */
+int fds_vector_fit(int J, int K, const fds_c64* s, const fds_c64* values, int n_orf,
+                   const int* orf, int order, int n_relocations, fds_c64* poles_out,
+                   fds_c64* residues_out, int* report_i, double* report_d,
+                   double* per_channel_rms, double* relocation_rms);
+/* eval_model (vecfit.cpp:503-509) at G points: out[g*K + k]. */
+int fds_eval_model(int M, const fds_c64* poles, int K, const fds_c64* residues, int G,
+                   const fds_c64* s, fds_c64* out);
+/* channel_errors (afs.cpp:118-145): e[k] = max_g|fH-fL| / max_g|fH|. */
+int fds_channel_errors(int MH, const fds_c64* poles_h, const fds_c64* res_h, int ML,
+                       const fds_c64* poles_l, const fds_c64* res_l, int K, int G,
+                       const fds_c64* grid, double* errors);
+/* select_new_frequency (afs.cpp:147-187). */
+int fds_select_new_frequency(int MH, const fds_c64* poles_h, const fds_c64* res_h, int ML,
+                             const fds_c64* poles_l, const fds_c64* res_l, int K, int G,
+                             const fds_c64* grid, int n_existing, const fds_c64* existing,
+                             int n_orf, const int* orf_positions, double exclusion_radius,
+                             fds_c64* s_new);
+
+/* ------------------------------------------------------------------------
+ * Time reconstruction — replaces proj/src/laplace.cpp (laplace.hpp:40-59).
+ * ---------------------------------------------------------------------- */
+/* fsm_invert (laplace.cpp:89-125): half[k*(Ns/2+1) + i] -> out[k*Ns + n]. */
+int fds_fsm_invert(double period, int Ns, double eta, int K, const fds_c64* half, int hanning,
+                   double* out);
+/* rational_invert (laplace.cpp:127-164): out[k*T + n]. */
+int fds_rational_invert(int M, const fds_c64* poles, int K, const fds_c64* residues, int T,
+                        const double* t, double* out);
+
+/* Device-resident VF/FSM stage for the bench (config 5): all pointers are HBM.
+ * residues: [k*M + m]; values: [j*K + k]; half: [i*K + k] (frequency-major);
+ * out: [k*Ns + n] / [k*T + n]. Each returns the kernel-only device ms. */
+int fds_vf_identify_residues_device(int J, int K, const fds_c64* s_host, const fds_c64* values_dev,
+                                    int M, const fds_c64* poles_host, fds_c64* residues_dev,
+                                    double* ms);
+int fds_rational_invert_device(int M, const fds_c64* poles_host, int K, const fds_c64* residues_dev,
+                               int T, const double* t_host, double* out_dev, double* ms);
+int fds_fsm_invert_device(double period, int Ns, double eta, int K, const fds_c64* half_dev,
+                          int hanning, double* out_dev, double* ms);
+
+/* ------------------------------------------------------------------------
+ * AFS driver — replaces run_afs (proj/src/afs.cpp:226-396) for a BEM system
+ * or a rational/modal closed-form system (evaluated on the host).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int initial_count;      /* J0 */
+    double alpha_high, alpha_low;
+    double e1_threshold, e2_threshold;
+    int validation_steps;   /* J_c */
+    int n_orf;
+    const int* orf_indices; /* NULL/0 => draw 5 with seed */
+    int n_test;
+    const int* test_indices; /* NULL/0 => all channels */
+    double omega_max, eta, period;
+    int grid_points, time_points, max_iterations;
+    uint64_t seed;
+    int n_relocations;
+} fds_afs_config;
+
+typedef struct {
+    int n_c;
+    int converged;
+    int solver_calls;
+    int n_history;
+    int order;              /* M_H of the final model */
+} fds_afs_summary;
+
+/* Callback system for non-BEM systems: fills out[K] at s; returns 0 on success. */
+typedef int (*fds_system_fn)(void* user, fds_c64 s, fds_c64* out);
+
+/* samples_s[cap], history[cap*8] rows {J, MH, ML, has_s_new, re, im, E1, E2},
+ * poles[cap], residues[K*cap] (final model over all channels, [k*order+m]). */
+int fds_run_afs_bem(fds_bem* bem, const fds_afs_config* cfg, int cap, fds_c64* samples_s,
+                    fds_c64* sample_values, double* history, fds_c64* poles, fds_c64* residues,
+                    fds_afs_summary* summary);
+int fds_run_afs_callback(fds_system_fn fn, void* user, int channels, const fds_afs_config* cfg,
+                         int cap, fds_c64* samples_s, fds_c64* sample_values, double* history,
+                         fds_c64* poles, fds_c64* residues, fds_afs_summary* summary);
+
+/* Count of kernels this library launched since load (evidence for the bench). */
+int64_t fds_kernel_launches(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FDSWEEP_B200_H */

@@ -1,0 +1,361 @@
+// C-ABI for the BEM frequency system and the batched complex LU
+// (include/fdsweep_b200.h). Replaces FrequencySystem::evaluate
+// (proj/include/fdsweep/systems.hpp:34-42) with a CUDA path; there is no CPU
+// fallback — every entry point fails with FDS_ECUDA if the device path fails.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "bem.cuh"
+#include "capi_util.h"
+#include "lu.cuh"
+
+namespace fdsb {
+
+std::atomic<int64_t> g_launches{0};
+
+const DeviceInfo& device_info() {
+    static thread_local DeviceInfo info;
+    static thread_local bool init = false;
+    if (!init) {
+        int dev = 0;
+        FDS_CUDA(cudaGetDevice(&dev));
+        cudaDeviceProp p;
+        FDS_CUDA(cudaGetDeviceProperties(&p, dev));
+        if (p.major != 10) throw CudaError("fdsweep_b200 is built for sm_100a (B200); found sm_" +
+                                           std::to_string(p.major) + std::to_string(p.minor));
+        info.device = dev;
+        info.sms = p.multiProcessorCount;
+        info.smem_optin = p.sharedMemPerBlockOptin;
+        init = true;
+    }
+    return info;
+}
+
+thread_local std::string g_error;
+
+__global__ void gather_channels_kernel(const cplx* __restrict__ rhs, size_t rstride, const int* __restrict__ ch,
+                                       int K, int B, cplx* __restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= K * B) return;
+    const int b = idx / K, k = idx % K;
+    out[idx] = rhs[static_cast<size_t>(b) * rstride + ch[k]];
+}
+
+}  // namespace fdsb
+
+using namespace fdsb;
+
+struct fds_bem {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    BemDevice dev;
+    int ne = 0, n = 0, ld = 0;
+    size_t plane = 0, mstride = 0;
+    int K = 0;
+    int* chan = nullptr;
+    int cap = 0, max_batch = 0;
+    double* A = nullptr;
+    int* ipiv = nullptr;
+    int* info = nullptr;
+    cplx* rhs = nullptr;
+    cplx* svec = nullptr;
+    cplx* out = nullptr;
+    LuWorkspace ws;
+    cudaEvent_t ev[4] = {};
+    double t_asm = 0, t_lu = 0, t_solve = 0;
+    int launches = 0;
+
+    void ensure(int B) {
+        if (B <= cap) return;
+        auto fr = [](void* p) { if (p) cudaFree(p); };
+        fr(A); fr(ipiv); fr(info); fr(rhs); fr(svec); fr(out); fr(dev.partial); fr(dev.corr);
+        FDS_CUDA(cudaMalloc(&A, mstride * B * sizeof(double)));
+        FDS_CUDA(cudaMemsetAsync(A, 0, mstride * B * sizeof(double), st));  // padding stays zero
+        FDS_CUDA(cudaMalloc(&ipiv, static_cast<size_t>(B) * n * sizeof(int)));
+        FDS_CUDA(cudaMalloc(&info, B * sizeof(int)));
+        FDS_CUDA(cudaMalloc(&rhs, static_cast<size_t>(B) * ld * sizeof(cplx)));
+        FDS_CUDA(cudaMalloc(&svec, B * sizeof(cplx)));
+        FDS_CUDA(cudaMalloc(&out, static_cast<size_t>(B) * K * sizeof(cplx)));
+        const int nchunks = ceil_div(ne, kFarChunk);
+        dev.pstride = static_cast<size_t>(nchunks) * 3 * ne;
+        FDS_CUDA(cudaMalloc(&dev.partial, dev.pstride * B * sizeof(cplx)));
+        dev.cstride = static_cast<size_t>(dev.npairs) * 3;
+        FDS_CUDA(cudaMalloc(&dev.corr, std::max<size_t>(dev.cstride, 3) * B * sizeof(cplx)));
+        cap = B;
+    }
+
+    int chunk_limit() const {
+        if (max_batch > 0) return max_batch;
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const size_t per = mstride * sizeof(double) + dev.pstride * sizeof(cplx) + 4096 * 64;
+        const size_t budget = static_cast<size_t>(0.85 * (fr + static_cast<size_t>(cap) * per));
+        return std::max<int>(1, static_cast<int>(budget / std::max<size_t>(per, 1)));
+    }
+
+    // Solves B frequencies already in svec_host; result (B x K) left in `out` on device.
+    void run(const fds_c64* s_host, int B) {
+        launches = 0;
+        t_asm = t_lu = t_solve = 0;
+        const int64_t l0 = g_launches.load();
+        ensure(B);
+        FDS_CUDA(cudaMemcpyAsync(svec, s_host, B * sizeof(cplx), cudaMemcpyHostToDevice, st));
+        FDS_CUDA(cudaEventRecord(ev[0], st));
+        bem_assemble(dev, svec, B, A, mstride, plane, ld, rhs, ld, st);
+        FDS_CUDA(cudaEventRecord(ev[1], st));
+        LuProblem pb;
+        pb.A = A;
+        pb.mstride = mstride;
+        pb.plane = plane;
+        pb.n = n;
+        pb.ld = ld;
+        pb.batch = B;
+        pb.ipiv = ipiv;
+        pb.info = info;
+        lu_factor(pb, ws, st);
+        FDS_CUDA(cudaEventRecord(ev[2], st));
+        lu_solve(pb, rhs, ld, st);
+        FDS_LAUNCH(gather_channels_kernel, ceil_div(K * B, 256), 256, 0, st, rhs, static_cast<size_t>(ld),
+                   chan, K, B, out);
+        FDS_CUDA(cudaEventRecord(ev[3], st));
+        std::vector<int> hinfo(B);
+        FDS_CUDA(cudaMemcpyAsync(hinfo.data(), info, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+        FDS_CUDA(cudaStreamSynchronize(st));
+        for (int b = 0; b < B; ++b)
+            if (hinfo[b] != 0) throw NumericError("bem: singular system matrix (zero pivot at column " +
+                                                  std::to_string(hinfo[b] - 1) + ")");
+        float ms;
+        FDS_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        t_asm = ms;
+        FDS_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+        t_lu = ms;
+        FDS_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+        t_solve = ms;
+        launches = static_cast<int>(g_launches.load() - l0);
+    }
+};
+
+extern "C" {
+
+const char* fds_last_error(void) { return g_error.c_str(); }
+const char* fds_version(void) { return "fdsweep_b200 0.1.0 sm_100a"; }
+int64_t fds_kernel_launches(void) { return g_launches.load(); }
+
+int fds_set_device(int device) {
+    return fds_guard([&] { FDS_CUDA(cudaSetDevice(device)); });
+}
+
+int fds_bem_create(const fds_bem_desc* d, fds_bem** out) {
+    return fds_guard([&] {
+        if (!d || !out) throw ValidationError("fds_bem_create: null argument");
+        if (d->n_elements < 1 || d->n_vertices < 3 || !d->vertices || !d->triangles || !d->traction)
+            throw ValidationError("fds_bem_create: empty mesh or load");
+        device_info();
+        auto* h = new fds_bem;
+        try {
+            h->ne = d->n_elements;
+            h->n = 3 * h->ne;
+            h->ld = lu_ld(h->n);
+            h->plane = lu_plane(h->n);
+            h->mstride = 2 * h->plane;
+            h->max_batch = d->max_batch;
+            h->dev.ne = h->ne;
+            h->dev.params = make_bem_params(d->shear_modulus, d->poisson_ratio, d->density);
+            std::vector<double> geo;
+            std::vector<int> pairs, ptr;
+            bem_build_geometry(d->vertices, d->n_vertices, d->triangles, h->ne, geo, pairs, ptr);
+            h->dev.npairs = static_cast<int>(pairs.size() / 3);
+            std::vector<int> chans;
+            if (d->n_channels > 0) {
+                for (int i = 0; i < d->n_channels; ++i) {
+                    if (d->channels[i] < 0 || d->channels[i] >= h->n)
+                        throw ValidationError("fds_bem_create: channel DOF out of range");
+                    chans.push_back(d->channels[i]);
+                }
+            } else {
+                for (int i = 0; i < h->n; ++i) chans.push_back(i);
+            }
+            h->K = static_cast<int>(chans.size());
+            FDS_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+            for (auto& e : h->ev) FDS_CUDA(cudaEventCreate(&e));
+            FDS_CUDA(cudaMalloc(&h->dev.geo, geo.size() * sizeof(double)));
+            FDS_CUDA(cudaMalloc(&h->dev.trac, 3 * h->ne * sizeof(double)));
+            FDS_CUDA(cudaMalloc(&h->dev.pairs, std::max<size_t>(pairs.size(), 3) * sizeof(int)));
+            FDS_CUDA(cudaMalloc(&h->dev.near_ptr, ptr.size() * sizeof(int)));
+            FDS_CUDA(cudaMalloc(&h->chan, chans.size() * sizeof(int)));
+            FDS_CUDA(cudaMemcpy(h->dev.geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
+            FDS_CUDA(cudaMemcpy(h->dev.trac, d->traction, 3 * h->ne * sizeof(double), cudaMemcpyHostToDevice));
+            FDS_CUDA(cudaMemcpy(h->dev.pairs, pairs.data(), pairs.size() * sizeof(int), cudaMemcpyHostToDevice));
+            FDS_CUDA(cudaMemcpy(h->dev.near_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+            FDS_CUDA(cudaMemcpy(h->chan, chans.data(), chans.size() * sizeof(int), cudaMemcpyHostToDevice));
+        } catch (...) {
+            fds_bem_destroy(h);
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int fds_bem_destroy(fds_bem* h) {
+    if (!h) return FDS_OK;
+    auto fr = [](void* p) { if (p) cudaFree(p); };
+    if (h->st) cudaStreamSynchronize(h->st);
+    fr(h->A); fr(h->ipiv); fr(h->info); fr(h->rhs); fr(h->svec); fr(h->out); fr(h->chan);
+    fr(h->dev.geo); fr(h->dev.trac); fr(h->dev.pairs); fr(h->dev.near_ptr); fr(h->dev.partial); fr(h->dev.corr);
+    h->ws.release();
+    for (auto e : h->ev) if (e) cudaEventDestroy(e);
+    if (h->st) cudaStreamDestroy(h->st);
+    delete h;
+    return FDS_OK;
+}
+
+int fds_bem_channels(const fds_bem* h) { return h ? h->K : -1; }
+int fds_bem_unknowns(const fds_bem* h) { return h ? h->n : -1; }
+
+int fds_bem_evaluate_batch(fds_bem* h, const fds_c64* s, int B, fds_c64* out) {
+    return fds_guard([&] {
+        if (!h || (B > 0 && (!s || !out))) throw ValidationError("fds_bem_evaluate_batch: null argument");
+        if (B < 0) throw ValidationError("fds_bem_evaluate_batch: negative batch");
+        for (int b = 0; b < B; ++b)
+            if (s[b].re == 0.0 && s[b].im == 0.0)
+                throw ValidationError("bem: s = 0 is the pole of the Heaviside load");
+        std::lock_guard<std::mutex> lk(h->mu);
+        const int lim = h->chunk_limit();
+        double ta = 0, tl = 0, ts = 0;
+        int nl = 0;
+        for (int b0 = 0; b0 < B; b0 += lim) {
+            const int nb = std::min(lim, B - b0);
+            h->run(s + b0, nb);
+            FDS_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(b0) * h->K, h->out,
+                                     static_cast<size_t>(nb) * h->K * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+            FDS_CUDA(cudaStreamSynchronize(h->st));
+            ta += h->t_asm;
+            tl += h->t_lu;
+            ts += h->t_solve;
+            nl += h->launches;
+        }
+        h->t_asm = ta;
+        h->t_lu = tl;
+        h->t_solve = ts;
+        h->launches = nl;
+    });
+}
+
+int fds_bem_evaluate(fds_bem* h, fds_c64 s, fds_c64* out) { return fds_bem_evaluate_batch(h, &s, 1, out); }
+
+int fds_bem_evaluate_batch_device(fds_bem* h, const fds_c64* s, int B, const fds_c64** dev_out) {
+    return fds_guard([&] {
+        if (!h || !s || !dev_out || B < 1) throw ValidationError("fds_bem_evaluate_batch_device: bad argument");
+        std::lock_guard<std::mutex> lk(h->mu);
+        if (h->max_batch > 0 && B > h->max_batch)
+            throw ValidationError("fds_bem_evaluate_batch_device: B exceeds max_batch");
+        h->run(s, B);
+        *dev_out = reinterpret_cast<const fds_c64*>(h->out);
+    });
+}
+
+int fds_bem_assemble_host(fds_bem* h, fds_c64 s, fds_c64* A, fds_c64* b) {
+    return fds_guard([&] {
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->ensure(1);
+        FDS_CUDA(cudaMemcpyAsync(h->svec, &s, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+        bem_assemble(h->dev, h->svec, 1, h->A, h->mstride, h->plane, h->ld, h->rhs, h->ld, h->st);
+        std::vector<double> re(h->plane), im(h->plane);
+        FDS_CUDA(cudaMemcpyAsync(re.data(), h->A, h->plane * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        FDS_CUDA(cudaMemcpyAsync(im.data(), h->A + h->plane, h->plane * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        FDS_CUDA(cudaMemcpyAsync(b, h->rhs, h->n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+        FDS_CUDA(cudaStreamSynchronize(h->st));
+        for (int j = 0; j < h->n; ++j)
+            for (int i = 0; i < h->n; ++i) {
+                const size_t gi = static_cast<size_t>(j) * h->ld + i;
+                A[static_cast<size_t>(j) * h->n + i] = {re[gi], im[gi]};
+            }
+    });
+}
+
+int fds_bem_last_timing(const fds_bem* h, double* a, double* l, double* s, int* launches) {
+    if (!h) return FDS_EVALIDATION;
+    if (a) *a = h->t_asm;
+    if (l) *l = h->t_lu;
+    if (s) *s = h->t_solve;
+    if (launches) *launches = h->launches;
+    return FDS_OK;
+}
+
+// ------------------------------------------------------------------ batched zgesv
+int fds_zgesv_batch(int n, int B, const fds_c64* A, const fds_c64* rhs, fds_c64* x) {
+    return fds_guard([&] {
+        if (n < 1 || B < 1 || !A || !rhs || !x) throw ValidationError("fds_zgesv_batch: bad argument");
+        device_info();
+        const int ld = lu_ld(n);
+        const size_t plane = lu_plane(n), mstride = 2 * plane;
+        std::vector<double> h(mstride * B, 0.0);
+        for (int b = 0; b < B; ++b)
+            for (int j = 0; j < n; ++j)
+                for (int i = 0; i < n; ++i) {
+                    const fds_c64 v = A[static_cast<size_t>(b) * n * n + static_cast<size_t>(j) * n + i];
+                    h[b * mstride + static_cast<size_t>(j) * ld + i] = v.re;
+                    h[b * mstride + plane + static_cast<size_t>(j) * ld + i] = v.im;
+                }
+        DeviceBuffer<double> dA(mstride * B);
+        DeviceBuffer<int> dp(static_cast<size_t>(n) * B), di(B);
+        DeviceBuffer<cplx> dr(static_cast<size_t>(ld) * B);
+        cudaStream_t st = nullptr;
+        FDS_CUDA(cudaMemcpy(dA.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+        for (int b = 0; b < B; ++b)
+            FDS_CUDA(cudaMemcpy(dr.p + static_cast<size_t>(b) * ld, rhs + static_cast<size_t>(b) * n,
+                                n * sizeof(cplx), cudaMemcpyHostToDevice));
+        LuProblem pb;
+        pb.A = dA.p;
+        pb.mstride = mstride;
+        pb.plane = plane;
+        pb.n = n;
+        pb.ld = ld;
+        pb.batch = B;
+        pb.ipiv = dp.p;
+        pb.info = di.p;
+        LuWorkspace ws;
+        lu_factor(pb, ws, st);
+        lu_solve(pb, dr.p, ld, st);
+        FDS_CUDA(cudaStreamSynchronize(st));
+        ws.release();
+        std::vector<int> info(B);
+        FDS_CUDA(cudaMemcpy(info.data(), di.p, B * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int b = 0; b < B; ++b)
+            if (info[b]) throw NumericError("zgesv: singular matrix");
+        for (int b = 0; b < B; ++b)
+            FDS_CUDA(cudaMemcpy(x + static_cast<size_t>(b) * n, dr.p + static_cast<size_t>(b) * ld, n * sizeof(cplx),
+                                cudaMemcpyDeviceToHost));
+    });
+}
+
+int fds_lu_factor_device(int n, int B, double* A_planar, int* ipiv, int* info, double* ms) {
+    return fds_guard([&] {
+        LuProblem pb;
+        pb.A = A_planar;
+        pb.plane = lu_plane(n);
+        pb.mstride = 2 * pb.plane;
+        pb.n = n;
+        pb.ld = lu_ld(n);
+        pb.batch = B;
+        pb.ipiv = ipiv;
+        pb.info = info;
+        static LuWorkspace ws;
+        cudaEvent_t e0, e1;
+        FDS_CUDA(cudaEventCreate(&e0));
+        FDS_CUDA(cudaEventCreate(&e1));
+        FDS_CUDA(cudaEventRecord(e0, nullptr));
+        lu_factor(pb, ws, nullptr);
+        FDS_CUDA(cudaEventRecord(e1, nullptr));
+        FDS_CUDA(cudaEventSynchronize(e1));
+        float t;
+        FDS_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        if (ms) *ms = t;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
+}  // extern "C"

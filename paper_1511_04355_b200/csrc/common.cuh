@@ -1,0 +1,81 @@
+// Shared device/host helpers for the fdsweep_b200 sm_100a library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "fdsweep_b200.h"
+
+namespace fdsb {
+
+// Error classes mirror proj/include/fdsweep/types.hpp:14-36; the C-ABI maps
+// each onto its FDS_E* status.
+struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ValidationError : Error { using Error::Error; };
+struct NumericError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct ConvergenceError : Error { using Error::Error; };
+struct CudaError : Error { using Error::Error; };
+
+extern std::atomic<int64_t> g_launches;
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define FDS_CUDA(x) ::fdsb::cuda_check((x), #x)
+// Every kernel launch of the library goes through this (launch accounting +
+// immediate launch-error check).
+#define FDS_LAUNCH(kernel, grid, block, smem, stream, ...)                        \
+    do {                                                                           \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);               \
+        ::fdsb::g_launches.fetch_add(1, std::memory_order_relaxed);               \
+        ::fdsb::cuda_check(cudaGetLastError(), #kernel);                           \
+    } while (0)
+
+// ---------------------------------------------------------------- complex
+struct cplx {
+    double re, im;
+};
+__host__ __device__ __forceinline__ cplx mk(double r, double i) { return {r, i}; }
+__host__ __device__ __forceinline__ cplx operator+(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+__host__ __device__ __forceinline__ cplx operator-(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+__host__ __device__ __forceinline__ cplx operator-(cplx a) { return {-a.re, -a.im}; }
+__host__ __device__ __forceinline__ cplx operator*(cplx a, cplx b) {
+    return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__host__ __device__ __forceinline__ cplx operator*(cplx a, double s) { return {a.re * s, a.im * s}; }
+__host__ __device__ __forceinline__ cplx operator*(double s, cplx a) { return {a.re * s, a.im * s}; }
+__host__ __device__ __forceinline__ cplx operator+(cplx a, double s) { return {a.re + s, a.im}; }
+__host__ __device__ __forceinline__ cplx conjg(cplx a) { return {a.re, -a.im}; }
+__host__ __device__ __forceinline__ double abs2(cplx a) { return a.re * a.re + a.im * a.im; }
+// Smith's algorithm (scaled), robust for the magnitudes met here.
+__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+    if (fabs(b.re) >= fabs(b.im)) {
+        const double r = b.im / b.re, d = b.re + b.im * r;
+        return {(a.re + a.im * r) / d, (a.im - a.re * r) / d};
+    }
+    const double r = b.re / b.im, d = b.re * r + b.im;
+    return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
+}
+__host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(mk(1.0, 0.0), b); }
+__device__ __forceinline__ cplx cexpd(cplx z) {
+    double s, c;
+    sincos(z.im, &s, &c);
+    const double e = exp(z.re);
+    return {e * c, e * s};
+}
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+struct DeviceInfo {
+    int device = 0;
+    int sms = 148;
+    size_t smem_optin = 227 * 1024;
+};
+const DeviceInfo& device_info();
+
+}  // namespace fdsb

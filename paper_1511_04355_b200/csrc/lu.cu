@@ -1,0 +1,653 @@
+// Right-looking blocked complex LU with partial pivoting, batched over
+// independent frequency systems, for sm_100a (FP64).
+//
+// The reference has no BEM/LU; this is the solve inside the new
+// FrequencySystem::evaluate (systems.hpp:34-42). Per panel step k (width w<=NB):
+//   lu_panel_kernel      cooperative grid: G groups x P CTAs, one group per
+//                        matrix (groups stride over the batch). The panel rows
+//                        [k,n) are split across the group's CTAs and kept in
+//                        shared memory for all w columns. One group barrier per
+//                        column: every CTA publishes its local |re|+|im| argmax
+//                        (LAPACK izamax rule, first max wins) with the full
+//                        candidate row; after the barrier each CTA picks the
+//                        winner, swaps/scales/updates its own rows.
+//   lu_swap_trsm_kernel  applies the panel's row swaps to the trailing columns
+//                        and solves U12 = L11^{-1} A12, 32-column strips in smem.
+//   lu_gemm_kernel       A22 -= L21 U12 as a complex GEMM on the FP64 tensor
+//                        pipe: four real mma.sync.m8n8k4.f64 (DMMA) products per
+//                        complex tile, 64x64 complex CTA tiles, cp.async
+//                        double-buffered smem, bank-conflict-free padded layouts.
+// Row swaps are LAPACK-style inside a panel and LINPACK-style across panels
+// (earlier L columns are not permuted); lu_solve applies them in that order.
+#include <climits>
+
+#include "lu.cuh"
+
+namespace fdsb {
+
+namespace {
+
+constexpr int kPanelThreads = 256;
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (ld_acquire(ctr) < target) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+}  // namespace
+
+template <int NB>
+__global__ void __launch_bounds__(kPanelThreads)
+lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batch, int k, int w,
+                int P, int R, int G, int* ipiv, int* info, double* slots, unsigned* counters) {
+    extern __shared__ double sm[];
+    double* tre = sm;             // [NB][R]
+    double* tim = tre + NB * R;   // [NB][R]
+    double* urow = tim + NB * R;  // [2NB]
+    double* drow = urow + 2 * NB; // [2NB]
+    __shared__ double red_v[kPanelThreads / 32];
+    __shared__ int red_i[kPanelThreads / 32];
+    __shared__ int s_piv;
+    __shared__ int s_win;
+    __shared__ double s_best;
+
+    const int g = blockIdx.x / P, p = blockIdx.x % P;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned* ctr = counters + g;
+    unsigned step = 0;
+    const size_t sstride = 2 + 2 * NB;
+    double* gslots = slots + static_cast<size_t>(g) * 2 * (P + 1) * sstride;
+
+    for (int b = g; b < batch; b += G) {
+        double* Are = A + static_cast<size_t>(b) * mstride;
+        double* Aim = Are + plane;
+        const int r0 = k + p * R;
+        const int r1 = min(r0 + R, n);
+        const int nr = max(0, r1 - r0);
+        for (int idx = tid; idx < w * R; idx += kPanelThreads) {
+            const int j = idx / R, i = idx % R;
+            if (i < nr) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + r0 + i;
+                tre[j * R + i] = Are[gi];
+                tim[j * R + i] = Aim[gi];
+            }
+        }
+        __syncthreads();
+        for (int j = 0; j < w; ++j) {
+            const int c = k + j;
+            // (a) local argmax of |re|+|im| over own rows >= c
+            double best = -1.0;
+            int bi = INT_MAX;
+            for (int i = tid; i < nr; i += kPanelThreads) {
+                const int gr = r0 + i;
+                if (gr >= c) {
+                    const double v = fabs(tre[j * R + i]) + fabs(tim[j * R + i]);
+                    if (v > best) { best = v; bi = gr; }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+            }
+            if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+            __syncthreads();
+            if (tid == 0) {
+                for (int q = 1; q < kPanelThreads / 32; ++q)
+                    if (red_v[q] > red_v[0] || (red_v[q] == red_v[0] && red_i[q] < red_i[0])) {
+                        red_v[0] = red_v[q];
+                        red_i[0] = red_i[q];
+                    }
+            }
+            __syncthreads();
+            const int par = step & 1;
+            double* myslot = gslots + (static_cast<size_t>(par) * (P + 1) + p) * sstride;
+            double* dslot = gslots + (static_cast<size_t>(par) * (P + 1) + P) * sstride;
+            const int lbi = red_i[0];
+            if (tid == 0) { myslot[0] = red_v[0]; myslot[1] = static_cast<double>(lbi); }
+            if (lbi != INT_MAX) {
+                const int li = lbi - r0;
+                for (int jj = tid; jj < 2 * NB; jj += kPanelThreads) {
+                    const int col = jj % NB;
+                    myslot[2 + jj] = col < w ? (jj < NB ? tre[col * R + li] : tim[col * R + li]) : 0.0;
+                }
+            }
+            if (c >= r0 && c < r1) {
+                const int li = c - r0;
+                for (int jj = tid; jj < 2 * NB; jj += kPanelThreads) {
+                    const int col = jj % NB;
+                    dslot[2 + jj] = col < w ? (jj < NB ? tre[col * R + li] : tim[col * R + li]) : 0.0;
+                }
+            }
+            ++step;
+            group_barrier(ctr, step * static_cast<unsigned>(P));
+            // (b) winner among the P candidates
+            if (wid == 0) {
+                double bv = -1.0;
+                int bidx = INT_MAX, bw = -1;
+                for (int q = lane; q < P; q += 32) {
+                    const double* sl = gslots + (static_cast<size_t>(par) * (P + 1) + q) * sstride;
+                    const double v = __ldcg(sl);
+                    const int ri = static_cast<int>(__ldcg(sl + 1));
+                    if (v > bv || (v == bv && ri < bidx)) { bv = v; bidx = ri; bw = q; }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+                    const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+                    if (ov > bv || (ov == bv && oi < bidx)) { bv = ov; bidx = oi; bw = ow; }
+                }
+                if (lane == 0) { s_piv = bidx; s_win = bw; s_best = bv; }
+            }
+            __syncthreads();
+            const int piv = s_piv;
+            {
+                const double* ws = gslots + (static_cast<size_t>(par) * (P + 1) + s_win) * sstride;
+                for (int jj = tid; jj < 2 * NB; jj += kPanelThreads) {
+                    urow[jj] = __ldcg(ws + 2 + jj);
+                    drow[jj] = __ldcg(dslot + 2 + jj);
+                }
+            }
+            if (p == 0 && tid == 0) {
+                ipiv[static_cast<size_t>(b) * n + c] = piv;
+                if (!(s_best > 0.0) && info[b] == 0) info[b] = c + 1;
+            }
+            __syncthreads();
+            // (c) swap rows c <-> piv inside the panel tile
+            if (piv != c) {
+                if (c >= r0 && c < r1)
+                    for (int jj = tid; jj < w; jj += kPanelThreads) {
+                        tre[jj * R + (c - r0)] = urow[jj];
+                        tim[jj * R + (c - r0)] = urow[NB + jj];
+                    }
+                if (piv >= r0 && piv < r1)
+                    for (int jj = tid; jj < w; jj += kPanelThreads) {
+                        tre[jj * R + (piv - r0)] = drow[jj];
+                        tim[jj * R + (piv - r0)] = drow[NB + jj];
+                    }
+            }
+            __syncthreads();
+            // (d) scale column j below the diagonal, then rank-1 update of the panel
+            const cplx u = mk(urow[j], urow[NB + j]);
+            if (u.re != 0.0 || u.im != 0.0) {
+                const cplx inv = crecip(u);
+                for (int i = tid; i < nr; i += kPanelThreads) {
+                    if (r0 + i > c) {
+                        const cplx l = mk(tre[j * R + i], tim[j * R + i]) * inv;
+                        tre[j * R + i] = l.re;
+                        tim[j * R + i] = l.im;
+                    }
+                }
+            }
+            __syncthreads();
+            const int cols = w - j - 1;
+            if (cols > 0) {
+                for (int idx = tid; idx < cols * nr; idx += kPanelThreads) {
+                    const int jj = j + 1 + idx / nr, i = idx % nr;
+                    if (r0 + i > c) {
+                        const double lr = tre[j * R + i], li = tim[j * R + i];
+                        const double ur = urow[jj], ui = urow[NB + jj];
+                        tre[jj * R + i] -= lr * ur - li * ui;
+                        tim[jj * R + i] -= lr * ui + li * ur;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        for (int idx = tid; idx < w * R; idx += kPanelThreads) {
+            const int j = idx / R, i = idx % R;
+            if (i < nr) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + r0 + i;
+                Are[gi] = tre[j * R + i];
+                Aim[gi] = tim[j * R + i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ swaps + TRSM
+constexpr int kTrsmCols = 32;
+
+template <int NB>
+__global__ void __launch_bounds__(256)
+lu_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w,
+                    const int* ipiv) {
+    extern __shared__ double sm[];
+    double* Lre = sm;                    // [NB][NB], L[j*NB+i]
+    double* Lim = Lre + NB * NB;
+    double* Xre = Lim + NB * NB;         // [kTrsmCols][NB], X[t*NB+i]
+    double* Xim = Xre + kTrsmCols * NB;
+    const int b = blockIdx.y;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int col0 = k + w + blockIdx.x * kTrsmCols;
+    const int ncols = min(kTrsmCols, n - col0);
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < w * w; idx += blockDim.x) {
+        const int j = idx / w, i = idx % w;
+        const size_t gi = static_cast<size_t>(k + j) * ld + k + i;
+        Lre[j * NB + i] = Are[gi];
+        Lim[j * NB + i] = Aim[gi];
+    }
+    for (int idx = tid; idx < ncols * w; idx += blockDim.x) {
+        const int t = idx / w, i = idx % w;
+        const size_t gi = static_cast<size_t>(col0 + t) * ld + k + i;
+        Xre[t * NB + i] = Are[gi];
+        Xim[t * NB + i] = Aim[gi];
+    }
+    __syncthreads();
+    if (tid < ncols) {
+        const size_t colbase = static_cast<size_t>(col0 + tid) * ld;
+        const int* pv = ipiv + static_cast<size_t>(b) * n;
+        for (int c = k; c < k + w; ++c) {
+            const int r = pv[c];
+            if (r == c) continue;
+            const int lc = c - k;
+            if (r < k + w) {
+                const int lr = r - k;
+                double t0 = Xre[tid * NB + lc], t1 = Xim[tid * NB + lc];
+                Xre[tid * NB + lc] = Xre[tid * NB + lr];
+                Xim[tid * NB + lc] = Xim[tid * NB + lr];
+                Xre[tid * NB + lr] = t0;
+                Xim[tid * NB + lr] = t1;
+            } else {
+                const double gr = Are[colbase + r], gi = Aim[colbase + r];
+                Are[colbase + r] = Xre[tid * NB + lc];
+                Aim[colbase + r] = Xim[tid * NB + lc];
+                Xre[tid * NB + lc] = gr;
+                Xim[tid * NB + lc] = gi;
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = 0; j < w - 1; ++j) {
+        const int rows = w - j - 1;
+        for (int idx = tid; idx < ncols * rows; idx += blockDim.x) {
+            const int t = idx / rows, i = j + 1 + idx % rows;
+            const double lr = Lre[j * NB + i], li = Lim[j * NB + i];
+            const double xr = Xre[t * NB + j], xi = Xim[t * NB + j];
+            Xre[t * NB + i] -= lr * xr - li * xi;
+            Xim[t * NB + i] -= lr * xi + li * xr;
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < ncols * w; idx += blockDim.x) {
+        const int t = idx / w, i = idx % w;
+        const size_t gi = static_cast<size_t>(col0 + t) * ld + k + i;
+        Are[gi] = Xre[t * NB + i];
+        Aim[gi] = Xim[t * NB + i];
+    }
+}
+
+// ------------------------------------------------------------------ DMMA GEMM
+constexpr int GBM = 64, GBN = 64, GBK = 16, GSTAGES = 2;
+constexpr int GAS = GBM + 4;  // A tile row stride (doubles) ≡ 4 (mod 16): conflict-free fragments
+constexpr int GBS = GBK + 4;  // B tile row stride
+constexpr int kGemmThreads = 128;
+constexpr int kGemmSmemDoubles = GSTAGES * 2 * (GBK * GAS + GBN * GBS);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 2)
+lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w) {
+    extern __shared__ __align__(16) double gsm[];
+    const int b = blockIdx.z;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int m0 = k + w + blockIdx.x * GBM;  // first row of this tile
+    const int n0 = k + w + blockIdx.y * GBN;  // first column
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    auto As = [&](int st, int pl) { return gsm + (st * 2 + pl) * (GBK * GAS); };
+    auto Bs = [&](int st, int pl) { return gsm + GSTAGES * 2 * (GBK * GAS) + (st * 2 + pl) * (GBN * GBS); };
+
+    auto load_stage = [&](int st, int kc) {
+        const int kk0 = kc * GBK;
+        // A tile: L21[m0..m0+64)[k+kk0 .. +16): per (plane, kk) 64 contiguous doubles = 32 chunks
+        for (int q = tid; q < 2 * GBK * (GBM / 2); q += kGemmThreads) {
+            const int pl = q / (GBK * (GBM / 2));
+            const int rem = q % (GBK * (GBM / 2));
+            const int kk = rem / (GBM / 2), ch = rem % (GBM / 2);
+            const double* src = (pl ? Aim : Are) + static_cast<size_t>(k + kk0 + kk) * ld + m0 + 2 * ch;
+            const int bytes = (kk0 + kk < w) ? 16 : 0;
+            cp_async16(As(st, pl) + kk * GAS + 2 * ch, bytes ? src : Are, bytes);
+        }
+        // B tile: U12[k+kk0 .. +16)[n0..n0+64): per (plane, column) 16 contiguous doubles = 8 chunks
+        for (int q = tid; q < 2 * GBN * (GBK / 2); q += kGemmThreads) {
+            const int pl = q / (GBN * (GBK / 2));
+            const int rem = q % (GBN * (GBK / 2));
+            const int nn = rem / (GBK / 2), ch = rem % (GBK / 2);
+            const int kk = kk0 + 2 * ch;
+            const double* src = (pl ? Aim : Are) + static_cast<size_t>(n0 + nn) * ld + k + kk;
+            const int bytes = kk + 2 <= w ? 16 : (kk < w ? 8 : 0);
+            cp_async16(Bs(st, pl) + nn * GBS + 2 * ch, bytes ? src : Are, bytes);
+        }
+    };
+
+    double acr[4][4][2], aci[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acr[i][j][0] = acr[i][j][1] = 0.0;
+            aci[i][j][0] = aci[i][j][1] = 0.0;
+        }
+
+    const int nk = (w + GBK - 1) / GBK;
+    load_stage(0, 0);
+    cp_async_commit();
+    for (int kc = 0; kc < nk; ++kc) {
+        if (kc + 1 < nk) load_stage((kc + 1) % GSTAGES, kc + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const int st = kc % GSTAGES;
+        const double* ar = As(st, 0);
+        const double* ai = As(st, 1);
+        const double* br = Bs(st, 0);
+        const double* bi = Bs(st, 1);
+#pragma unroll
+        for (int k4 = 0; k4 < GBK; k4 += 4) {
+            double fa_r[4], fa_i[4], fa_n[4], fb_r[4], fb_i[4];
+            const int kr = k4 + (lane & 3);
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const int m = wm * 32 + mi * 8 + (lane >> 2);
+                fa_r[mi] = ar[kr * GAS + m];
+                fa_i[mi] = ai[kr * GAS + m];
+                fa_n[mi] = -fa_i[mi];
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int nn = wn * 32 + ni * 8 + (lane >> 2);
+                fb_r[ni] = br[nn * GBS + kr];
+                fb_i[ni] = bi[nn * GBS + kr];
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {
+                    dmma(acr[mi][ni][0], acr[mi][ni][1], fa_r[mi], fb_r[ni]);
+                    dmma(aci[mi][ni][0], aci[mi][ni][1], fa_r[mi], fb_i[ni]);
+                    dmma(acr[mi][ni][0], acr[mi][ni][1], fa_n[mi], fb_i[ni]);
+                    dmma(aci[mi][ni][0], aci[mi][ni][1], fa_i[mi], fb_r[ni]);
+                }
+        }
+        __syncthreads();
+    }
+    // epilogue: C -= acc
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int row = m0 + wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+                if (row < n && col < n) {
+                    const size_t gi = static_cast<size_t>(col) * ld + row;
+                    Are[gi] -= acr[mi][ni][e];
+                    Aim[gi] -= aci[mi][ni][e];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ solves
+__global__ void lu_fwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld,
+                                    int k, int w, const int* ipiv, cplx* rhs, size_t rstride) {
+    __shared__ cplx y[64];
+    const int b = blockIdx.x;
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    cplx* x = rhs + static_cast<size_t>(b) * rstride;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        const int* pv = ipiv + static_cast<size_t>(b) * n;
+        for (int c = k; c < k + w; ++c) {
+            const int r = pv[c];
+            if (r != c) { const cplx t = x[c]; x[c] = x[r]; x[r] = t; }
+        }
+    }
+    __syncthreads();
+    if (tid < w) y[tid] = x[k + tid];
+    __syncthreads();
+    for (int j = 0; j < w - 1; ++j) {
+        if (tid > j && tid < w) {
+            const size_t gi = static_cast<size_t>(k + j) * ld + k + tid;
+            y[tid] = y[tid] - mk(Are[gi], Aim[gi]) * y[j];
+        }
+        __syncthreads();
+    }
+    if (tid < w) x[k + tid] = y[tid];
+}
+
+__global__ void lu_fwd_gemv_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k,
+                                   int w, cplx* rhs, size_t rstride) {
+    __shared__ cplx y[64];
+    const int b = blockIdx.y;
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    cplx* x = rhs + static_cast<size_t>(b) * rstride;
+    if (threadIdx.x < w) y[threadIdx.x] = x[k + threadIdx.x];
+    __syncthreads();
+    const int r = k + w + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    cplx acc = mk(0.0, 0.0);
+    for (int j = 0; j < w; ++j) {
+        const size_t gi = static_cast<size_t>(k + j) * ld + r;
+        acc = acc + mk(Are[gi], Aim[gi]) * y[j];
+    }
+    x[r] = x[r] - acc;
+}
+
+__global__ void lu_bwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld,
+                                    int k, int w, cplx* rhs, size_t rstride) {
+    __shared__ cplx y[64];
+    const int b = blockIdx.x;
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    cplx* x = rhs + static_cast<size_t>(b) * rstride;
+    const int tid = threadIdx.x;
+    if (tid < w) y[tid] = x[k + tid];
+    __syncthreads();
+    for (int j = w - 1; j >= 0; --j) {
+        if (tid == j) {
+            const size_t gi = static_cast<size_t>(k + j) * ld + k + j;
+            y[j] = cdiv(y[j], mk(Are[gi], Aim[gi]));
+        }
+        __syncthreads();
+        if (tid < j) {
+            const size_t gi = static_cast<size_t>(k + j) * ld + k + tid;
+            y[tid] = y[tid] - mk(Are[gi], Aim[gi]) * y[j];
+        }
+        __syncthreads();
+    }
+    if (tid < w) x[k + tid] = y[tid];
+}
+
+__global__ void lu_bwd_gemv_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k,
+                                   int w, cplx* rhs, size_t rstride) {
+    __shared__ cplx y[64];
+    const int b = blockIdx.y;
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    cplx* x = rhs + static_cast<size_t>(b) * rstride;
+    if (threadIdx.x < w) y[threadIdx.x] = x[k + threadIdx.x];
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= k) return;
+    cplx acc = mk(0.0, 0.0);
+    for (int j = 0; j < w; ++j) {
+        const size_t gi = static_cast<size_t>(k + j) * ld + r;
+        acc = acc + mk(Are[gi], Aim[gi]) * y[j];
+    }
+    x[r] = x[r] - acc;
+}
+
+// ------------------------------------------------------------------ host
+void LuWorkspace::ensure(int groups, int P, int nb) {
+    const size_t need = static_cast<size_t>(groups) * 2 * (P + 1) * (2 + 2 * nb) * sizeof(double);
+    if (need > slot_bytes) {
+        if (slots) cudaFree(slots);
+        FDS_CUDA(cudaMalloc(&slots, need));
+        slot_bytes = need;
+    }
+    if (groups > counter_count) {
+        if (counters) cudaFree(counters);
+        FDS_CUDA(cudaMalloc(&counters, groups * sizeof(unsigned)));
+        counter_count = groups;
+    }
+}
+
+void LuWorkspace::release() {
+    if (slots) cudaFree(slots);
+    if (counters) cudaFree(counters);
+    slots = nullptr;
+    counters = nullptr;
+    slot_bytes = 0;
+    counter_count = 0;
+}
+
+namespace {
+
+size_t panel_smem(int nb, int R) { return (2 * static_cast<size_t>(nb) * R + 4 * nb) * sizeof(double); }
+
+template <int NB>
+int panel_rows_max() {
+    const size_t budget = device_info().smem_optin - 8 * 1024;
+    return static_cast<int>((budget / sizeof(double) - 4 * NB) / (2 * NB));
+}
+
+template <int NB>
+void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t st) {
+    const int sms = device_info().sms;
+    const int rows = pb.n - k;
+    const int rmax = panel_rows_max<NB>();
+    int P = ceil_div(rows, rmax);
+    if (P > sms) throw NumericError("lu: panel does not fit in on-chip memory");
+    const int R = ceil_div(rows, P);
+    const int G = std::max(1, std::min(pb.batch, sms / P));
+    const size_t smem = panel_smem(NB, R);
+    static size_t attr_smem = 0;
+    if (smem > attr_smem) {
+        FDS_CUDA(cudaFuncSetAttribute(lu_panel_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr_smem = smem;
+    }
+    ws.ensure(G, P, NB);
+    FDS_CUDA(cudaMemsetAsync(ws.counters, 0, G * sizeof(unsigned), st));
+    double* A = pb.A;
+    size_t mstride = pb.mstride, plane = pb.plane;
+    int n = pb.n, ld = pb.ld, batch = pb.batch;
+    int* ipiv = pb.ipiv;
+    int* info = pb.info;
+    double* slots = ws.slots;
+    unsigned* counters = ws.counters;
+    int kk = k, ww = w, PP = P, RR = R, GG = G;
+    void* args[] = {&A, &mstride, &plane, &n, &ld, &batch, &kk, &ww, &PP, &RR, &GG, &ipiv, &info, &slots, &counters};
+    FDS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_panel_kernel<NB>), dim3(G * P),
+                                         dim3(kPanelThreads), args, smem, st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <int NB>
+void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
+    const int rest = pb.n - k - w;
+    if (rest <= 0) return;
+    static bool attr_set = false;
+    const size_t smem = (2 * NB * NB + 2 * kTrsmCols * NB) * sizeof(double);
+    if (!attr_set) {
+        FDS_CUDA(cudaFuncSetAttribute(lu_swap_trsm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        FDS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kGemmSmemDoubles * sizeof(double))));
+        attr_set = true;
+    }
+    dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
+    FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, 256, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
+               pb.ipiv);
+    dim3 gg(ceil_div(rest, GBM), ceil_div(rest, GBN), pb.batch);
+    FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
+               pb.plane, pb.n, pb.ld, k, w);
+}
+
+}  // namespace
+
+int lu_panel_width(int n) {
+    // NB = 64 unless the 64-wide panel of one matrix cannot live in the SMs' shared memory.
+    const int sms = device_info().sms;
+    return ceil_div(n, panel_rows_max<64>()) <= sms ? 64 : 32;
+}
+
+void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
+    FDS_CUDA(cudaMemsetAsync(pb.info, 0, pb.batch * sizeof(int), st));
+    const int nb = lu_panel_width(pb.n);
+    for (int k = 0; k < pb.n; k += nb) {
+        const int w = std::min(nb, pb.n - k);
+        if (nb == 64) {
+            panel_step<64>(pb, ws, k, w, st);
+            trailing_step<64>(pb, k, w, st);
+        } else {
+            panel_step<32>(pb, ws, k, w, st);
+            trailing_step<32>(pb, k, w, st);
+        }
+    }
+}
+
+void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st) {
+    const int nb = lu_panel_width(pb.n);
+    for (int k = 0; k < pb.n; k += nb) {
+        const int w = std::min(nb, pb.n - k);
+        FDS_LAUNCH(lu_fwd_panel_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
+                   pb.ipiv, rhs, rstride);
+        const int rest = pb.n - k - w;
+        if (rest > 0) {
+            dim3 g(ceil_div(rest, 128), pb.batch);
+            FDS_LAUNCH(lu_fwd_gemv_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, rhs,
+                       rstride);
+        }
+    }
+    const int last = ((pb.n - 1) / nb) * nb;
+    for (int k = last; k >= 0; k -= nb) {
+        const int w = std::min(nb, pb.n - k);
+        FDS_LAUNCH(lu_bwd_panel_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
+                   rhs, rstride);
+        if (k > 0) {
+            dim3 g(ceil_div(k, 128), pb.batch);
+            FDS_LAUNCH(lu_bwd_gemv_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, rhs,
+                       rstride);
+        }
+    }
+}
+
+}  // namespace fdsb

@@ -1,0 +1,39 @@
+// Batched / blocked complex LU with partial pivoting on sm_100a.
+#pragma once
+
+#include "common.cuh"
+
+namespace fdsb {
+
+// B matrices of order n, planar FP64 (re plane then im plane, each ld x ld,
+// column-major); matrix b starts at A + b*mstride, im plane at +plane.
+struct LuProblem {
+    double* A = nullptr;
+    size_t mstride = 0;
+    size_t plane = 0;
+    int n = 0;
+    int ld = 0;
+    int batch = 0;
+    int* ipiv = nullptr;  // [batch][n], 0-based row swapped with row c at step c
+    int* info = nullptr;  // [batch], 0 = ok, c+1 = first zero pivot
+};
+
+struct LuWorkspace {
+    double* slots = nullptr;
+    unsigned* counters = nullptr;
+    size_t slot_bytes = 0;
+    int counter_count = 0;
+    void ensure(int groups, int P, int nb);
+    void release();
+};
+
+inline int lu_ld(int n) { return (n + 63) / 64 * 64; }
+inline size_t lu_plane(int n) { return static_cast<size_t>(lu_ld(n)) * lu_ld(n); }
+
+// Per-step timings are not taken here; the caller brackets with events.
+void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st);
+// rhs[b*rstride + i], complex interleaved, overwritten with the solution.
+void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st);
+int lu_panel_width(int n);
+
+}  // namespace fdsb
