@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 BEM / VF / FSM hot path (BASELINE.json metric).
+
+Headline workload (configs[1]): spherical cavity, 1280-triangle icosphere
+(N = 3840 unknowns), Heaviside pressure, the full FSM contour of T = 20,
+N_s = 256 (N_c = N_s/2 + 1 = 129 frequencies, s_k = 5/T + i k 2π/T) solved as one
+batch of independent dense systems; displacement at 16 collocation points
+(48 DOFs). One step = assembly + batched LU + solve of all 129 systems.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun (N > 1) every rank solves its own 129-frequency sweep (replicas
+only: the path has no exchange step), the step time is the max
+over ranks, and value = total solves / time ("scaling": "weak").
+``--impl reference`` times the CPU oracle port of the same path (OpenMP
+assembly + OpenBLAS zgetrf on all host cores) — the reference has no BEM.
+"""
+from __future__ import annotations
+
+import argparse
+import faulthandler
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BEM frequency solves/sec (assembly+LU)"
+UNIT = "solves/s"
+T_PERIOD, NS = 20.0, 256
+ETA = 5.0 / T_PERIOD
+
+
+def cfg2_inputs():
+    from paper_1511_04355_b200 import mesh
+
+    V, F = mesh.icosphere(3)
+    tr = mesh.pressure_traction(V, F)
+    pts = mesh.draw_indices(F.shape[0], 16, 0)
+    dofs = [3 * p + i for p in pts for i in range(3)]
+    nc = NS // 2 + 1
+    s = ETA + 1j * (2 * math.pi / T_PERIOD) * np.arange(nc)
+    return V, F, tr, dofs, s
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, parts[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_fp64_peak():
+    p = ROOT / "profiles" / "r01_fp64_peak.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["fp64_peak_tflops"]), "measured (profiles/r01_fp64_peak.json: DMMA microbench / cuBLAS ZGEMM)"
+    except Exception:
+        return 36.9, "fallback (B200 FP64 datasheet class)"
+
+
+def ncu_traffic(kernel: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(kernel)
+    except Exception:
+        return None
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local, dist
+
+
+def allreduce_max(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_oracle_solves(n_freq: int, warm: int = 0):
+    """Oracle port: OpenMP assembly + OpenBLAS zgetrf/zgetrs, all host cores."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as O
+
+    V, F, tr, dofs, s = cfg2_inputs()
+    bem = O.Bem(V, F, tr)
+    ob = O.openblas_path()
+    for i in range(warm):
+        bem.solve_openblas(s[1 + i], ob)
+    t0 = time.perf_counter()
+    for i in range(n_freq):
+        bem.solve_openblas(s[1 + (i % (len(s) - 1))], ob)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    per = []
+    cpu_oracle_solves(0, warm=min(args.warmup, 1))
+    for _ in range(args.steps):
+        per.append(cpu_oracle_solves(1))
+    dt = float(np.mean(per))
+    v = 1.0 / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": "cfg2 sphere 1280 tri N=3840, one FSM frequency per step (bounded CPU sample)",
+                   "sample": "1 frequency solve per step"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": "oracle BEM (OpenMP assembly) + OpenBLAS zgetrf/zgetrs, 1 frequency of cfg2 per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_ours(args, world, rank, local, dist):
+    import paper_1511_04355_b200 as P
+    from paper_1511_04355_b200 import BemSystem
+
+    L = P.lib()
+    P.api._check(L.fds_set_device(local))
+    V, F, tr, dofs, s = cfg2_inputs()
+    B = len(s)
+    sysb = BemSystem(V, F, tr, channels=dofs, max_batch=B)
+    for _ in range(args.warmup):
+        sysb.evaluate_batch_device(s)
+    barrier(dist)
+    launches0 = P.kernel_launches()
+    dev_ms = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            sysb.evaluate_batch_device(s)
+            t = sysb.last_timing()
+            dev_ms.append(t["assembly_ms"] + t["lu_ms"] + t["solve_ms"])
+        wall = time.perf_counter() - t0
+    launches = (P.kernel_launches() - launches0) // args.steps
+    stage = sysb.last_timing()
+    total_ms = allreduce_max(dist, float(np.sum(dev_ms)))
+    ms_step = total_ms / args.steps
+    value = B * world / (ms_step * 1e-3)
+
+    # end to end through the public C-ABI with host buffers (H2D s, D2H values)
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sysb.evaluate_batch(s)
+    e2e_s = allreduce_max(dist, time.perf_counter() - t0) / args.steps
+    e2e = {"value": B * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * B,
+           "d2h_bytes_per_step": 16 * B * len(dofs)}
+
+    # roofline of the dominant kernel (LU trailing GEMM on the FP64 tensor pipe)
+    P.api._check(L.fds_profile_enable(1))
+    sysb.evaluate_batch_device(s)
+    import ctypes
+
+    c, ms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    P.api._check(L.fds_profile_read(0, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
+    gemm = dict(launches=c.value, ms=ms.value, flops=wk.value)
+    P.api._check(L.fds_profile_read(1, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
+    panel = dict(launches=c.value, ms=ms.value)
+    P.api._check(L.fds_profile_read(2, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
+    trsm = dict(launches=c.value, ms=ms.value)
+    P.api._check(L.fds_profile_enable(0))
+    peak, peak_src = measured_fp64_peak()
+    achieved = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
+    traffic = ncu_traffic("lu_gemm_kernel")
+    n = 3 * F.shape[0]
+    lu_flops = B * 8.0 * n ** 3 / 3.0
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic",
+        "config": {"workload": "cfg2: sphere cavity, 1280-tri icosphere, N=3840, 129-frequency FSM batch "
+                               "(T=20, Ns=256, eta=5/T), 16 collocation points",
+                   "global_batch": B * world, "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2 (129 x 236 MB matrices)"},
+        "e2e": e2e,
+        "roofline": {"bound": "tensor", "kernel": "lu_gemm_kernel (DMMA complex GEMM)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+                     "peak_source": peak_src, "traffic": traffic,
+                     "work_def": "8*rest^2*w FP64 flops per launch (A22 -= L21 U12)",
+                     "share_of_lu": gemm["ms"] / max(gemm["ms"] + panel["ms"] + trsm["ms"], 1e-9)},
+        "stages_ms": {"assembly": stage["assembly_ms"], "lu": stage["lu_ms"], "solve": stage["solve_ms"],
+                      "lu_panel": panel["ms"], "lu_trsm": trsm["ms"], "lu_gemm": gemm["ms"]},
+        "lu_tflops": lu_flops / (stage["lu_ms"] * 1e-3) / 1e12,
+        "wall_ms_per_step": wall * 1e3 / args.steps,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    sysb.close()
+    if rank == 0 and world == 1 and not args.no_extra:
+        result["extra"] = extra_configs(args)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ncpu = 2
+        dt = cpu_oracle_solves(ncpu, warm=1)
+        result["cpu_baseline"] = {"value": ncpu / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                  "sample": f"{ncpu} frequencies of cfg2 (N=3840): oracle BEM assembly (OpenMP) "
+                                            "+ OpenBLAS zgetrf/zgetrs"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def extra_configs(args):
+    """Secondary measurements (not the headline): cfg4 single N=15360 solve."""
+    from paper_1511_04355_b200 import BemSystem, mesh
+
+    out = {}
+    try:
+        V, F = mesh.icosphere(4)
+        tr = mesh.random_traction(F.shape[0], seed=0)
+        sysb = BemSystem(V, F, tr, channels=list(range(48)), max_batch=1)
+        s = np.array([0.25 + 1j * 2 * math.pi / 20.0])
+        sysb.evaluate_batch_device(s)
+        sysb.evaluate_batch_device(s)
+        t = sysb.last_timing()
+        n = 3 * F.shape[0]
+        out["cfg4_N15360_single_solve"] = {**{k: v for k, v in t.items()},
+                                           "lu_tflops": 8.0 * n ** 3 / 3 / (t["lu_ms"] * 1e-3) / 1e12}
+        sysb.close()
+    except Exception as e:  # noqa: BLE001
+        out["cfg4_error"] = repr(e)
+    return out
+
+
+def main():
+    faulthandler.enable()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

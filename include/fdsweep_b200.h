@@ -194,6 +194,13 @@ int fds_run_afs_callback(fds_system_fn fn, void* user, int channels, const fds_a
 
 /* Count of kernels this library launched since load (evidence for the bench). */
 int64_t fds_kernel_launches(void);
+/* Per-kernel device timing for roofline reporting. enable(1) clears and starts
+ * recording (CUDA events around each launch of the profiled kernels on their
+ * own stream); read() sums launches of one kind: 0 LU GEMM (work = FP64 flops),
+ * 1 LU panel, 2 LU swap+TRSM, 3 assembly far field, 4 assembly near field,
+ * 5 VF residue apply (work = bytes), 6 rational invert, 7 FSM, 8 channel errors. */
+int fds_profile_enable(int on);
+int fds_profile_read(int kind, int* count, double* total_ms, double* total_work);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

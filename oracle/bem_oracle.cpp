@@ -192,6 +192,7 @@ BemOracle::BemOracle(const std::vector<double>& vertices, const std::vector<int>
         g[15] = 0.5 * twice;
     }
     ne_ = ne;
+    gauss_legendre01(kSelfGauss, glx_, glw_);  // built once here: assemble() is OpenMP-parallel
 }
 
 namespace {
@@ -240,8 +241,8 @@ int subdivision_level(double d, double h) {
 
 // Self-element integrals (polar quadrature about the centroid).
 void BemOracle::self_block(int e, C s, C Ui[9], C Ti[9]) const {
-    static std::vector<double> gx, gw;
-    if (gx.empty()) gauss_legendre01(kSelfGauss, gx, gw);
+    const std::vector<double>& gx = glx_;
+    const std::vector<double>& gw = glw_;
     const Elem el = elem_of(&geo_[static_cast<size_t>(e) * 16]);
     const double n[3] = {el.n.x, el.n.y, el.n.z};
     for (int i = 0; i < 9; ++i) Ui[i] = Ti[i] = C(0.0, 0.0);

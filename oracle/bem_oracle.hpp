@@ -39,6 +39,7 @@ class BemOracle {
   private:
     KernelCoeffs kc_;
     std::vector<double> traction_;
+    std::vector<double> glx_, glw_;  // self-element Gauss–Legendre rule on [0,1]
     std::vector<double> geo_;  // per element: v0,v1,v2 (9), centroid (3), normal (3), area
     int ne_ = 0;
 };

@@ -35,6 +35,26 @@ const DeviceInfo& device_info() {
 
 thread_local std::string g_error;
 
+KernelProfile& profiler() {
+    static KernelProfile p;
+    return p;
+}
+
+void KernelProfile::begin(cudaStream_t st, int, double, cudaEvent_t& a) {
+    a = nullptr;
+    if (!enabled) return;
+    FDS_CUDA(cudaEventCreate(&a));
+    FDS_CUDA(cudaEventRecord(a, st));
+}
+
+void KernelProfile::end(cudaStream_t st, cudaEvent_t a, int kind, double work) {
+    if (!enabled || !a) return;
+    cudaEvent_t b;
+    FDS_CUDA(cudaEventCreate(&b));
+    FDS_CUDA(cudaEventRecord(b, st));
+    recs.push_back({a, b, work, kind});
+}
+
 __global__ void gather_channels_kernel(const cplx* __restrict__ rhs, size_t rstride, const int* __restrict__ ch,
                                        int K, int B, cplx* __restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,6 +162,35 @@ extern "C" {
 const char* fds_last_error(void) { return g_error.c_str(); }
 const char* fds_version(void) { return "fdsweep_b200 0.1.0 sm_100a"; }
 int64_t fds_kernel_launches(void) { return g_launches.load(); }
+
+int fds_profile_enable(int on) {
+    return fds_guard([&] {
+        auto& p = profiler();
+        for (auto& r : p.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+        p.recs.clear();
+        p.enabled = on != 0;
+    });
+}
+
+int fds_profile_read(int kind, int* count, double* total_ms, double* total_work) {
+    return fds_guard([&] {
+        auto& p = profiler();
+        int c = 0;
+        double ms = 0, w = 0;
+        for (auto& r : p.recs) {
+            if (r.kind != kind) continue;
+            FDS_CUDA(cudaEventSynchronize(r.b));
+            float t;
+            FDS_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            ++c;
+            ms += t;
+            w += r.work;
+        }
+        if (count) *count = c;
+        if (total_ms) *total_ms = ms;
+        if (total_work) *total_work = w;
+    });
+}
 
 int fds_set_device(int device) {
     return fds_guard([&] { FDS_CUDA(cudaSetDevice(device)); });

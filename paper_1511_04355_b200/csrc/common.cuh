@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "fdsweep_b200.h"
 
@@ -70,6 +71,20 @@ __device__ __forceinline__ cplx cexpd(cplx z) {
 }
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Optional per-kernel timing (bench roofline): when enabled, selected launches
+// are bracketed by CUDA events on their stream; totals are read back with
+// fds_profile_read(). Disabled by default (zero overhead).
+struct KernelProfile {
+    bool enabled = false;
+    struct Rec { cudaEvent_t a, b; double work; int kind; };
+    std::vector<Rec> recs;
+    void begin(cudaStream_t st, int kind, double work, cudaEvent_t& a);
+    void end(cudaStream_t st, cudaEvent_t a, int kind, double work);
+};
+KernelProfile& profiler();
+enum ProfKind { kProfLuGemm = 0, kProfLuPanel = 1, kProfLuTrsm = 2, kProfAsmFar = 3, kProfAsmNear = 4,
+                kProfVfResidue = 5, kProfRatInv = 6, kProfFsm = 7, kProfChanErr = 8, kProfCount = 9 };
 
 struct DeviceInfo {
     int device = 0;

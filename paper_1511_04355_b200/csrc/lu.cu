@@ -53,15 +53,17 @@ template <int NB>
 __global__ void __launch_bounds__(kPanelThreads)
 lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batch, int k, int w,
                 int P, int R, int G, int* ipiv, int* info, double* slots, unsigned* counters) {
+    // One thread per panel row (R <= kPanelThreads): a thread owns its row in
+    // shared memory for all w columns, so scaling / rank-1 updates need no
+    // intra-CTA synchronisation; only the pivot choice crosses threads / CTAs.
     extern __shared__ double sm[];
     double* tre = sm;             // [NB][R]
     double* tim = tre + NB * R;   // [NB][R]
-    double* urow = tim + NB * R;  // [2NB]
-    double* drow = urow + 2 * NB; // [2NB]
+    double* urow = tim + NB * R;  // [2NB] pivot row (new row c)
+    double* drow = urow + 2 * NB; // [2NB] old row c (moves to the pivot row)
     __shared__ double red_v[kPanelThreads / 32];
     __shared__ int red_i[kPanelThreads / 32];
-    __shared__ int s_piv;
-    __shared__ int s_win;
+    __shared__ int s_lrow, s_piv;
     __shared__ double s_best;
 
     const int g = blockIdx.x / P, p = blockIdx.x % P;
@@ -77,26 +79,22 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
         const int r0 = k + p * R;
         const int r1 = min(r0 + R, n);
         const int nr = max(0, r1 - r0);
-        for (int idx = tid; idx < w * R; idx += kPanelThreads) {
-            const int j = idx / R, i = idx % R;
-            if (i < nr) {
-                const size_t gi = static_cast<size_t>(k + j) * ld + r0 + i;
-                tre[j * R + i] = Are[gi];
-                tim[j * R + i] = Aim[gi];
+        const int myrow = r0 + tid;
+        const bool own = tid < nr;
+        if (own)
+            for (int j = 0; j < w; ++j) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + myrow;
+                tre[j * R + tid] = Are[gi];
+                tim[j * R + tid] = Aim[gi];
             }
-        }
-        __syncthreads();
         for (int j = 0; j < w; ++j) {
             const int c = k + j;
-            // (a) local argmax of |re|+|im| over own rows >= c
+            // (a) CTA-local argmax of |re|+|im| (LAPACK izamax: first maximum)
             double best = -1.0;
             int bi = INT_MAX;
-            for (int i = tid; i < nr; i += kPanelThreads) {
-                const int gr = r0 + i;
-                if (gr >= c) {
-                    const double v = fabs(tre[j * R + i]) + fabs(tim[j * R + i]);
-                    if (v > best) { best = v; bi = gr; }
-                }
+            if (own && myrow >= c) {
+                best = fabs(tre[j * R + tid]) + fabs(tim[j * R + tid]);
+                bi = myrow;
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
@@ -106,39 +104,42 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
             }
             if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
             __syncthreads();
-            if (tid == 0) {
-                for (int q = 1; q < kPanelThreads / 32; ++q)
-                    if (red_v[q] > red_v[0] || (red_v[q] == red_v[0] && red_i[q] < red_i[0])) {
-                        red_v[0] = red_v[q];
-                        red_i[0] = red_i[q];
-                    }
-            }
-            __syncthreads();
             const int par = step & 1;
             double* myslot = gslots + (static_cast<size_t>(par) * (P + 1) + p) * sstride;
             double* dslot = gslots + (static_cast<size_t>(par) * (P + 1) + P) * sstride;
-            const int lbi = red_i[0];
-            if (tid == 0) { myslot[0] = red_v[0]; myslot[1] = static_cast<double>(lbi); }
-            if (lbi != INT_MAX) {
-                const int li = lbi - r0;
-                for (int jj = tid; jj < 2 * NB; jj += kPanelThreads) {
-                    const int col = jj % NB;
-                    myslot[2 + jj] = col < w ? (jj < NB ? tre[col * R + li] : tim[col * R + li]) : 0.0;
+            if (wid == 0) {
+                double v = lane < kPanelThreads / 32 ? red_v[lane] : -1.0;
+                int ri = lane < kPanelThreads / 32 ? red_i[lane] : INT_MAX;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+                    const int oi = __shfl_xor_sync(0xffffffffu, ri, off);
+                    if (ov > v || (ov == v && oi < ri)) { v = ov; ri = oi; }
                 }
-            }
-            if (c >= r0 && c < r1) {
-                const int li = c - r0;
-                for (int jj = tid; jj < 2 * NB; jj += kPanelThreads) {
+                if (lane == 0) {
+                    myslot[0] = v;
+                    myslot[1] = static_cast<double>(ri);
+                    s_lrow = ri;
+                }
+                __syncwarp();
+                const int lr = s_lrow;
+                if (lr != INT_MAX)
+                    for (int jj = lane; jj < 2 * NB; jj += 32) {
+                        const int col = jj % NB;
+                        myslot[2 + jj] = col < w ? (jj < NB ? tre[col * R + lr - r0] : tim[col * R + lr - r0]) : 0.0;
+                    }
+            } else if (wid == 1 && c >= r0 && c < r1) {
+                for (int jj = lane; jj < 2 * NB; jj += 32) {
                     const int col = jj % NB;
-                    dslot[2 + jj] = col < w ? (jj < NB ? tre[col * R + li] : tim[col * R + li]) : 0.0;
+                    dslot[2 + jj] = col < w ? (jj < NB ? tre[col * R + c - r0] : tim[col * R + c - r0]) : 0.0;
                 }
             }
             ++step;
             group_barrier(ctr, step * static_cast<unsigned>(P));
-            // (b) winner among the P candidates
+            // (b) winner among the P candidates; stage pivot row + old row c
             if (wid == 0) {
                 double bv = -1.0;
-                int bidx = INT_MAX, bw = -1;
+                int bidx = INT_MAX, bw = 0;
                 for (int q = lane; q < P; q += 32) {
                     const double* sl = gslots + (static_cast<size_t>(par) * (P + 1) + q) * sstride;
                     const double v = __ldcg(sl);
@@ -152,71 +153,50 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
                     const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
                     if (ov > bv || (ov == bv && oi < bidx)) { bv = ov; bidx = oi; bw = ow; }
                 }
-                if (lane == 0) { s_piv = bidx; s_win = bw; s_best = bv; }
-            }
-            __syncthreads();
-            const int piv = s_piv;
-            {
-                const double* ws = gslots + (static_cast<size_t>(par) * (P + 1) + s_win) * sstride;
-                for (int jj = tid; jj < 2 * NB; jj += kPanelThreads) {
+                const double* ws = gslots + (static_cast<size_t>(par) * (P + 1) + bw) * sstride;
+                for (int jj = lane; jj < 2 * NB; jj += 32) {
                     urow[jj] = __ldcg(ws + 2 + jj);
                     drow[jj] = __ldcg(dslot + 2 + jj);
                 }
-            }
-            if (p == 0 && tid == 0) {
-                ipiv[static_cast<size_t>(b) * n + c] = piv;
-                if (!(s_best > 0.0) && info[b] == 0) info[b] = c + 1;
-            }
-            __syncthreads();
-            // (c) swap rows c <-> piv inside the panel tile
-            if (piv != c) {
-                if (c >= r0 && c < r1)
-                    for (int jj = tid; jj < w; jj += kPanelThreads) {
-                        tre[jj * R + (c - r0)] = urow[jj];
-                        tim[jj * R + (c - r0)] = urow[NB + jj];
-                    }
-                if (piv >= r0 && piv < r1)
-                    for (int jj = tid; jj < w; jj += kPanelThreads) {
-                        tre[jj * R + (piv - r0)] = drow[jj];
-                        tim[jj * R + (piv - r0)] = drow[NB + jj];
-                    }
-            }
-            __syncthreads();
-            // (d) scale column j below the diagonal, then rank-1 update of the panel
-            const cplx u = mk(urow[j], urow[NB + j]);
-            if (u.re != 0.0 || u.im != 0.0) {
-                const cplx inv = crecip(u);
-                for (int i = tid; i < nr; i += kPanelThreads) {
-                    if (r0 + i > c) {
-                        const cplx l = mk(tre[j * R + i], tim[j * R + i]) * inv;
-                        tre[j * R + i] = l.re;
-                        tim[j * R + i] = l.im;
+                if (lane == 0) {
+                    s_piv = bidx;
+                    s_best = bv;
+                    if (p == 0) {
+                        ipiv[static_cast<size_t>(b) * n + c] = bidx;
+                        if (!(bv > 0.0) && info[b] == 0) info[b] = c + 1;
                     }
                 }
             }
             __syncthreads();
-            const int cols = w - j - 1;
-            if (cols > 0) {
-                for (int idx = tid; idx < cols * nr; idx += kPanelThreads) {
-                    const int jj = j + 1 + idx / nr, i = idx % nr;
-                    if (r0 + i > c) {
-                        const double lr = tre[j * R + i], li = tim[j * R + i];
-                        const double ur = urow[jj], ui = urow[NB + jj];
-                        tre[jj * R + i] -= lr * ur - li * ui;
-                        tim[jj * R + i] -= lr * ui + li * ur;
+            // (c) swap, scale, rank-1 update of the own row
+            const int piv = s_piv;
+            if (own) {
+                if (myrow == c && piv != c) {
+                    for (int jj = 0; jj < w; ++jj) { tre[jj * R + tid] = urow[jj]; tim[jj * R + tid] = urow[NB + jj]; }
+                } else if (myrow == piv && piv != c) {
+                    for (int jj = 0; jj < w; ++jj) { tre[jj * R + tid] = drow[jj]; tim[jj * R + tid] = drow[NB + jj]; }
+                }
+                if (myrow > c) {
+                    const cplx u = mk(urow[j], urow[NB + j]);
+                    if (u.re != 0.0 || u.im != 0.0) {
+                        const cplx l = mk(tre[j * R + tid], tim[j * R + tid]) * crecip(u);
+                        tre[j * R + tid] = l.re;
+                        tim[j * R + tid] = l.im;
+                        for (int jj = j + 1; jj < w; ++jj) {
+                            const double ur = urow[jj], ui = urow[NB + jj];
+                            tre[jj * R + tid] -= l.re * ur - l.im * ui;
+                            tim[jj * R + tid] -= l.re * ui + l.im * ur;
+                        }
                     }
                 }
             }
-            __syncthreads();
         }
-        for (int idx = tid; idx < w * R; idx += kPanelThreads) {
-            const int j = idx / R, i = idx % R;
-            if (i < nr) {
-                const size_t gi = static_cast<size_t>(k + j) * ld + r0 + i;
-                Are[gi] = tre[j * R + i];
-                Aim[gi] = tim[j * R + i];
+        if (own)
+            for (int j = 0; j < w; ++j) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + myrow;
+                Are[gi] = tre[j * R + tid];
+                Aim[gi] = tim[j * R + tid];
             }
-        }
         __syncthreads();
     }
 }
@@ -352,18 +332,25 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
         }
     };
 
-    double acr[4][4][2], aci[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            acr[i][j][0] = acr[i][j][1] = 0.0;
-            aci[i][j][0] = aci[i][j][1] = 0.0;
-        }
-
     const int nk = (w + GBK - 1) / GBK;
     load_stage(0, 0);
     cp_async_commit();
+    // Accumulators start from C (loads overlap the first A/B stage); the
+    // mainloop subtracts L21 U12 and the epilogue is a plain store.
+    double acr[4][4][2], aci[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int row = m0 + wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+                const size_t gi = static_cast<size_t>(col) * ld + row;
+                acr[mi][ni][e] = Are[gi];
+                aci[mi][ni][e] = Aim[gi];
+            }
+    }
     for (int kc = 0; kc < nk; ++kc) {
         if (kc + 1 < nk) load_stage((kc + 1) % GSTAGES, kc + 1);
         cp_async_commit();
@@ -376,14 +363,14 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
         const double* bi = Bs(st, 1);
 #pragma unroll
         for (int k4 = 0; k4 < GBK; k4 += 4) {
-            double fa_r[4], fa_i[4], fa_n[4], fb_r[4], fb_i[4];
+            double na_r[4], fa_i[4], na_i[4], fb_r[4], fb_i[4];
             const int kr = k4 + (lane & 3);
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) {
                 const int m = wm * 32 + mi * 8 + (lane >> 2);
-                fa_r[mi] = ar[kr * GAS + m];
+                na_r[mi] = -ar[kr * GAS + m];
                 fa_i[mi] = ai[kr * GAS + m];
-                fa_n[mi] = -fa_i[mi];
+                na_i[mi] = -fa_i[mi];
             }
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) {
@@ -395,15 +382,16 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) {
-                    dmma(acr[mi][ni][0], acr[mi][ni][1], fa_r[mi], fb_r[ni]);
-                    dmma(aci[mi][ni][0], aci[mi][ni][1], fa_r[mi], fb_i[ni]);
-                    dmma(acr[mi][ni][0], acr[mi][ni][1], fa_n[mi], fb_i[ni]);
-                    dmma(aci[mi][ni][0], aci[mi][ni][1], fa_i[mi], fb_r[ni]);
+                    // C - (ar + i ai)(br + i bi)
+                    dmma(acr[mi][ni][0], acr[mi][ni][1], na_r[mi], fb_r[ni]);
+                    dmma(aci[mi][ni][0], aci[mi][ni][1], na_r[mi], fb_i[ni]);
+                    dmma(acr[mi][ni][0], acr[mi][ni][1], fa_i[mi], fb_i[ni]);
+                    dmma(aci[mi][ni][0], aci[mi][ni][1], na_i[mi], fb_r[ni]);
                 }
         }
         __syncthreads();
     }
-    // epilogue: C -= acc
+    // epilogue: store C - L21 U12
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
         const int row = m0 + wm * 32 + mi * 8 + (lane >> 2);
@@ -414,8 +402,8 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
                 const int col = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
                 if (row < n && col < n) {
                     const size_t gi = static_cast<size_t>(col) * ld + row;
-                    Are[gi] -= acr[mi][ni][e];
-                    Aim[gi] -= aci[mi][ni][e];
+                    Are[gi] = acr[mi][ni][e];
+                    Aim[gi] = aci[mi][ni][e];
                 }
             }
         }
@@ -545,7 +533,8 @@ size_t panel_smem(int nb, int R) { return (2 * static_cast<size_t>(nb) * R + 4 *
 template <int NB>
 int panel_rows_max() {
     const size_t budget = device_info().smem_optin - 8 * 1024;
-    return static_cast<int>((budget / sizeof(double) - 4 * NB) / (2 * NB));
+    const int by_smem = static_cast<int>((budget / sizeof(double) - 4 * NB) / (2 * NB));
+    return std::min(by_smem, kPanelThreads);  // one thread per row
 }
 
 template <int NB>
@@ -575,8 +564,11 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
     unsigned* counters = ws.counters;
     int kk = k, ww = w, PP = P, RR = R, GG = G;
     void* args[] = {&A, &mstride, &plane, &n, &ld, &batch, &kk, &ww, &PP, &RR, &GG, &ipiv, &info, &slots, &counters};
+    cudaEvent_t pe;
+    profiler().begin(st, kProfLuPanel, 0.0, pe);
     FDS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_panel_kernel<NB>), dim3(G * P),
                                          dim3(kPanelThreads), args, smem, st));
+    profiler().end(st, pe, kProfLuPanel, 8.0 * rows * w * w / 2.0 * pb.batch);
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -594,11 +586,18 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
         attr_set = true;
     }
     dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
+    cudaEvent_t te;
+    profiler().begin(st, kProfLuTrsm, 0.0, te);
     FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, 256, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
                pb.ipiv);
+    profiler().end(st, te, kProfLuTrsm, 4.0 * w * w * rest * pb.batch);
     dim3 gg(ceil_div(rest, GBM), ceil_div(rest, GBN), pb.batch);
+    cudaEvent_t ge;
+    profiler().begin(st, kProfLuGemm, 0.0, ge);
     FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
                pb.plane, pb.n, pb.ld, k, w);
+    // algorithmic flops of A22 -= L21 U12 (complex): 8 * rest^2 * w per matrix
+    profiler().end(st, ge, kProfLuGemm, 8.0 * rest * rest * w * pb.batch);
 }
 
 }  // namespace
