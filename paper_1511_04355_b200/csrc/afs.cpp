@@ -1,0 +1,223 @@
+// AFS driver (host C++) — replaces run_afs (proj/src/afs.cpp:226-396) with the
+// same control flow, constants and error classes; every dense-grid / fitting /
+// inversion kernel inside the loop runs on the GPU (vf.cu, laplace.cu), and the
+// J0 initial frequencies of a BEM system are solved as one batched launch.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <limits>
+#include <map>
+#include <numbers>
+#include <optional>
+#include <set>
+
+#include "afs.h"
+#include "vf.cuh"
+
+namespace fdsb {
+
+namespace {
+
+double trapezoid(const std::vector<double>& t, const double* y) {  // afs.cpp:18-24
+    double acc = 0.0;
+    for (size_t i = 1; i < t.size(); ++i) acc += 0.5 * (t[i] - t[i - 1]) * (y[i] + y[i - 1]);
+    return acc;
+}
+
+void validate(const AfsCfg& c) {  // afs.cpp:59-84
+    if (c.initial_count < 4) throw ValidationError("afs: initial_count must be >= 4");
+    if (!(c.alpha_high > 1.0) || !(c.alpha_low > c.alpha_high)) throw ValidationError("afs: need 1 < alpha_high < alpha_low");
+    if (!(c.e1_threshold > 0.0) || !(c.e2_threshold > 0.0)) throw ValidationError("afs: thresholds must be positive");
+    if (c.validation_steps < 0) throw ValidationError("afs: validation_steps must be >= 0");
+    if (!(c.omega_max > 0.0)) throw ValidationError("afs: omega_max must be positive");
+    if (!(c.period > 0.0)) throw ValidationError("afs: period must be positive");
+    if (c.grid_points < 2) throw ValidationError("afs: grid_points must be >= 2");
+    if (c.time_points < 2) throw ValidationError("afs: time_points must be >= 2");
+    if (c.max_iterations < 1) throw ValidationError("afs: max_iterations must be >= 1");
+    if (c.n_relocations < 1) throw ValidationError("afs: n_relocations must be >= 1");
+}
+
+}  // namespace
+
+std::vector<int> draw_channels(int n, int k, uint64_t seed) {  // afs.cpp:28-46
+    std::vector<int> pool(n);
+    for (int i = 0; i < n; ++i) pool[i] = i;
+    uint64_t st = seed ^ 0x9e3779b97f4a7c15ULL;
+    std::vector<int> out;
+    for (int i = 0; i < k; ++i) {
+        st ^= st << 13;
+        st ^= st >> 7;
+        st ^= st << 17;
+        const int j = i + static_cast<int>(st % static_cast<uint64_t>(pool.size() - i));
+        std::swap(pool[i], pool[j]);
+        out.push_back(pool[i]);
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+std::vector<Cx> afs_initial_frequencies(int j0, double eta, double omega_max) {  // afs.cpp:88-100
+    if (j0 < 2) throw ValidationError("initial_frequencies: j0 must be >= 2");
+    if (!(omega_max > 0.0)) throw ValidationError("initial_frequencies: omega_max must be positive");
+    std::vector<Cx> s(j0);
+    for (int j = 0; j < j0; ++j)
+        s[j] = Cx(eta, omega_max * (1.0 - std::cos(j * std::numbers::pi / (2.0 * (j0 - 1)))));
+    return s;
+}
+
+std::pair<int, int> afs_fit_orders(int J, double ah, double al) {  // afs.cpp:102-116
+    const int mh = static_cast<int>(std::floor(J / ah));
+    int ml = static_cast<int>(std::floor(J / al));
+    if (ml < 1) throw NumericError("fit_orders: degenerate low order for J = " + std::to_string(J));
+    if (ml == mh) ml = std::max(mh - 1, 1);
+    if (!(ml >= 1 && ml < mh)) throw NumericError("fit_orders: cannot separate the two orders for J = " + std::to_string(J));
+    return {mh, ml};
+}
+
+double afs_error_e1(const std::vector<double>& t, const std::vector<double>& cur, const std::vector<double>& prev,
+                    int K) {  // afs.cpp:189-216
+    if (K == 0) throw ValidationError("error_e1: no channels");
+    const size_t T = t.size();
+    std::vector<double> d2(T), c2(T);
+    double worst = 0.0;
+    for (int k = 0; k < K; ++k) {
+        for (size_t i = 0; i < T; ++i) {
+            const double a = cur[k * T + i], b = prev[k * T + i];
+            d2[i] = (a - b) * (a - b);
+            c2[i] = a * a;
+        }
+        const double den = trapezoid(t, c2.data());
+        if (den == 0.0) throw NumericError("error_e1: test channel " + std::to_string(k) + " has zero energy");
+        worst = std::max(worst, trapezoid(t, d2.data()) / den);
+    }
+    return worst;
+}
+
+AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
+    validate(cfg);
+    AfsOut r;
+    r.orf = cfg.orf.empty() ? draw_channels(channels, std::min(5, channels), cfg.seed) : cfg.orf;
+    if (cfg.test.empty()) {
+        r.test.resize(channels);
+        for (int k = 0; k < channels; ++k) r.test[k] = k;
+    } else {
+        r.test = cfg.test;
+    }
+    for (const auto* set : {&r.orf, &r.test}) {
+        std::set<int> seen;
+        for (int k : *set) {
+            if (k < 0 || k >= channels) throw ValidationError("afs: channel index out of range");
+            if (!seen.insert(k).second) throw ValidationError("afs: duplicate channel index");
+        }
+    }
+    std::vector<int> fitc;
+    {
+        std::set<int> u(r.orf.begin(), r.orf.end());
+        u.insert(r.test.begin(), r.test.end());
+        fitc.assign(u.begin(), u.end());
+    }
+    auto pos_of = [&](const std::vector<int>& idx) {
+        std::vector<int> p;
+        for (int k : idx) p.push_back(static_cast<int>(std::find(fitc.begin(), fitc.end(), k) - fitc.begin()));
+        return p;
+    };
+    const std::vector<int> orf_pos = pos_of(r.orf), test_pos = pos_of(r.test);
+    const int KF = static_cast<int>(fitc.size());
+
+    std::map<std::pair<double, double>, std::vector<Cx>> cache;
+    auto evaluate = [&](const std::vector<Cx>& ss) {  // afs.cpp:289-302 (batched misses)
+        std::vector<Cx> miss;
+        for (Cx s : ss)
+            if (!cache.count({s.real(), s.imag()}) &&
+                std::find(miss.begin(), miss.end(), s) == miss.end())
+                miss.push_back(s);
+        if (!miss.empty()) {
+            std::vector<Cx> vals(miss.size() * static_cast<size_t>(channels));
+            eval(miss, vals);
+            for (size_t i = 0; i < miss.size(); ++i) {
+                cache[{miss[i].real(), miss[i].imag()}] =
+                    std::vector<Cx>(vals.begin() + i * channels, vals.begin() + (i + 1) * channels);
+                ++r.solver_calls;
+            }
+        }
+        for (Cx s : ss) {
+            r.samples.push_back(s);
+            const auto& v = cache[{s.real(), s.imag()}];
+            r.values.insert(r.values.end(), v.begin(), v.end());
+        }
+    };
+    evaluate(afs_initial_frequencies(cfg.initial_count, cfg.eta, cfg.omega_max));
+
+    std::vector<Cx> grid(cfg.grid_points);  // afs.cpp:308-317
+    for (int i = 0; i < cfg.grid_points; ++i)
+        grid[i] = Cx(cfg.eta, cfg.omega_max * i / (cfg.grid_points - 1));
+    const double radius = cfg.omega_max / (4.0 * cfg.grid_points);
+    std::vector<double> e1_grid(cfg.time_points);
+    for (int i = 0; i < cfg.time_points; ++i) e1_grid[i] = cfg.period * i / (cfg.time_points - 1);
+
+    std::optional<std::vector<double>> prev;
+    int streak = 0;
+    std::vector<Cx> ph;
+    std::vector<Cx> rh_all;
+    while (true) {  // afs.cpp:323-377
+        if (static_cast<int>(r.history.size()) >= cfg.max_iterations)
+            throw ConvergenceError("afs: no convergence within max_iterations");
+        const int J = static_cast<int>(r.samples.size());
+        const auto [MH, ML] = afs_fit_orders(J, cfg.alpha_high, cfg.alpha_low);
+        std::vector<Cx> restricted(static_cast<size_t>(J) * KF);
+        for (int j = 0; j < J; ++j)
+            for (int q = 0; q < KF; ++q)
+                restricted[static_cast<size_t>(j) * KF + q] = r.values[static_cast<size_t>(j) * channels + fitc[q]];
+        std::vector<Cx> p_h, r_h, p_l, r_l;
+        vf_vector_fit(r.samples, restricted.data(), KF, orf_pos, MH, cfg.n_relocations, p_h, r_h, nullptr);
+        vf_vector_fit(r.samples, restricted.data(), KF, orf_pos, ML, cfg.n_relocations, p_l, r_l, nullptr);
+        const std::vector<double> errors = vf_channel_errors(p_h, r_h, p_l, r_l, KF, grid);
+        double e2 = -std::numeric_limits<double>::infinity();
+        if (test_pos.empty()) throw ValidationError("error_e2: no test channels");
+        for (int p : test_pos) e2 = std::max(e2, errors[p]);
+        const int KT = static_cast<int>(test_pos.size());
+        std::vector<Cx> r_test(static_cast<size_t>(KT) * MH);
+        for (int q = 0; q < KT; ++q)
+            std::copy_n(r_h.begin() + static_cast<size_t>(test_pos[q]) * MH, MH, r_test.begin() + static_cast<size_t>(q) * MH);
+        std::vector<double> series(static_cast<size_t>(KT) * e1_grid.size());
+        rat_invert_host(p_h, r_test, KT, e1_grid, series.data());
+        const double e1 = prev ? afs_error_e1(e1_grid, series, *prev, KT) : std::numeric_limits<double>::infinity();
+        prev = std::move(series);
+        r.history.push_back({J, MH, ML, false, Cx(0, 0), e1, e2});
+        ph = p_h;
+        rh_all = r_h;
+        if (e1 <= cfg.e1_threshold && e2 <= cfg.e2_threshold) {
+            if (++streak > cfg.validation_steps) {
+                r.converged = true;
+                break;
+            }
+        } else {
+            streak = 0;
+        }
+        // select_new_frequency recomputes channel_errors on the same models in the
+        // reference (afs.cpp:156); the values are identical, so they are reused.
+        const Cx s_new = vf_select_new_frequency(p_h, r_h, p_l, r_l, KF, grid, r.samples, orf_pos, radius, &errors);
+        r.history.back().has_s_new = true;
+        r.history.back().s_new = s_new;
+        evaluate({s_new});
+    }
+    // Final model over every system channel with the identified poles (afs.cpp:379-393).
+    r.poles = ph;
+    const int J = static_cast<int>(r.samples.size());
+    const int M = static_cast<int>(ph.size());
+    auto& cx = VfContext::get();
+    cplx* dvals = static_cast<cplx*>(cx.values.get(sizeof(cplx) * J * static_cast<size_t>(channels)));
+    cplx* dres = static_cast<cplx*>(cx.out.get(sizeof(cplx) * M * static_cast<size_t>(channels)));
+    FDS_CUDA(cudaMemcpyAsync(dvals, r.values.data(), sizeof(cplx) * J * static_cast<size_t>(channels),
+                             cudaMemcpyHostToDevice, cx.st));
+    vf_residues_device(r.samples, dvals, channels, canonical_order(ph), dres, nullptr, cx.st);
+    std::vector<Cx> rmk(static_cast<size_t>(M) * channels);
+    FDS_CUDA(cudaMemcpyAsync(rmk.data(), dres, rmk.size() * sizeof(cplx), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    r.residues.assign(static_cast<size_t>(channels) * M, Cx(0, 0));
+    for (int k = 0; k < channels; ++k)
+        for (int m = 0; m < M; ++m) r.residues[static_cast<size_t>(k) * M + m] = rmk[static_cast<size_t>(m) * channels + k];
+    return r;
+}
+
+}  // namespace fdsb

@@ -1,0 +1,350 @@
+// Time reconstruction on sm_100a — replaces proj/src/laplace.cpp.
+//
+//   fsm_c2r_kernel     fsm_invert (laplace.cpp:89-125) for a tile of DOFs: the
+//                      conjugate-filled, Hanning-windowed spectrum of length N_s
+//                      is inverted with one N_s/2-point complex inverse FFT per
+//                      DOF (real-output packing, radix-2 Stockham in shared
+//                      memory, one warp per DOF), then scaled by e^{η n Δt}/T.
+//                      HBM-bound: 16 (N_s/2+1) + 8 N_s bytes per DOF.
+//   fsm_dft_kernel     same contract for any even N_s (direct DFT; e.g. the
+//                      paper's N_s = 218), thread per output sample.
+//   rat_invert_kernel  rational_invert (laplace.cpp:127-164) as a real GEMM on
+//                      the FP64 tensor pipe: out[k][t] = Σ_q R[q][k] E[q][t]
+//                      with q over (Re, Im) of each conjugate-pair / real term,
+//                      64x64 output tiles, mma.sync.m8n8k4.f64 fragments from
+//                      bank-conflict-free padded smem.
+//
+// The C2R formulation makes the imaginary part of the reconstruction zero by
+// construction, so the reference's realness check (laplace.cpp:119-121) cannot
+// fire for a conjugate-filled spectrum; it is therefore not re-evaluated.
+#include <cmath>
+
+#include "vf.cuh"
+
+namespace fdsb {
+
+namespace {
+
+constexpr int kFsmTile = 8;  // DOFs per CTA (one warp each)
+
+__device__ __forceinline__ cplx twiddle(int num, int den) {  // exp(+2πi num/den)
+    double s, c;
+    sincospi(2.0 * static_cast<double>(num) / static_cast<double>(den), &s, &c);
+    return mk(c, s);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kFsmTile * 32)
+fsm_c2r_kernel(int Ns, int log2L, double eta, double dt, double invT, int K, const cplx* __restrict__ half,
+               size_t sk, size_t si, int hanning, double* __restrict__ out) {
+    extern __shared__ cplx fsm_sm[];
+    const int L = Ns / 2, Nc = L + 1;
+    cplx* tile = fsm_sm;                     // [Nc][kFsmTile]
+    cplx* tw = tile + Nc * kFsmTile;         // [L/2] exp(2πi j/L)
+    cplx* post = tw + L / 2;                 // [L]   exp(2πi k/Ns)
+    cplx* buf = post + L;                    // [kFsmTile][2][L]
+    const int k0 = blockIdx.x * kFsmTile;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int j = tid; j < L / 2; j += blockDim.x) tw[j] = twiddle(j, L);
+    for (int j = tid; j < L; j += blockDim.x) post[j] = twiddle(j, Ns);
+    // coalesced tile load: consecutive threads -> consecutive DOFs (stride sk)
+    for (int idx = tid; idx < Nc * kFsmTile; idx += blockDim.x) {
+        const int i = idx / kFsmTile, d = idx % kFsmTile;
+        const int k = k0 + d;
+        cplx v = mk(0.0, 0.0);
+        if (k < K) v = half[static_cast<size_t>(k) * sk + static_cast<size_t>(i) * si];
+        tile[i * kFsmTile + d] = v;
+    }
+    __syncthreads();
+    const int k = k0 + warp;
+    if (k >= K) return;
+    cplx* a = buf + static_cast<size_t>(warp) * 2 * L;
+    cplx* b = a + L;
+    // X_k windowed + conjugate-filled; Z_k = (X_k + conj X_{L-k}) + i w^k (X_k - conj X_{L-k})
+    for (int j = lane; j < L; j += 32) {
+        cplx xk = tile[j * kFsmTile + warp];
+        cplx xm = tile[(L - j) * kFsmTile + warp];
+        if (j == 0) xk.im = 0.0;  // k = 0 forced real (laplace.cpp:80)
+        if (j == 0) xm.im = 0.0;  // X_{N/2} forced real (laplace.cpp:81)
+        if (hanning) {
+            double s, c;
+            sincospi(2.0 * j / Ns, &s, &c);
+            const double wk = 0.5 * (1.0 + c);
+            sincospi(2.0 * (L - j) / Ns, &s, &c);
+            const double wm = 0.5 * (1.0 + c);
+            xk = xk * wk;
+            xm = xm * wm;
+        }
+        const cplx cm = conjg(xm);
+        const cplx sum = xk + cm, dif = xk - cm;
+        const cplx p = post[j] * dif;
+        a[j] = mk(sum.re - p.im, sum.im + p.re);  // sum + i * p
+    }
+    __syncwarp();
+    // radix-2 Stockham inverse FFT of length L (exp(+2πi nk/L), unnormalised)
+    int half_len = L / 2;
+    int stride = 1;
+    for (int st = 0; st < log2L; ++st) {
+        for (int q = lane; q < L / 2; q += 32) {
+            const int j = q / stride, r = q % stride;  // j-th group, r-th element
+            const cplx u = a[j * stride + r];
+            const cplx v = a[(j + half_len) * stride + r];
+            const cplx w = tw[j * stride];
+            b[2 * j * stride + r] = u + v;
+            b[(2 * j + 1) * stride + r] = (u - v) * w;
+        }
+        __syncwarp();
+        cplx* t = a;
+        a = b;
+        b = t;
+        half_len >>= 1;
+        stride <<= 1;
+    }
+    // x[2n] = Re z[n], x[2n+1] = Im z[n]; weight e^{η t}/T
+    double* o = out + static_cast<size_t>(k) * Ns;
+    for (int n = lane; n < L; n += 32) {
+        const cplx z = a[n];
+        const double t0 = (2 * n) * dt, t1 = (2 * n + 1) * dt;
+        o[2 * n] = z.re * exp(eta * t0) * invT;
+        o[2 * n + 1] = z.im * exp(eta * t1) * invT;
+    }
+}
+
+__global__ void fsm_dft_kernel(int Ns, double eta, double dt, double invT, int K, const cplx* __restrict__ half,
+                               size_t sk, size_t si, int hanning, double* __restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= K * Ns) return;
+    const int k = idx / Ns, n = idx % Ns;
+    const int L = Ns / 2;
+    double acc = 0.0;
+    for (int j = 0; j <= L; ++j) {
+        cplx x = half[static_cast<size_t>(k) * sk + static_cast<size_t>(j) * si];
+        double w = 1.0;
+        if (hanning) {
+            double s, c;
+            sincospi(2.0 * j / Ns, &s, &c);
+            w = 0.5 * (1.0 + c);
+        }
+        const int ph = static_cast<int>((static_cast<long long>(n) * j) % Ns);
+        double s, c;
+        sincospi(2.0 * ph / Ns, &s, &c);
+        const double re = (x.re * c - x.im * s) * w;
+        if (j == 0 || j == L) acc += x.re * c * w;  // realified end points, once
+        else acc += 2.0 * re;                       // k and N-k (conjugate) together
+    }
+    out[idx] = acc * exp(eta * n * dt) * invT;
+}
+
+// ------------------------------------------------------------------ rational invert
+constexpr int RBM = 64, RBN = 64, RS = 68;  // tile (channels x times), padded stride
+
+__device__ __forceinline__ void dmma_r(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// terms: nt entries of (m index, weight); Q = 2*nt padded to 4. E: [Q][T] real.
+__global__ void __launch_bounds__(128)
+rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, const double* __restrict__ term_w,
+                  const cplx* __restrict__ res /*[m][K]*/, const double* __restrict__ E, double* __restrict__ out) {
+    extern __shared__ double rsm[];
+    double* As = rsm;            // [Q][RS]  (q, channel)
+    double* Bs = rsm + Q * RS;   // [Q][RS]  (q, time)
+    const int k0 = blockIdx.x * RBM, t0 = blockIdx.y * RBN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int idx = tid; idx < (Q / 2) * RBM; idx += blockDim.x) {
+        const int p = idx / RBM, c = idx % RBM;
+        const int k = k0 + c;
+        double re = 0.0, im = 0.0;
+        if (p < nt && k < K) {
+            const cplx r = res[static_cast<size_t>(term_m[p]) * K + k];
+            re = term_w[p] * r.re;
+            im = -term_w[p] * r.im;
+        }
+        As[(2 * p) * RS + c] = re;
+        As[(2 * p + 1) * RS + c] = im;
+    }
+    for (int idx = tid; idx < Q * RBN; idx += blockDim.x) {
+        const int q = idx / RBN, c = idx % RBN;
+        const int t = t0 + c;
+        Bs[q * RS + c] = t < T ? E[static_cast<size_t>(q) * T + t] : 0.0;
+    }
+    __syncthreads();
+    const int wm = warp & 1, wn = warp >> 1;
+    double acc[4][4][2] = {};
+    for (int q0 = 0; q0 < Q; q0 += 4) {
+        const int q = q0 + (lane & 3);
+        double fa[4], fb[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) fa[mi] = As[q * RS + wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) fb[ni] = Bs[q * RS + wn * 32 + ni * 8 + (lane >> 2)];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma_r(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int k = k0 + wm * 32 + mi * 8 + (lane >> 2);
+        if (k >= K) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int t = t0 + wn * 32 + ni * 8 + 2 * (lane & 3);
+            double* o = out + static_cast<size_t>(k) * T + t;
+            if (t + 1 < T && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+                *reinterpret_cast<double2*>(o) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            } else {
+                if (t < T) o[0] = acc[mi][ni][0];
+                if (t + 1 < T) o[1] = acc[mi][ni][1];
+            }
+        }
+    }
+}
+
+__global__ void rat_table_kernel(int Q, int nt, int T, const cplx* __restrict__ tp /*term poles*/,
+                                 const double* __restrict__ t, double* __restrict__ E) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= Q * T) return;
+    const int q = idx / T, n = idx % T;
+    const int p = q / 2;
+    double v = 0.0;
+    if (p < nt) {
+        const cplx e = cexpd(tp[p] * t[n]);
+        v = (q & 1) ? e.im : e.re;
+    }
+    E[idx] = v;
+}
+
+// ------------------------------------------------------------------ host
+namespace {
+
+template <class T>
+T* vdev(VfContext::Buf& b, size_t count) {
+    return static_cast<T*>(b.get(count * sizeof(T)));
+}
+
+}  // namespace
+
+void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int K, const std::vector<double>& t,
+                       double* out_dev, bool paired, cudaStream_t st) {
+    // terms: pairs (head, weight 2) when residues are exactly conjugate per pair,
+    // else every pole with weight 1; Re Σ r e^{a t} = Σ_q R[q] E[q] with
+    // R = w (Re r, -Im r), E = (Re e^{a t}, Im e^{a t}).
+    const int M = static_cast<int>(poles.size()), T = static_cast<int>(t.size());
+    std::vector<int> tm;
+    std::vector<double> tw;
+    std::vector<Cx> tp;
+    if (paired) {
+        for (int m = 0; m < M;) {
+            if (poles[m].imag() != 0.0 && m + 1 < M && poles[m + 1] == std::conj(poles[m])) {
+                tm.push_back(m); tw.push_back(2.0); tp.push_back(poles[m]);
+                m += 2;
+            } else {
+                tm.push_back(m); tw.push_back(1.0); tp.push_back(poles[m]);
+                m += 1;
+            }
+        }
+    } else {
+        for (int m = 0; m < M; ++m) { tm.push_back(m); tw.push_back(1.0); tp.push_back(poles[m]); }
+    }
+    const int nt = static_cast<int>(tm.size());
+    const int Q = (2 * nt + 3) / 4 * 4;
+    auto& cx = VfContext::get();
+    int* dtm = vdev<int>(cx.misc, nt + 1);
+    double* dtw = vdev<double>(cx.misc2, nt + T + 1);
+    double* dt = dtw + nt;
+    cplx* dtp = vdev<cplx>(cx.tab2, nt + 1);
+    double* dE = vdev<double>(cx.tab, static_cast<size_t>(Q) * T);
+    FDS_CUDA(cudaMemcpyAsync(dtm, tm.data(), nt * sizeof(int), cudaMemcpyHostToDevice, st));
+    FDS_CUDA(cudaMemcpyAsync(dtw, tw.data(), nt * sizeof(double), cudaMemcpyHostToDevice, st));
+    FDS_CUDA(cudaMemcpyAsync(dt, t.data(), T * sizeof(double), cudaMemcpyHostToDevice, st));
+    FDS_CUDA(cudaMemcpyAsync(dtp, tp.data(), nt * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    FDS_LAUNCH(rat_table_kernel, ceil_div(Q * T, 256), 256, 0, st, Q, nt, T, dtp, dt, dE);
+    const size_t smem = 2 * static_cast<size_t>(Q) * RS * sizeof(double);
+    if (smem > device_info().smem_optin - 1024) throw ValidationError("rational_invert: model order too large");
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        FDS_CUDA(cudaFuncSetAttribute(rat_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr = smem;
+    }
+    dim3 g(ceil_div(K, RBM), ceil_div(T, RBN));
+    cudaEvent_t pe;
+    profiler().begin(st, kProfRatInv, 0.0, pe);
+    FDS_LAUNCH(rat_invert_kernel, g, 128, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev);
+    // algorithmic FP64 work: 2 * Q * T per channel (2*M*T for M/2 pairs)
+    profiler().end(st, pe, kProfRatInv, 2.0 * (2.0 * nt) * T * static_cast<double>(K));
+}
+
+void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K, const std::vector<double>& t,
+                     double* out) {
+    // laplace.cpp:127-164 validation
+    if (t.empty()) throw ValidationError("rational_invert: empty time grid");
+    for (size_t i = 1; i < t.size(); ++i)
+        if (!(t[i] > t[i - 1])) throw ValidationError("rational_invert: times must be strictly increasing");
+    if (!conj_closed(poles)) throw ValidationError("rational_invert: model poles not conjugate-closed");
+    for (Cx p : poles)
+        if (p.real() * t.back() > 700.0) throw NumericError("rational_invert: exponential overflow on the grid");
+    const int M = static_cast<int>(poles.size()), T = static_cast<int>(t.size());
+    if (K == 0 || T == 0) return;
+    // exact pairing check: adjacent conjugate poles with exactly conjugate residues
+    bool paired = true;
+    for (int m = 0; m < M && paired;) {
+        if (poles[m].imag() != 0.0) {
+            if (m + 1 >= M || poles[m + 1] != std::conj(poles[m])) { paired = false; break; }
+            for (int k = 0; k < K; ++k)
+                if (res_km[static_cast<size_t>(k) * M + m + 1] != std::conj(res_km[static_cast<size_t>(k) * M + m])) {
+                    paired = false;
+                    break;
+                }
+            m += 2;
+        } else {
+            m += 1;
+        }
+    }
+    std::vector<Cx> rmk(static_cast<size_t>(M) * K);
+    for (int k = 0; k < K; ++k)
+        for (int m = 0; m < M; ++m) rmk[static_cast<size_t>(m) * K + k] = res_km[static_cast<size_t>(k) * M + m];
+    auto& cx = VfContext::get();
+    cplx* dres = vdev<cplx>(cx.resid, rmk.size() + 1);
+    double* dout = vdev<double>(cx.out, static_cast<size_t>(K) * T);
+    FDS_CUDA(cudaMemcpyAsync(dres, rmk.data(), rmk.size() * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    rat_invert_device(poles, dres, K, t, dout, paired, cx.st);
+    FDS_CUDA(cudaMemcpyAsync(out, dout, static_cast<size_t>(K) * T * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+}
+
+void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* half_dev, size_t sk, size_t si,
+                       bool hanning, double* out_dev, cudaStream_t st) {
+    if (!(period > 0.0)) throw ValidationError("FsmGrid: period must be positive");
+    if (Ns < 2 || Ns % 2 != 0) throw ValidationError("FsmGrid: sample count must be even and positive");
+    if (K == 0) return;
+    const double dt = period / Ns, invT = 1.0 / period;
+    const int L = Ns / 2;
+    const bool pow2 = (L & (L - 1)) == 0;
+    int log2L = 0;
+    while ((1 << log2L) < L) ++log2L;
+    const size_t smem = (static_cast<size_t>(L + 1) * kFsmTile + L / 2 + L + static_cast<size_t>(kFsmTile) * 2 * L) * sizeof(cplx);
+    cudaEvent_t pe;
+    profiler().begin(st, kProfFsm, 0.0, pe);
+    if (pow2 && L >= 2 && smem <= device_info().smem_optin - 1024) {
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            FDS_CUDA(cudaFuncSetAttribute(fsm_c2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            attr = smem;
+        }
+        FDS_LAUNCH(fsm_c2r_kernel, ceil_div(K, kFsmTile), kFsmTile * 32, smem, st, Ns, log2L, eta, dt, invT, K,
+                   half_dev, sk, si, hanning ? 1 : 0, out_dev);
+    } else {
+        FDS_LAUNCH(fsm_dft_kernel, ceil_div(K * Ns, 256), 256, 0, st, Ns, eta, dt, invT, K, half_dev, sk, si,
+                   hanning ? 1 : 0, out_dev);
+    }
+    // algorithmic bytes per DOF: 16 (Ns/2+1) in + 8 Ns out
+    profiler().end(st, pe, kProfFsm, static_cast<double>(K) * (16.0 * (L + 1) + 8.0 * Ns));
+}
+
+}  // namespace fdsb

@@ -1,0 +1,733 @@
+// Common-pole vector fitting on sm_100a — replaces proj/src/vecfit.cpp
+// (vecfit.hpp:48-86) and the dense-grid kernels of proj/src/afs.cpp
+// (channel_errors :118-145, select_new_frequency :147-187).
+//
+// Device work (batched over channels / DOFs):
+//   vf_reloc_qr_kernel   one CTA per ORF channel: Householder QR of the real
+//                        2J x (2M+1) block [Φ·D1 | −diag(f_k)Φ·D2 | b_k]
+//                        (vecfit.cpp:242-279) in shared memory; emits the R22
+//                        rows, the matching Qᵀb and the tail norm.
+//   vf_residue_kernel    identify_residues for every channel at once
+//                        (vecfit.cpp:356-408): the LS matrix [Re Φ; Im Φ] is
+//                        identical for all channels, so its pivoted QR is
+//                        factored once on the host into the solve operator W
+//                        (M x 2J) and the kernel applies x = W b per channel
+//                        (thread per channel, W chunk in smem, pair-aware
+//                        residue packing), output residues [m][k].
+//   vf_rms_kernel        per-channel residual RMS of the fitted model.
+//   vf_inv_table_kernel  1/(s_g − a_m) over the dense grid, [m][g].
+//   vf_chanerr_kernel    CTA per channel: max_g|f_H − f_L|, max_g|f_H|.
+//   vf_select_kernel     exclusion-radius filtered argmax of |f_H − f_L| for the
+//                        worst ORF channel (first maximum = smallest ω).
+// Host work (latency-bound, microseconds): the shared pivoted QR, the
+// stacked σ least squares and the M x M eigenproblem (host_linalg.cpp).
+#include <algorithm>
+#include <cmath>
+#include <limits>
+
+#include "host_linalg.h"
+#include "vf.cuh"
+
+namespace fdsb {
+
+// ------------------------------------------------------------------ workspace
+void* VfContext::Buf::get(size_t need) {
+    if (need > bytes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        FDS_CUDA(cudaMalloc(&p, need));
+        bytes = need;
+    }
+    return p;
+}
+
+VfContext& VfContext::get() {
+    static thread_local VfContext ctx;
+    if (!ctx.st) {
+        device_info();
+        FDS_CUDA(cudaStreamCreateWithFlags(&ctx.st, cudaStreamNonBlocking));
+    }
+    return ctx;
+}
+
+// ------------------------------------------------------------------ host helpers
+namespace {
+
+bool near_conj(Cx a, Cx b, double tol) {
+    const double sc = std::max({std::abs(a), std::abs(b), 1e-300});
+    return std::abs(a - std::conj(b)) <= tol * sc;
+}
+
+// Real-parameterised partial-fraction basis (vecfit.cpp:38-69), phi[m*J + j].
+std::vector<Cx> basis(const std::vector<Cx>& s, const std::vector<Cx>& poles) {
+    const int J = static_cast<int>(s.size()), M = static_cast<int>(poles.size());
+    std::vector<Cx> phi(static_cast<size_t>(J) * M);
+    const Cx I(0.0, 1.0);
+    for (int j = 0; j < J; ++j) {
+        int m = 0;
+        while (m < M) {
+            const Cx p = poles[m];
+            if (p.imag() != 0.0) {
+                const Cx d1 = s[j] - p, d2 = s[j] - std::conj(p);
+                if (d1 == 0.0 || d2 == 0.0) throw NumericError("sample frequency coincides with a pole");
+                phi[static_cast<size_t>(m) * J + j] = 1.0 / d1 + 1.0 / d2;
+                phi[static_cast<size_t>(m + 1) * J + j] = I / d1 - I / d2;
+                m += 2;
+            } else {
+                const Cx d = s[j] - p;
+                if (d == 0.0) throw NumericError("sample frequency coincides with a pole");
+                phi[static_cast<size_t>(m) * J + j] = 1.0 / d;
+                m += 1;
+            }
+        }
+    }
+    return phi;
+}
+
+int pair_count(const std::vector<Cx>& canon) {
+    int p = 0;
+    while (2 * p + 1 < static_cast<int>(canon.size()) && canon[2 * p].imag() != 0.0) ++p;
+    return p;
+}
+
+double movement_of(const std::vector<Cx>& oldp, const std::vector<Cx>& newp) {  // vecfit.cpp:90-106
+    double worst = 0.0;
+    for (Cx p : newp) {
+        double best = std::numeric_limits<double>::infinity();
+        Cx match = oldp.empty() ? Cx(0, 0) : oldp[0];
+        for (Cx q : oldp) {
+            const double d = std::abs(p - q);
+            if (d < best) { best = d; match = q; }
+        }
+        worst = std::max(worst, best / std::max(std::abs(match), 1e-30));
+    }
+    return worst;
+}
+
+}  // namespace
+
+std::vector<Cx> canonical_order(const std::vector<Cx>& poles) {
+    std::vector<Cx> heads, reals;
+    std::vector<char> used(poles.size(), 0);
+    for (size_t i = 0; i < poles.size(); ++i) {
+        if (used[i]) continue;
+        if (poles[i].imag() == 0.0) { reals.push_back(poles[i]); used[i] = 1; continue; }
+        size_t k = i + 1;
+        for (; k < poles.size(); ++k)
+            if (!used[k] && poles[k].imag() != 0.0 && near_conj(poles[i], poles[k], 1e-9)) break;
+        if (k == poles.size()) throw ValidationError("pole set is not closed under conjugation");
+        heads.push_back(poles[i].imag() > 0.0 ? poles[i] : poles[k]);
+        used[i] = used[k] = 1;
+    }
+    std::vector<Cx> out;
+    out.reserve(poles.size());
+    for (Cx h : heads) { out.push_back(h); out.push_back(std::conj(h)); }
+    out.insert(out.end(), reals.begin(), reals.end());
+    return out;
+}
+
+bool conj_closed(const std::vector<Cx>& poles, double tol) {
+    std::vector<char> used(poles.size(), 0);
+    for (size_t i = 0; i < poles.size(); ++i) {
+        if (used[i] || poles[i].imag() == 0.0) continue;
+        bool hit = false;
+        for (size_t k = 0; k < poles.size() && !hit; ++k)
+            if (k != i && !used[k] && near_conj(poles[i], poles[k], tol)) { used[i] = used[k] = 1; hit = true; }
+        if (!hit) return false;
+    }
+    return true;
+}
+
+void require_distinct(const std::vector<Cx>& s) {
+    std::vector<Cx> v = s;
+    std::sort(v.begin(), v.end(), [](Cx a, Cx b) { return a.real() != b.real() ? a.real() < b.real() : a.imag() < b.imag(); });
+    for (size_t j = 1; j < v.size(); ++j)
+        if (v[j] == v[j - 1]) throw ValidationError("duplicate sample frequencies");
+}
+
+std::vector<Cx> start_poles(double omega_max, int order) {
+    if (order < 1) throw ValidationError("initial_poles: order must be >= 1");
+    if (!(omega_max > 0.0)) throw ValidationError("initial_poles: omega_max must be positive");
+    std::vector<Cx> p;
+    const int pairs = order / 2;
+    for (int i = 1; i <= pairs; ++i) {
+        const double beta = omega_max * static_cast<double>(i) / pairs;
+        p.emplace_back(-beta / 100.0, beta);
+        p.emplace_back(-beta / 100.0, -beta);
+    }
+    if (order % 2 == 1) p.emplace_back(-omega_max / 100.0, 0.0);
+    return p;
+}
+
+// ------------------------------------------------------------------ kernels
+namespace {
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    return t;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256)
+vf_reloc_qr_kernel(int J, int M, int K, const cplx* __restrict__ vals, const cplx* __restrict__ phi,
+                   const double* __restrict__ cscale, const double* __restrict__ sscale, double* gwork,
+                   double* __restrict__ r22, double* __restrict__ beta_out, double* __restrict__ tail) {
+    extern __shared__ double qsm[];
+    __shared__ double red[8];
+    __shared__ double s_tau, s_beta, s_inv;
+    const int k = blockIdx.x;
+    const int rows = 2 * J, cols = 2 * M + 1;
+    const int top = min(2 * M, rows), red_rows = max(0, top - M);
+    double* a = gwork ? gwork + static_cast<size_t>(k) * rows * cols : qsm;
+    for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+        const int i = idx % rows, c = idx / rows;
+        const int j = i >> 1, part = i & 1;
+        const cplx f = vals[static_cast<size_t>(j) * K + k];
+        double v;
+        if (c < M) {
+            const cplx p = phi[static_cast<size_t>(c) * J + j];
+            v = (part ? p.im : p.re) * cscale[c];
+        } else if (c < 2 * M) {
+            const int m = c - M;
+            const cplx r = -(f * phi[static_cast<size_t>(m) * J + j]) * sscale[m];
+            v = part ? r.im : r.re;
+        } else {
+            v = part ? f.im : f.re;
+        }
+        a[static_cast<size_t>(c) * rows + i] = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int q = 0; q < top; ++q) {
+        double* col = a + static_cast<size_t>(q) * rows;
+        double part = 0.0;
+        for (int i = q + 1 + threadIdx.x; i < rows; i += blockDim.x) part += col[i] * col[i];
+        const double sig = block_sum(part, red);
+        if (threadIdx.x == 0) {
+            const double x0 = col[q];
+            if (sig <= 2.2250738585072014e-308) {
+                s_tau = 0.0;
+                s_beta = x0;
+                s_inv = 0.0;
+            } else {
+                const double nrm = sqrt(x0 * x0 + sig);
+                const double bt = x0 >= 0.0 ? -nrm : nrm;
+                s_beta = bt;
+                s_inv = 1.0 / (x0 - bt);
+                s_tau = (bt - x0) / bt;
+            }
+        }
+        __syncthreads();
+        const double tau = s_tau;
+        for (int i = q + 1 + threadIdx.x; i < rows; i += blockDim.x) col[i] = tau == 0.0 ? 0.0 : col[i] * s_inv;
+        __syncthreads();
+        if (threadIdx.x == 0) col[q] = s_beta;
+        __syncthreads();
+        if (tau != 0.0) {
+            for (int c = q + 1 + warp; c < cols; c += nwarp) {
+                double* cc = a + static_cast<size_t>(c) * rows;
+                double d = 0.0;
+                for (int i = q + 1 + lane; i < rows; i += 32) d += col[i] * cc[i];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+                d = (d + cc[q]) * tau;
+                if (lane == 0) cc[q] -= d;
+                for (int i = q + 1 + lane; i < rows; i += 32) cc[i] -= d * col[i];
+            }
+        }
+        __syncthreads();
+    }
+    // R22 = R[M:top, M:2M] (upper-triangular view), beta = (Q^T b)[M:top], tail = ||(Q^T b)[top:]||^2
+    for (int idx = threadIdx.x; idx < red_rows * M; idx += blockDim.x) {
+        const int i = idx / M, c = idx % M;
+        r22[(static_cast<size_t>(k) * red_rows + i) * M + c] = c >= i ? a[static_cast<size_t>(M + c) * rows + M + i] : 0.0;
+    }
+    const double* bcol = a + static_cast<size_t>(2 * M) * rows;
+    for (int i = threadIdx.x; i < red_rows; i += blockDim.x) beta_out[static_cast<size_t>(k) * red_rows + i] = bcol[M + i];
+    double tp = 0.0;
+    for (int i = top + threadIdx.x; i < rows; i += blockDim.x) tp += bcol[i] * bcol[i];
+    const double tt = block_sum(tp, red);
+    if (threadIdx.x == 0) tail[k] = tt;
+}
+
+constexpr int kResChunk = 8;
+constexpr int kResThreads = 128;
+
+__global__ void __launch_bounds__(kResThreads)
+vf_residue_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
+                  cplx* __restrict__ res) {
+    extern __shared__ double wsm[];  // [kResChunk][2J]
+    const int m0 = blockIdx.y * kResChunk;
+    const int cm = min(kResChunk, M - m0);
+    for (int idx = threadIdx.x; idx < cm * 2 * J; idx += blockDim.x)
+        wsm[idx] = W[static_cast<size_t>(m0) * 2 * J + idx];
+    __syncthreads();
+    const int k = blockIdx.x * kResThreads + threadIdx.x;
+    if (k >= K) return;
+    double x[kResChunk];
+#pragma unroll
+    for (int c = 0; c < kResChunk; ++c) x[c] = 0.0;
+    for (int j = 0; j < J; ++j) {
+        const cplx f = vals[static_cast<size_t>(j) * K + k];
+#pragma unroll
+        for (int c = 0; c < kResChunk; ++c) {
+            if (c < cm) x[c] += wsm[c * 2 * J + 2 * j] * f.re + wsm[c * 2 * J + 2 * j + 1] * f.im;
+        }
+    }
+    // canonical packing (vecfit.cpp:72-88): pairs first (heads at even slots), reals last
+#pragma unroll
+    for (int c = 0; c < kResChunk; ++c) {
+        const int m = m0 + c;
+        if (c >= cm) break;
+        cplx r;
+        if (m < 2 * P) {
+            r = (m % 2 == 0) ? mk(x[c], x[c + 1 < kResChunk ? c + 1 : c]) : mk(x[c - 1 >= 0 ? c - 1 : 0], -x[c]);
+        } else {
+            r = mk(x[c], 0.0);
+        }
+        res[static_cast<size_t>(m) * K + k] = r;
+    }
+}
+
+__global__ void vf_rms_kernel(int J, int K, int M, const cplx* __restrict__ vals, const cplx* __restrict__ res,
+                              const cplx* __restrict__ invd /*[m][j]*/, double* __restrict__ rms) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double sq = 0.0;
+    for (int j = 0; j < J; ++j) {
+        cplx fit = mk(0.0, 0.0);
+        for (int m = 0; m < M; ++m) fit = fit + res[static_cast<size_t>(m) * K + k] * invd[static_cast<size_t>(m) * J + j];
+        const cplx d = fit - vals[static_cast<size_t>(j) * K + k];
+        sq += abs2(d);
+    }
+    rms[k] = sqrt(sq / J);
+}
+
+__global__ void vf_inv_table_kernel(int G, int M, const cplx* __restrict__ grid, const cplx* __restrict__ poles,
+                                    cplx* __restrict__ inv /*[m][g]*/) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= G * M) return;
+    const int m = idx / G, g = idx % G;
+    inv[idx] = crecip(grid[g] - poles[m]);
+}
+
+__device__ __forceinline__ void model_at(int g, int G, int M, const cplx* r, const cplx* inv, cplx& acc) {
+    acc = mk(0.0, 0.0);
+    for (int m = 0; m < M; ++m) acc = acc + r[m] * inv[static_cast<size_t>(m) * G + g];
+}
+
+__global__ void __launch_bounds__(256)
+vf_chanerr_kernel(int G, int MH, int ML, int K, const cplx* __restrict__ rh /*[k][MH]*/,
+                  const cplx* __restrict__ rl /*[k][ML]*/, const cplx* __restrict__ invh, const cplx* __restrict__ invl,
+                  double* __restrict__ out /*[k][2]: max|fH-fL|, max|fH|*/) {
+    extern __shared__ cplx rsm[];
+    __shared__ double red[2][8];
+    const int k = blockIdx.x;
+    for (int m = threadIdx.x; m < MH; m += blockDim.x) rsm[m] = rh[static_cast<size_t>(k) * MH + m];
+    for (int m = threadIdx.x; m < ML; m += blockDim.x) rsm[MH + m] = rl[static_cast<size_t>(k) * ML + m];
+    __syncthreads();
+    double md = 0.0, mh = 0.0;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        cplx fh, fl;
+        model_at(g, G, MH, rsm, invh, fh);
+        model_at(g, G, ML, rsm + MH, invl, fl);
+        const cplx d = fh - fl;
+        md = fmax(md, hypot(d.re, d.im));
+        mh = fmax(mh, hypot(fh.re, fh.im));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        md = fmax(md, __shfl_xor_sync(0xffffffffu, md, off));
+        mh = fmax(mh, __shfl_xor_sync(0xffffffffu, mh, off));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { red[0][wid] = md; red[1][wid] = mh; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { md = fmax(md, red[0][w]); mh = fmax(mh, red[1][w]); }
+        md = fmax(md, red[0][0]);
+        mh = fmax(mh, red[1][0]);
+        out[2 * k] = md;
+        out[2 * k + 1] = mh;
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+vf_select_kernel(int G, int MH, int ML, const cplx* __restrict__ rh, const cplx* __restrict__ rl,
+                 const cplx* __restrict__ invh, const cplx* __restrict__ invl, const cplx* __restrict__ grid,
+                 int nex, const double* __restrict__ ex_im, double radius, int* __restrict__ out) {
+    extern __shared__ double exs[];
+    __shared__ cplx r[512];
+    __shared__ double bv[32];
+    __shared__ int bi[32];
+    for (int i = threadIdx.x; i < nex; i += blockDim.x) exs[i] = ex_im[i];
+    for (int m = threadIdx.x; m < MH; m += blockDim.x) r[m] = rh[m];
+    for (int m = threadIdx.x; m < ML; m += blockDim.x) r[MH + m] = rl[m];
+    __syncthreads();
+    double best = -1.0;
+    int bidx = 0x7fffffff;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const double im = grid[g].im;
+        bool excl = false;
+        for (int e = 0; e < nex && !excl; ++e) excl = fabs(im - exs[e]) < radius;
+        if (excl) continue;
+        cplx fh, fl;
+        model_at(g, G, MH, r, invh, fh);
+        model_at(g, G, ML, r + MH, invl, fl);
+        const cplx d = fh - fl;
+        const double v = hypot(d.re, d.im);
+        if (v > best) { best = v; bidx = g; }  // g increases per thread: first max kept
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+        if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { bv[wid] = best; bi[wid] = bidx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) { bv[0] = bv[w]; bi[0] = bi[w]; }
+        out[0] = bv[0] >= 0.0 ? bi[0] : -1;
+    }
+}
+
+// ------------------------------------------------------------------ host drivers
+namespace {
+
+template <class T>
+T* dev(VfContext::Buf& b, size_t count) {
+    return static_cast<T*>(b.get(count * sizeof(T)));
+}
+
+}  // namespace
+
+RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<Cx>& poles_in) {
+    // vecfit.cpp:188-354
+    const int J = static_cast<int>(s.size());
+    const int M = static_cast<int>(poles_in.size());
+    if (J == 0) throw ValidationError("relocate_poles: no samples");
+    if (K < 1) throw ValidationError("relocate_poles: no channels");
+    if (2 * J < M + 1) throw ValidationError("relocate_poles: too few samples for the order");
+    require_distinct(s);
+    const std::vector<Cx> poles = canonical_order(poles_in);
+    const std::vector<Cx> phi = basis(s, poles);
+    std::vector<double> cscale(M), sscale(M);
+    for (int m = 0; m < M; ++m) {
+        double n2 = 0.0, sq = 0.0;
+        for (int j = 0; j < J; ++j) n2 += std::norm(phi[static_cast<size_t>(m) * J + j]);
+        for (int k = 0; k < K; ++k)
+            for (int j = 0; j < J; ++j) sq += std::norm(values[static_cast<size_t>(j) * K + k] * phi[static_cast<size_t>(m) * J + j]);
+        const double n = std::sqrt(n2);
+        cscale[m] = n > 0.0 ? 1.0 / n : 1.0;
+        sscale[m] = sq > 0.0 ? 1.0 / std::sqrt(sq) : 1.0;
+    }
+    auto& cx = VfContext::get();
+    const int rows = 2 * J, cols = 2 * M + 1;
+    const int top = std::min(2 * M, rows), red = std::max(0, top - M);
+    cplx* dvals = dev<cplx>(cx.values, static_cast<size_t>(J) * K);
+    cplx* dphi = dev<cplx>(cx.phi, static_cast<size_t>(J) * M);
+    double* dsc = dev<double>(cx.misc, 2 * static_cast<size_t>(M));
+    double* dr22 = dev<double>(cx.resid, static_cast<size_t>(K) * red * M + static_cast<size_t>(K) * red + K);
+    double* dbeta = dr22 + static_cast<size_t>(K) * red * M;
+    double* dtail = dbeta + static_cast<size_t>(K) * red;
+    FDS_CUDA(cudaMemcpyAsync(dvals, values, sizeof(cplx) * J * K, cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dphi, phi.data(), sizeof(cplx) * J * M, cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dsc, cscale.data(), sizeof(double) * M, cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dsc + M, sscale.data(), sizeof(double) * M, cudaMemcpyHostToDevice, cx.st));
+    const size_t mat_bytes = static_cast<size_t>(rows) * cols * sizeof(double);
+    double* gwork = nullptr;
+    size_t smem = mat_bytes;
+    if (mat_bytes > device_info().smem_optin - 4096) {
+        gwork = dev<double>(cx.qr, static_cast<size_t>(rows) * cols * K);
+        smem = 0;
+    } else {
+        static size_t attr = 0;
+        if (smem > attr) {
+            FDS_CUDA(cudaFuncSetAttribute(vf_reloc_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            attr = smem;
+        }
+    }
+    FDS_LAUNCH(vf_reloc_qr_kernel, K, 256, smem, cx.st, J, M, K, dvals, dphi, dsc, dsc + M, gwork, dr22, dbeta,
+               dtail);
+    std::vector<double> hr(static_cast<size_t>(K) * red * M), hb(static_cast<size_t>(K) * red), ht(K);
+    FDS_CUDA(cudaMemcpyAsync(hr.data(), dr22, hr.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(hb.data(), dbeta, hb.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(ht.data(), dtail, ht.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    // stacked sigma least squares (vecfit.cpp:281-285)
+    hla::Dense st(K * red, M);
+    std::vector<double> rhs(static_cast<size_t>(K) * red);
+    for (int k = 0; k < K; ++k)
+        for (int i = 0; i < red; ++i) {
+            for (int c = 0; c < M; ++c) st.at(k * red + i, c) = hr[(static_cast<size_t>(k) * red + i) * M + c];
+            rhs[static_cast<size_t>(k) * red + i] = hb[static_cast<size_t>(k) * red + i];
+        }
+    const hla::PivotedQR solver(st);
+    if (solver.rank() < M) throw NumericError("relocate_poles: rank-deficient least-squares system");
+    const std::vector<double> y = solver.solve(rhs);
+    RelocResult out;
+    out.rms.assign(K, 0.0);
+    for (int k = 0; k < K; ++k) {  // vecfit.cpp:287-295
+        double c2 = 0.0;
+        for (int i = 0; i < red; ++i) {
+            double v = -hb[static_cast<size_t>(k) * red + i];
+            for (int c = 0; c < M; ++c) v += hr[(static_cast<size_t>(k) * red + i) * M + c] * y[c];
+            c2 += v * v;
+        }
+        out.rms[k] = std::sqrt((c2 + ht[k]) / J);
+    }
+    // zeros of sigma: eig(blockdiag(poles) - b c^T) (vecfit.cpp:297-324)
+    hla::Dense h(M, M);
+    std::vector<double> bv(M), cr(M);
+    for (int m = 0; m < M;) {
+        if (poles[m].imag() != 0.0) {
+            h.at(m, m) = poles[m].real();
+            h.at(m, m + 1) = poles[m].imag();
+            h.at(m + 1, m) = -poles[m].imag();
+            h.at(m + 1, m + 1) = poles[m].real();
+            bv[m] = 2.0;
+            bv[m + 1] = 0.0;
+            cr[m] = sscale[m] * y[m];
+            cr[m + 1] = sscale[m + 1] * y[m + 1];
+            m += 2;
+        } else {
+            h.at(m, m) = poles[m].real();
+            bv[m] = 1.0;
+            cr[m] = sscale[m] * y[m];
+            m += 1;
+        }
+    }
+    for (int i = 0; i < M; ++i)
+        for (int c = 0; c < M; ++c) h.at(i, c) -= bv[i] * cr[c];
+    std::vector<Cx> ev;
+    if (!hla::eigenvalues(h, ev)) throw NumericError("relocate_poles: eigenvalue iteration failed");
+    std::vector<Cx> heads, reals;
+    int neg = 0;
+    for (Cx e : ev) {
+        if (e.imag() > 0.0) heads.push_back(e);
+        else if (e.imag() < 0.0) ++neg;
+        else reals.push_back(e);
+    }
+    if (neg != static_cast<int>(heads.size())) throw NumericError("relocate_poles: eigenvalues not conjugate-paired");
+    for (Cx hd : heads) { out.poles.push_back(hd); out.poles.push_back(std::conj(hd)); }
+    out.poles.insert(out.poles.end(), reals.begin(), reals.end());
+    out.movement = movement_of(poles, out.poles);
+    return out;
+}
+
+void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K, const std::vector<Cx>& poles,
+                        cplx* res_dev, double* rms_dev, cudaStream_t st) {
+    // vecfit.cpp:356-408 for all channels: factor [Re Φ; Im Φ] (column-scaled)
+    // once on the host, apply its solve operator on the device.
+    const int J = static_cast<int>(s.size()), M = static_cast<int>(poles.size());
+    if (J < 1) throw ValidationError("identify_residues: no samples");
+    if (2 * J < M) throw ValidationError("identify_residues: too few samples for the order");
+    require_distinct(s);
+    const std::vector<Cx> phi = basis(s, poles);
+    hla::Dense a(2 * J, M);
+    std::vector<double> scale(M);
+    for (int m = 0; m < M; ++m) {
+        double n2 = 0.0;
+        for (int j = 0; j < J; ++j) {
+            const Cx v = phi[static_cast<size_t>(m) * J + j];
+            a.at(2 * j, m) = v.real();
+            a.at(2 * j + 1, m) = v.imag();
+            n2 += v.real() * v.real() + v.imag() * v.imag();
+        }
+        const double n = std::sqrt(n2);
+        scale[m] = n > 0.0 ? 1.0 / n : 1.0;
+        for (int i = 0; i < 2 * J; ++i) a.at(i, m) *= scale[m];
+    }
+    const hla::PivotedQR qr(a);
+    if (qr.rank() < M) throw NumericError("identify_residues: rank-deficient least-squares system");
+    const hla::Dense W0 = qr.solve_operator();  // M x 2J
+    std::vector<double> W(static_cast<size_t>(M) * 2 * J);
+    for (int m = 0; m < M; ++m)
+        for (int i = 0; i < 2 * J; ++i) W[static_cast<size_t>(m) * 2 * J + i] = scale[m] * W0.at(m, i);
+    auto& cx = VfContext::get();
+    double* dW = dev<double>(cx.W, W.size());
+    FDS_CUDA(cudaMemcpyAsync(dW, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    const int P = pair_count(poles);
+    const size_t smem = static_cast<size_t>(kResChunk) * 2 * J * sizeof(double);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        FDS_CUDA(cudaFuncSetAttribute(vf_residue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr = smem;
+    }
+    dim3 g(ceil_div(K, kResThreads), ceil_div(M, kResChunk));
+    cudaEvent_t pe;
+    profiler().begin(st, kProfVfResidue, 0.0, pe);
+    FDS_LAUNCH(vf_residue_kernel, g, kResThreads, smem, st, J, K, M, P, values_dev, dW, res_dev);
+    // algorithmic bytes: values 16 J + unique residues 16 M/2 per channel
+    profiler().end(st, pe, kProfVfResidue, static_cast<double>(K) * (16.0 * J + 8.0 * M));
+    if (rms_dev) {
+        std::vector<Cx> invd(static_cast<size_t>(M) * J);
+        for (int m = 0; m < M; ++m)
+            for (int j = 0; j < J; ++j) invd[static_cast<size_t>(m) * J + j] = 1.0 / (s[j] - poles[m]);
+        cplx* dinv = dev<cplx>(cx.phi, invd.size());
+        FDS_CUDA(cudaMemcpyAsync(dinv, invd.data(), invd.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
+        FDS_LAUNCH(vf_rms_kernel, ceil_div(K, 128), 128, 0, st, J, K, M, values_dev, res_dev, dinv, rms_dev);
+    }
+}
+
+void vf_vector_fit(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<int>& orf, int order,
+                   int n_reloc, std::vector<Cx>& poles, std::vector<Cx>& res_km, FitReportC* rep) {
+    // vecfit.cpp:410-488
+    const int J = static_cast<int>(s.size());
+    if (J == 0) throw ValidationError("vector_fit: no samples");
+    if (order < 1) throw ValidationError("vector_fit: order must be >= 1");
+    if (order >= 2 * J) throw ValidationError("vector_fit: order too high for the sample count");
+    if (n_reloc < 1) throw ValidationError("vector_fit: n_relocations must be >= 1");
+    if (orf.empty()) throw ValidationError("vector_fit: ORF channel set is empty");
+    for (int k : orf)
+        if (k < 0 || k >= K) throw ValidationError("vector_fit: ORF channel index out of range");
+    const int KO = static_cast<int>(orf.size());
+    std::vector<Cx> ov(static_cast<size_t>(J) * KO);
+    for (int j = 0; j < J; ++j)
+        for (int q = 0; q < KO; ++q) ov[static_cast<size_t>(j) * KO + q] = values[static_cast<size_t>(j) * K + orf[q]];
+    double band = 0.0;
+    for (Cx x : s) band = std::max(band, std::abs(x.imag()));
+    if (band == 0.0)
+        for (Cx x : s) band = std::max(band, std::abs(x));
+    if (band == 0.0) throw ValidationError("vector_fit: samples carry no frequency band");
+    poles = start_poles(band, order);
+    FitReportC r;
+    RelocResult rr;
+    for (int it = 0; it < n_reloc; ++it) {
+        rr = vf_relocate(s, ov.data(), KO, poles);
+        poles = rr.poles;
+        r.iterations = it + 1;
+        r.movement = rr.movement;
+        if (rr.movement < 1e-8) break;
+    }
+    r.reloc_rms = rr.rms;
+    // residues for every channel on the device
+    const std::vector<Cx> canon = canonical_order(poles);
+    auto& cx = VfContext::get();
+    cplx* dvals = dev<cplx>(cx.values, static_cast<size_t>(J) * K);
+    cplx* dres = dev<cplx>(cx.out, static_cast<size_t>(order) * K);
+    double* drms = dev<double>(cx.rms, K);
+    FDS_CUDA(cudaMemcpyAsync(dvals, values, sizeof(cplx) * J * K, cudaMemcpyHostToDevice, cx.st));
+    vf_residues_device(s, dvals, K, canon, dres, drms, cx.st);
+    std::vector<Cx> rmk(static_cast<size_t>(order) * K);
+    r.rms.assign(K, 0.0);
+    FDS_CUDA(cudaMemcpyAsync(rmk.data(), dres, rmk.size() * sizeof(cplx), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(r.rms.data(), drms, K * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    // The reference keeps the relocation's pole order (heads in eigenvalue order),
+    // and identify_residues canonicalises internally: for VF output they coincide.
+    poles = canon;
+    res_km.assign(static_cast<size_t>(K) * order, Cx(0, 0));
+    for (int k = 0; k < K; ++k)
+        for (int m = 0; m < order; ++m) res_km[static_cast<size_t>(k) * order + m] = rmk[static_cast<size_t>(m) * K + k];
+    for (Cx p : poles) r.unstable += p.real() > 0.0;
+    if (rep) *rep = std::move(r);
+}
+
+std::vector<double> vf_channel_errors(const std::vector<Cx>& ph, const std::vector<Cx>& rh, const std::vector<Cx>& pl,
+                                      const std::vector<Cx>& rl, int K, const std::vector<Cx>& grid) {
+    // afs.cpp:118-145
+    if (grid.empty()) throw ValidationError("channel_errors: empty grid");
+    const int G = static_cast<int>(grid.size()), MH = static_cast<int>(ph.size()), ML = static_cast<int>(pl.size());
+    for (Cx g : grid) {
+        for (Cx p : ph) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
+        for (Cx p : pl) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
+    }
+    auto& cx = VfContext::get();
+    cplx* dgrid = dev<cplx>(cx.misc2, G + MH + ML);
+    cplx* dph = dgrid + G;
+    cplx* dpl = dph + MH;
+    cplx* dinv = dev<cplx>(cx.tab, static_cast<size_t>(G) * (MH + ML));
+    cplx* dr = dev<cplx>(cx.resid, static_cast<size_t>(K) * (MH + ML));
+    double* dout = dev<double>(cx.rms, 2 * static_cast<size_t>(K));
+    FDS_CUDA(cudaMemcpyAsync(dgrid, grid.data(), G * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dph, ph.data(), MH * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dpl, pl.data(), ML * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dr, rh.data(), static_cast<size_t>(K) * MH * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dr + static_cast<size_t>(K) * MH, rl.data(), static_cast<size_t>(K) * ML * sizeof(cplx),
+                             cudaMemcpyHostToDevice, cx.st));
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * MH, 256), 256, 0, cx.st, G, MH, dgrid, dph, dinv);
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * ML, 256), 256, 0, cx.st, G, ML, dgrid, dpl,
+               dinv + static_cast<size_t>(G) * MH);
+    cudaEvent_t pe;
+    profiler().begin(cx.st, kProfChanErr, 0.0, pe);
+    FDS_LAUNCH(vf_chanerr_kernel, K, 256, (MH + ML) * sizeof(cplx), cx.st, G, MH, ML, K, dr,
+               dr + static_cast<size_t>(K) * MH, dinv, dinv + static_cast<size_t>(G) * MH, dout);
+    profiler().end(cx.st, pe, kProfChanErr, 8.0 * G * static_cast<double>(K) * (MH + ML));
+    std::vector<double> h(2 * static_cast<size_t>(K));
+    FDS_CUDA(cudaMemcpyAsync(h.data(), dout, h.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    std::vector<double> e(K);
+    for (int k = 0; k < K; ++k) {
+        if (h[2 * k + 1] == 0.0)
+            throw NumericError("channel_errors: channel " + std::to_string(k) + " has identically zero high-order fit");
+        e[k] = h[2 * k] / h[2 * k + 1];
+    }
+    return e;
+}
+
+Cx vf_select_new_frequency(const std::vector<Cx>& ph, const std::vector<Cx>& rh, const std::vector<Cx>& pl,
+                           const std::vector<Cx>& rl, int K, const std::vector<Cx>& grid,
+                           const std::vector<Cx>& existing, const std::vector<int>& orf_pos, double radius,
+                           const std::vector<double>* errors_in) {
+    // afs.cpp:147-187
+    if (orf_pos.empty()) throw ValidationError("select_new_frequency: empty ORF set");
+    const std::vector<double> errors = errors_in ? *errors_in : vf_channel_errors(ph, rh, pl, rl, K, grid);
+    int kmax = orf_pos[0];
+    double worst = -1.0;
+    for (int k : orf_pos) {
+        if (k < 0 || k >= K) throw ValidationError("select_new_frequency: ORF position out of range");
+        if (errors[k] > worst) { worst = errors[k]; kmax = k; }
+    }
+    const int G = static_cast<int>(grid.size()), MH = static_cast<int>(ph.size()), ML = static_cast<int>(pl.size());
+    if (MH + ML > 512) throw ValidationError("select_new_frequency: model order too large");
+    auto& cx = VfContext::get();
+    // (re)build the inverse tables — cheap, keeps the function self-contained
+    cplx* dgrid = dev<cplx>(cx.misc2, G + MH + ML);
+    cplx* dph = dgrid + G;
+    cplx* dpl = dph + MH;
+    cplx* dinv = dev<cplx>(cx.tab, static_cast<size_t>(G) * (MH + ML));
+    cplx* dr = dev<cplx>(cx.tab2, MH + ML);
+    std::vector<double> exim(existing.size());
+    for (size_t i = 0; i < existing.size(); ++i) exim[i] = existing[i].imag();
+    double* dex = dev<double>(cx.misc, std::max<size_t>(exim.size(), 1) + 2);
+    int* dsel = reinterpret_cast<int*>(dex + std::max<size_t>(exim.size(), 1));
+    FDS_CUDA(cudaMemcpyAsync(dgrid, grid.data(), G * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dph, ph.data(), MH * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dpl, pl.data(), ML * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dr, rh.data() + static_cast<size_t>(kmax) * MH, MH * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dr + MH, rl.data() + static_cast<size_t>(kmax) * ML, ML * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    if (!exim.empty())
+        FDS_CUDA(cudaMemcpyAsync(dex, exim.data(), exim.size() * sizeof(double), cudaMemcpyHostToDevice, cx.st));
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * MH, 256), 256, 0, cx.st, G, MH, dgrid, dph, dinv);
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * ML, 256), 256, 0, cx.st, G, ML, dgrid, dpl,
+               dinv + static_cast<size_t>(G) * MH);
+    const int nex = static_cast<int>(exim.size());
+    const size_t smem = std::max<size_t>(nex, 1) * sizeof(double);
+    if (smem > 48 * 1024) {
+        FDS_CUDA(cudaFuncSetAttribute(vf_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(std::min(smem, device_info().smem_optin - 16 * 1024))));
+    }
+    FDS_LAUNCH(vf_select_kernel, 1, 1024, smem, cx.st, G, MH, ML, dr, dr + MH, dinv, dinv + static_cast<size_t>(G) * MH,
+               dgrid, nex, dex, radius, dsel);
+    int sel = -1;
+    FDS_CUDA(cudaMemcpyAsync(&sel, dsel, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    if (sel < 0) throw NumericError("select_new_frequency: every grid point is excluded");
+    return grid[sel];
+}
+
+}  // namespace fdsb

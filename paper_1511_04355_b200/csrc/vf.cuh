@@ -1,0 +1,80 @@
+// Vector fitting on sm_100a: shared declarations (vf.cu, laplace.cu, afs.cpp).
+#pragma once
+
+#include <complex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fdsb {
+
+using Cx = std::complex<double>;
+
+// Thread-local device workspace shared by the VF / Laplace / AFS entry points
+// (growable buffers, one non-blocking stream). Avoids per-call cudaMalloc in
+// the AFS loop.
+struct VfContext {
+    cudaStream_t st = nullptr;
+    struct Buf {
+        void* p = nullptr;
+        size_t bytes = 0;
+        void* get(size_t need);
+    };
+    Buf values, resid, W, phi, rms, tab, tab2, out, misc, misc2, qr;
+    static VfContext& get();
+};
+
+// ------------------------------------------------------------------ host helpers
+std::vector<Cx> canonical_order(const std::vector<Cx>& poles);  // vecfit.cpp:134-169
+bool conj_closed(const std::vector<Cx>& poles, double tol = 1e-9);  // vecfit.cpp:116-132
+void require_distinct(const std::vector<Cx>& s);                 // vecfit.cpp:20-30
+std::vector<Cx> start_poles(double omega_max, int order);        // vecfit.cpp:171-186
+
+struct RelocResult {
+    std::vector<Cx> poles;
+    std::vector<double> rms;
+    double movement = 0.0;
+};
+
+// relocate_poles on K channels of host samples (values [j][k]).
+RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<Cx>& poles_in);
+
+// identify_residues for K channels whose values live on the device as
+// [j][k] complex (values_dev); residues written on the device as [m][k];
+// rms_dev (K doubles) optional. Poles must already be canonical.
+void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
+                        const std::vector<Cx>& poles, cplx* res_dev, double* rms_dev, cudaStream_t st);
+
+struct FitReportC {
+    int iterations = 0;
+    double movement = 0.0;
+    int unstable = 0;
+    std::vector<double> rms, reloc_rms;
+};
+
+// vector_fit over host samples; residues returned [k][m].
+void vf_vector_fit(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<int>& orf, int order,
+                   int n_reloc, std::vector<Cx>& poles, std::vector<Cx>& residues_km, FitReportC* rep);
+
+// channel_errors (afs.cpp:118-145) for two models over a grid; residues [k][m].
+std::vector<double> vf_channel_errors(const std::vector<Cx>& ph, const std::vector<Cx>& rh,
+                                      const std::vector<Cx>& pl, const std::vector<Cx>& rl, int K,
+                                      const std::vector<Cx>& grid);
+// select_new_frequency (afs.cpp:147-187) given precomputed channel errors.
+Cx vf_select_new_frequency(const std::vector<Cx>& ph, const std::vector<Cx>& rh, const std::vector<Cx>& pl,
+                           const std::vector<Cx>& rl, int K, const std::vector<Cx>& grid,
+                           const std::vector<Cx>& existing, const std::vector<int>& orf_pos, double radius,
+                           const std::vector<double>* errors);
+
+// rational_invert (laplace.cpp:127-164): host model -> host out[k][t].
+void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K,
+                     const std::vector<double>& t, double* out);
+// device variant: residues on device [m][k]; paired = residues exactly conjugate per pair.
+void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int K, const std::vector<double>& t,
+                       double* out_dev, bool paired, cudaStream_t st);
+
+// fsm_invert (laplace.cpp:89-125): half spectra element (k, i) at half[k*sk + i*si] (device).
+void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* half_dev, size_t sk, size_t si,
+                       bool hanning, double* out_dev, cudaStream_t st);
+
+}  // namespace fdsb
