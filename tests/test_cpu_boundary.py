@@ -1,0 +1,109 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and exports
+every entry point include/fdsweep_b200.h declares (no compute without a GPU),
+host-side mesh/load generators, and the multi-rank bench plumbing (gloo).
+"""
+import ctypes
+import os
+import re
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1511_04355_b200 as P
+import pyoracle as O
+from paper_1511_04355_b200 import mesh
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "fdsweep_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fds_[a-z0-9_]+)\s*\(", text)) - {"fds_system_fn"})
+
+
+def test_library_exports_every_declared_symbol():
+    lib = P.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.fds_version().decode().startswith("fdsweep_b200")
+
+
+def test_library_built_for_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(P.library_path())], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_library_has_dmma_sass():
+    out = subprocess.run(["cuobjdump", "-sass", str(P.library_path())], capture_output=True, text=True).stdout
+    assert "DMMA" in out  # LU trailing GEMM and rational inversion on the FP64 tensor pipe
+
+
+def test_no_gpu_fails_loudly():
+    """Without a GPU the product must raise, never fall back to a CPU path."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.CudaError):
+        V, F = mesh.icosphere(0)
+        P.BemSystem(V, F, mesh.pressure_traction(V, F))
+
+
+def test_draw_indices_matches_reference():
+    # the reference's draw_indices (afs.cpp:28-46) picks the ORFs when none are given
+    fx_json = '{"type": "modal", "omega": [1.0, 2.0], "zeta": [0.1, 0.1], "participation": ' + \
+              "{" + ", ".join(f'"c{k}": [1.0, {k + 1.0}]' for k in range(12)) + "}}"
+    sysm = O.System.from_json(fx_json)
+    r = O.run_afs(sysm, omega_max=3.0, eta=0.3, period=10.0, initial_count=8, e1_threshold=float("inf"),
+                  e2_threshold=float("inf"), grid_points=64, time_points=32, seed=11, validation_steps=0,
+                  test=[0])
+    assert list(r["orf"]) == mesh.draw_indices(12, 5, 11)
+
+
+def test_meshes():
+    V, F = mesh.icosphere(4)
+    assert F.shape == (5120, 3)
+    V, F = mesh.cube_cavity(32)
+    assert F.shape == (12288, 3)
+    c, n, a = mesh.element_geometry(V, F)
+    assert abs(a.sum() - 6.0) < 1e-12
+    tr = mesh.random_traction(10, 0)
+    assert tr.shape == (10, 3) and abs(tr.mean()) < 1.5
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_bench_replica_reduction_gloo():
+    """bench.py's max-over-ranks reduction over world_size 2 (gloo, CPU)."""
+    code = r'''
+import os, torch, torch.distributed as dist
+dist.init_process_group("gloo")
+r = dist.get_rank()
+t = torch.tensor([10.0 + 5.0 * r], dtype=torch.float64)
+dist.all_reduce(t, op=dist.ReduceOp.MAX)
+assert t.item() == 15.0
+dist.barrier()
+if r == 0: print("OK", dist.get_world_size())
+dist.destroy_process_group()
+'''
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    procs = []
+    for r in range(2):
+        e = dict(env, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r))
+        procs.append(subprocess.Popen([sys.executable, "-c", code], env=e, stdout=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=120)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs)
+    assert "OK 2" in outs[0]

@@ -231,3 +231,27 @@ def test_afs_infinite_thresholds():
                   test_indices=[2, 3], initial_count=8, e1_threshold=float("inf"), e2_threshold=float("inf"),
                   grid_points=512, time_points=128)
     assert r["converged"] and r["n_c"] == 11 and r["solver_calls"] == 11
+
+
+def test_afs_bem_identical_sequence():
+    """320-triangle sphere (cfg 1 mesh, T=20, eta=0.25) under the seeded random traction of
+    cfg 4 (the pressure load leaves tangential DOFs at pure rounding noise, which makes E2
+    noise-dominated — SURVEY.md A.4): product run_afs on the GPU BEM vs the reference
+    run_afs on the oracle BEM. Infinite thresholds keep the loop away from the reference
+    algorithm's rank-deficiency on this smooth response while exercising
+    J_c = 6 adaptive selections on BEM data."""
+    from paper_1511_04355_b200 import mesh
+
+    V, F = mesh.icosphere(2)
+    tr = mesh.random_traction(F.shape[0], seed=0)
+    pts = mesh.draw_indices(F.shape[0], 16, 0)
+    dofs = [3 * p + i for p in pts for i in range(3)]
+    kw = dict(omega_max=math.pi * 256 / 20.0, eta=0.25, period=20.0, initial_count=12,
+              e1_threshold=float("inf"), e2_threshold=float("inf"), validation_steps=6)
+    r = P.run_afs(P.BemSystem(V, F, tr, channels=dofs), **kw)
+    o = O.run_afs(O.System.bem(O.Bem(V, F, tr), dofs), **kw)
+    assert r["n_c"] == o["n_c"] == 18
+    np.testing.assert_array_equal(r["samples"], o["samples"])
+    np.testing.assert_array_equal(r["history"][:, :3], o["history"][:, :3])
+    np.testing.assert_allclose(r["history"][:, 7], o["history"][:, 7], rtol=1e-6)
+    assert worst_match(r["poles"], o["poles"]) < 1e-6
