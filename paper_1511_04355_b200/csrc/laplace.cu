@@ -140,7 +140,7 @@ __global__ void fsm_dft_kernel(int Ns, double eta, double dt, double invT, int K
 constexpr int RBM = 64, RBN = 64, RS = 68;  // tile (channels x times), padded stride
 
 __device__ __forceinline__ void dmma_r(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }

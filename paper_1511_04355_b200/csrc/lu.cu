@@ -12,7 +12,8 @@
 //                        candidate row; after the barrier each CTA picks the
 //                        winner, swaps/scales/updates its own rows.
 //   lu_swap_trsm_kernel  applies the panel's row swaps to the trailing columns
-//                        and solves U12 = L11^{-1} A12, 32-column strips in smem.
+//                        and solves U12 = L11^{-1} A12, 128-column strips in smem
+//                        (L11 is re-read once per strip from L2).
 //   lu_gemm_kernel       A22 -= L21 U12 as a complex GEMM on the FP64 tensor
 //                        pipe: four real mma.sync.m8n8k4.f64 (DMMA) products per
 //                        complex tile, 64x64 complex CTA tiles, cp.async
@@ -20,6 +21,8 @@
 // Row swaps are LAPACK-style inside a panel and LINPACK-style across panels
 // (earlier L columns are not permuted); lu_solve applies them in that order.
 #include <climits>
+#include <cstdlib>
+#include <string>
 
 #include "lu.cuh"
 
@@ -40,9 +43,7 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(ctr, 1u);
-        while (ld_acquire(ctr) < target) {
-        }
-        __threadfence();
+        while (ld_acquire(ctr) < target) __nanosleep(20);
     }
     __syncthreads();
 }
@@ -72,6 +73,9 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
     unsigned step = 0;
     const size_t sstride = 2 + 2 * NB;
     double* gslots = slots + static_cast<size_t>(g) * 2 * (P + 1) * sstride;
+    // compact (value, row) keys of the P candidates per parity, after all groups' rows
+    double2* gkeys = reinterpret_cast<double2*>(slots + static_cast<size_t>(G) * 2 * (P + 1) * sstride) +
+                     static_cast<size_t>(g) * 2 * P;
 
     for (int b = g; b < batch; b += G) {
         double* Are = A + static_cast<size_t>(b) * mstride;
@@ -117,8 +121,7 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
                     if (ov > v || (ov == v && oi < ri)) { v = ov; ri = oi; }
                 }
                 if (lane == 0) {
-                    myslot[0] = v;
-                    myslot[1] = static_cast<double>(ri);
+                    gkeys[par * P + p] = make_double2(v, static_cast<double>(ri));
                     s_lrow = ri;
                 }
                 __syncwarp();
@@ -141,10 +144,9 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
                 double bv = -1.0;
                 int bidx = INT_MAX, bw = 0;
                 for (int q = lane; q < P; q += 32) {
-                    const double* sl = gslots + (static_cast<size_t>(par) * (P + 1) + q) * sstride;
-                    const double v = __ldcg(sl);
-                    const int ri = static_cast<int>(__ldcg(sl + 1));
-                    if (v > bv || (v == bv && ri < bidx)) { bv = v; bidx = ri; bw = q; }
+                    const double2 kv = __ldcg(&gkeys[par * P + q]);
+                    const int ri = static_cast<int>(kv.y);
+                    if (kv.x > bv || (kv.x == bv && ri < bidx)) { bv = kv.x; bidx = ri; bw = q; }
                 }
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
@@ -202,10 +204,11 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
 }
 
 // ------------------------------------------------------------------ swaps + TRSM
-constexpr int kTrsmCols = 32;
+constexpr int kTrsmCols = 128;
+constexpr int kTrsmThreads = 512;
 
 template <int NB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kTrsmThreads)
 lu_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w,
                     const int* ipiv) {
     extern __shared__ double sm[];
@@ -291,7 +294,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
@@ -378,13 +381,19 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
                 fb_r[ni] = br[nn * GBS + kr];
                 fb_i[ni] = bi[nn * GBS + kr];
             }
+            // C - (ar + i ai)(br + i bi): two passes over the 16 tiles so that the
+            // two products accumulated into one register pair are 32 DMMAs apart.
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) {
-                    // C - (ar + i ai)(br + i bi)
                     dmma(acr[mi][ni][0], acr[mi][ni][1], na_r[mi], fb_r[ni]);
                     dmma(aci[mi][ni][0], aci[mi][ni][1], na_r[mi], fb_i[ni]);
+                }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {
                     dmma(acr[mi][ni][0], acr[mi][ni][1], fa_i[mi], fb_i[ni]);
                     dmma(aci[mi][ni][0], aci[mi][ni][1], na_i[mi], fb_r[ni]);
                 }
@@ -407,6 +416,161 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
                 }
             }
         }
+    }
+}
+
+// ------------------------------------------------------------------ TRSM via L11^{-1} (DMMA)
+// U12 = L11^{-1} P A12: the unit-lower 64x64 inverse is formed once per panel
+// and matrix (lu_l11_inverse_kernel), then every 64-column strip applies the
+// panel's row swaps in shared memory and multiplies by L11^{-1} on the FP64
+// tensor pipe (lu_swap_apply_kernel), replacing 63 dependent sweeps per strip.
+__global__ void __launch_bounds__(64)
+lu_l11_inverse_kernel(const double* A, size_t mstride, size_t plane, int ld, int k, double* linv) {
+    extern __shared__ double ism[];
+    double* lre = ism;              // [col m][row i], stride 65
+    double* lim = lre + 64 * 65;
+    double* xre = lim + 64 * 65;    // [row i][col c], stride 65
+    double* xim = xre + 64 * 65;
+    const int b = blockIdx.x, c = threadIdx.x;
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    for (int q = c; q < 64 * 64; q += 64) {
+        const int j = q / 64, i = q % 64;
+        const size_t gi = static_cast<size_t>(k + j) * ld + k + i;
+        lre[j * 65 + i] = Are[gi];
+        lim[j * 65 + i] = Aim[gi];
+    }
+    __syncthreads();
+    // column c of X = L^{-1}: X[c][c] = 1, X[i][c] = -sum_{m=c}^{i-1} L[i][m] X[m][c]
+    for (int i = 0; i < 64; ++i) {
+        double sr = 0.0, si = 0.0;
+        if (i > c) {
+            for (int m = c; m < i; ++m) {
+                const double a = lre[m * 65 + i], bb = lim[m * 65 + i];
+                const double yr = xre[m * 65 + c], yi = xim[m * 65 + c];
+                sr += a * yr - bb * yi;
+                si += a * yi + bb * yr;
+            }
+            sr = -sr;
+            si = -si;
+        } else if (i == c) {
+            sr = 1.0;
+        }
+        xre[i * 65 + c] = sr;
+        xim[i * 65 + c] = si;
+    }
+    double* out = linv + static_cast<size_t>(b) * 2 * 64 * 64;
+    for (int i = 0; i < 64; ++i) {
+        out[c * 64 + i] = xre[i * 65 + c];  // [col c][row i]
+        out[64 * 64 + c * 64 + i] = xim[i * 65 + c];
+    }
+}
+
+constexpr int SAS = 68;  // padded smem stride (≡ 4 mod 16 doubles)
+
+__global__ void __launch_bounds__(128)
+lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const int* ipiv,
+                     const double* linv) {
+    extern __shared__ __align__(16) double ssm[];
+    double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
+    double* Li = Lr + 64 * SAS;
+    double* Xr = Li + 64 * SAS;       // [n][kk]
+    double* Xi = Xr + 64 * SAS;
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int col0 = k + 64 + blockIdx.x * 64;
+    const int ncols = min(64, n - col0);
+    const double* L = linv + static_cast<size_t>(b) * 2 * 64 * 64;
+    for (int q = tid; q < 64 * 64; q += blockDim.x) {
+        const int kk = q / 64, m = q % 64;
+        Lr[kk * SAS + m] = L[kk * 64 + m];
+        Li[kk * SAS + m] = L[64 * 64 + kk * 64 + m];
+    }
+    for (int q = tid; q < 64 * 64; q += blockDim.x) {
+        const int nn = q / 64, kk = q % 64;
+        double vr = 0.0, vi = 0.0;
+        if (nn < ncols) {
+            const size_t gi = static_cast<size_t>(col0 + nn) * ld + k + kk;
+            vr = Are[gi];
+            vi = Aim[gi];
+        }
+        Xr[nn * SAS + kk] = vr;
+        Xi[nn * SAS + kk] = vi;
+    }
+    __syncthreads();
+    if (tid < ncols) {  // the panel's sequential row swaps, one column per thread
+        const size_t colbase = static_cast<size_t>(col0 + tid) * ld;
+        const int* pv = ipiv + static_cast<size_t>(b) * n;
+        for (int c = k; c < k + 64; ++c) {
+            const int r = pv[c];
+            if (r == c) continue;
+            const int lc = c - k;
+            if (r < k + 64) {
+                const int lr = r - k;
+                double t0 = Xr[tid * SAS + lc], t1 = Xi[tid * SAS + lc];
+                Xr[tid * SAS + lc] = Xr[tid * SAS + lr];
+                Xi[tid * SAS + lc] = Xi[tid * SAS + lr];
+                Xr[tid * SAS + lr] = t0;
+                Xi[tid * SAS + lr] = t1;
+            } else {
+                const double gr = Are[colbase + r], gi = Aim[colbase + r];
+                Are[colbase + r] = Xr[tid * SAS + lc];
+                Aim[colbase + r] = Xi[tid * SAS + lc];
+                Xr[tid * SAS + lc] = gr;
+                Xi[tid * SAS + lc] = gi;
+            }
+        }
+    }
+    __syncthreads();
+    const int wm = warp & 1, wn = warp >> 1;
+    double acr[4][4][2] = {}, aci[4][4][2] = {};
+#pragma unroll 4
+    for (int k4 = 0; k4 < 64; k4 += 4) {
+        const int kr = k4 + (lane & 3);
+        double ar[4], ai[4], an[4], br[4], bi[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int m = wm * 32 + mi * 8 + (lane >> 2);
+            ar[mi] = Lr[kr * SAS + m];
+            ai[mi] = Li[kr * SAS + m];
+            an[mi] = -ai[mi];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int nn = wn * 32 + ni * 8 + (lane >> 2);
+            br[ni] = Xr[nn * SAS + kr];
+            bi[ni] = Xi[nn * SAS + kr];
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                dmma(acr[mi][ni][0], acr[mi][ni][1], ar[mi], br[ni]);
+                dmma(aci[mi][ni][0], aci[mi][ni][1], ar[mi], bi[ni]);
+            }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                dmma(acr[mi][ni][0], acr[mi][ni][1], an[mi], bi[ni]);
+                dmma(aci[mi][ni][0], aci[mi][ni][1], ai[mi], br[ni]);
+            }
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int row = k + wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int cl = wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+                if (cl < ncols) {
+                    const size_t gi = static_cast<size_t>(col0 + cl) * ld + row;
+                    Are[gi] = acr[mi][ni][e];
+                    Aim[gi] = aci[mi][ni][e];
+                }
+            }
     }
 }
 
@@ -504,7 +668,8 @@ __global__ void lu_bwd_gemv_kernel(const double* A, size_t mstride, size_t plane
 
 // ------------------------------------------------------------------ host
 void LuWorkspace::ensure(int groups, int P, int nb) {
-    const size_t need = static_cast<size_t>(groups) * 2 * (P + 1) * (2 + 2 * nb) * sizeof(double);
+    const size_t need = static_cast<size_t>(groups) * 2 * (P + 1) * (2 + 2 * nb) * sizeof(double) +
+                        static_cast<size_t>(groups) * 2 * P * sizeof(double2);
     if (need > slot_bytes) {
         if (slots) cudaFree(slots);
         FDS_CUDA(cudaMalloc(&slots, need));
@@ -517,7 +682,26 @@ void LuWorkspace::ensure(int groups, int P, int nb) {
     }
 }
 
+double* LuWorkspace::linv(int batch) {
+    if (batch > linv_cap) {
+        if (linv_buf) cudaFree(linv_buf);
+        FDS_CUDA(cudaMalloc(&linv_buf, static_cast<size_t>(batch) * 2 * 64 * 64 * sizeof(double)));
+        linv_cap = batch;
+    }
+    return linv_buf;
+}
+
 void LuWorkspace::release() {
+    if (linv_buf) cudaFree(linv_buf);
+    linv_buf = nullptr;
+    linv_cap = 0;
+    calu.release();
+    if (calu.top) cudaFree(calu.top);
+    if (calu.disp) cudaFree(calu.disp);
+    if (calu.moves) cudaFree(calu.moves);
+    calu.top = calu.disp = nullptr;
+    calu.moves = nullptr;
+    calu.batch_cap = 0;
     if (slots) cudaFree(slots);
     if (counters) cudaFree(counters);
     slots = nullptr;
@@ -573,7 +757,7 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
 }
 
 template <int NB>
-void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
+void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv) {
     const int rest = pb.n - k - w;
     if (rest <= 0) return;
     static bool attr_set = false;
@@ -585,11 +769,27 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
                                       static_cast<int>(kGemmSmemDoubles * sizeof(double))));
         attr_set = true;
     }
-    dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
     cudaEvent_t te;
     profiler().begin(st, kProfLuTrsm, 0.0, te);
-    FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, 256, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
-               pb.ipiv);
+    if (NB == 64 && w == 64) {
+        const size_t asmem = 4 * 64 * SAS * sizeof(double);
+        const size_t ismem = 4 * 64 * 65 * sizeof(double);
+        static bool aset = false;
+        if (!aset) {
+            FDS_CUDA(cudaFuncSetAttribute(lu_swap_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(asmem)));
+            FDS_CUDA(cudaFuncSetAttribute(lu_l11_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(ismem)));
+            aset = true;
+        }
+        FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, 64, ismem, st, pb.A, pb.mstride, pb.plane, pb.ld, k, linv);
+        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, 64), pb.batch), 128, asmem, st, pb.A, pb.mstride,
+                   pb.plane, pb.n, pb.ld, k, pb.ipiv, linv);
+    } else {
+        dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
+        FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, kTrsmThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
+                   w, pb.ipiv);
+    }
     profiler().end(st, te, kProfLuTrsm, 4.0 * w * w * rest * pb.batch);
     dim3 gg(ceil_div(rest, GBM), ceil_div(rest, GBN), pb.batch);
     cudaEvent_t ge;
@@ -602,8 +802,25 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
 
 }  // namespace
 
+namespace {
+
+// Panel algorithm: barrier-per-column partial pivoting (default; measured
+// faster on B200 for both the 129-matrix N=3840 batch and the single N=15360
+// matrix) or tournament pivoting (FDSWEEP_PANEL=calu, lu_calu.cu).
+bool use_calu() {
+    static const bool v = [] {
+        const char* e = std::getenv("FDSWEEP_PANEL");
+        return e && std::string(e) == "calu";
+    }();
+    return v;
+}
+
+}  // namespace
+
 int lu_panel_width(int n) {
-    // NB = 64 unless the 64-wide panel of one matrix cannot live in the SMs' shared memory.
+    // NB = 64; the GEPP panel falls back to 32 when a 64-wide panel of one
+    // matrix cannot live in the SMs' shared memory.
+    if (use_calu()) return 64;
     const int sms = device_info().sms;
     return ceil_div(n, panel_rows_max<64>()) <= sms ? 64 : 32;
 }
@@ -613,12 +830,15 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     const int nb = lu_panel_width(pb.n);
     for (int k = 0; k < pb.n; k += nb) {
         const int w = std::min(nb, pb.n - k);
-        if (nb == 64) {
+        if (use_calu()) {
+            calu_panel_step(pb, ws.calu, k, w, st);
+            trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
+        } else if (nb == 64) {
             panel_step<64>(pb, ws, k, w, st);
-            trailing_step<64>(pb, k, w, st);
+            trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
         } else {
             panel_step<32>(pb, ws, k, w, st);
-            trailing_step<32>(pb, k, w, st);
+            trailing_step<32>(pb, k, w, st, nullptr);
         }
     }
 }

@@ -18,7 +18,26 @@ struct LuProblem {
     int* info = nullptr;  // [batch], 0 = ok, c+1 = first zero pivot
 };
 
+// Tournament-pivoting panel buffers (lu_calu.cu).
+struct CaluWorkspace {
+    int* cand_idx = nullptr;
+    int* cand_cnt = nullptr;
+    double* cand_val = nullptr;
+    unsigned* counters = nullptr;
+    size_t node_cap = 0;
+    double* top = nullptr;
+    double* disp = nullptr;
+    int* moves = nullptr;
+    int batch_cap = 0;
+    void ensure(int batch, int nodes);
+    void release();
+};
+
 struct LuWorkspace {
+    CaluWorkspace calu;
+    double* linv_buf = nullptr;  // [batch][2][64][64] L11^{-1} per panel
+    int linv_cap = 0;
+    double* linv(int batch);
     double* slots = nullptr;
     unsigned* counters = nullptr;
     size_t slot_bytes = 0;
@@ -35,5 +54,6 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st);
 // rhs[b*rstride + i], complex interleaved, overwritten with the solution.
 void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st);
 int lu_panel_width(int n);
+void calu_panel_step(const LuProblem& pb, CaluWorkspace& ws, int k, int w, cudaStream_t st);
 
 }  // namespace fdsb
