@@ -337,10 +337,28 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
     Ns = 512
     sk = eta + 1j * (2 * math.pi / Tper) * torch.arange(Ns // 2 + 1, device=dev, dtype=torch.float64)
     half = (res @ (1.0 / (sk[None, :] - poles[:, None]))).T.contiguous()  # (Nc, D)
-    del vals
+    vals_keep = vals
     t_fsm = best(lambda: P.api._check(L.fds_fsm_invert_device(
         ctypes.c_double(Tper), Ns, ctypes.c_double(eta), D, ctypes.c_void_p(half.data_ptr()), 1, ctypes.c_void_p(out_dev.data_ptr()),
         ctypes.byref(ms))))
+    # kernel-only device times (CUDA events around the launches, library profiler)
+    P.api._check(L.fds_profile_enable(1))
+    for _ in range(reps):
+        P.api._check(L.fds_vf_identify_residues_device(
+            J, D, s_np.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(vals_keep.data_ptr()), M,
+            ph.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(res_dev.data_ptr()), ctypes.byref(ms)))
+        P.api._check(L.fds_rational_invert_device(
+            M, ph.ctypes.data_as(ctypes.c_void_p), D, ctypes.c_void_p(res_dev.data_ptr()), T_steps,
+            tgrid.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(out_dev.data_ptr()), ctypes.byref(ms)))
+        P.api._check(L.fds_fsm_invert_device(
+            ctypes.c_double(Tper), Ns, ctypes.c_double(eta), D, ctypes.c_void_p(half.data_ptr()), 1,
+            ctypes.c_void_p(out_dev.data_ptr()), ctypes.byref(ms)))
+    kern = {}
+    for name, kind in (("residue", 5), ("rational", 6), ("fsm", 7)):
+        c, kms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        P.api._check(L.fds_profile_read(kind, ctypes.byref(c), ctypes.byref(kms), ctypes.byref(wk)))
+        kern[name] = kms.value / max(c.value, 1)
+    P.api._check(L.fds_profile_enable(0))
     hbm = 6543.4
     try:
         hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
@@ -350,16 +368,19 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
     b_res = D * (16.0 * J + 16.0 * M / 2)
     b_fsm = D * (16.0 * (Ns // 2 + 1) + 8.0 * Ns)
     f_rat = D * 2.0 * M * T_steps
+    kr, kt, kf = kern["residue"], kern["rational"], kern["fsm"]
     out = {
         "dofs": D, "J": J, "M": M, "time_steps": T_steps, "relocation_s": t_reloc,
-        "residue_id_ms": t_res, "residue_id_dof_per_s": D / (t_res * 1e-3),
-        "residue_id_gbs": b_res / (t_res * 1e-3) / 1e9, "residue_id_hbm_frac": b_res / (t_res * 1e-3) / 1e9 / hbm,
-        "rational_invert_ms": t_rat, "rational_invert_dof_per_s": D / (t_rat * 1e-3),
-        "rational_invert_tflops": f_rat / (t_rat * 1e-3) / 1e12,
-        "rational_invert_fp64_frac": f_rat / (t_rat * 1e-3) / 1e12 / fp64,
-        "fsm_ms": t_fsm, "fsm_dof_per_s": D / (t_fsm * 1e-3), "fsm_gbs": b_fsm / (t_fsm * 1e-3) / 1e9,
-        "fsm_hbm_frac": b_fsm / (t_fsm * 1e-3) / 1e9 / hbm,
-        "vf_fsm_dof_per_s": D / ((t_res + t_rat) * 1e-3),
+        "api_ms": {"residue_id": t_res, "rational_invert": t_rat, "fsm": t_fsm},
+        "kernel_ms": {"residue_id": kr, "rational_invert": kt, "fsm": kf},
+        "residue_id_dof_per_s": D / (kr * 1e-3), "residue_id_gbs": b_res / (kr * 1e-3) / 1e9,
+        "residue_id_hbm_frac": b_res / (kr * 1e-3) / 1e9 / hbm,
+        "rational_invert_dof_per_s": D / (kt * 1e-3), "rational_invert_tflops": f_rat / (kt * 1e-3) / 1e12,
+        "rational_invert_fp64_frac": f_rat / (kt * 1e-3) / 1e12 / fp64,
+        "fsm_dof_per_s": D / (kf * 1e-3), "fsm_gbs": b_fsm / (kf * 1e-3) / 1e9,
+        "fsm_hbm_frac": b_fsm / (kf * 1e-3) / 1e9 / hbm,
+        "vf_fsm_dof_per_s": D / ((kr + kt) * 1e-3),
+        "bytes_per_dof": {"residue_id": b_res / D, "fsm": b_fsm / D}, "flops_per_dof_rational": f_rat / D,
         "pinned": "Chebyshev J=40, Omega_s=1.2 max Im a, T=pi*512/Omega_s, eta=3ln10/T, torch CUDA seed 0",
     }
     return out

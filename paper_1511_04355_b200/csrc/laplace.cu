@@ -35,79 +35,97 @@ __device__ __forceinline__ cplx twiddle(int num, int den) {  // exp(+2πi num/de
 
 }  // namespace
 
+// Per-call tables (frequency/time only, shared by every DOF): window W_k,
+// conjugate-pack twiddle exp(2πi k/Ns), FFT twiddles exp(2πi j/L), and the
+// output weight e^{η n Δt}/T.
+__global__ void fsm_tables_kernel(int Ns, double eta, double dt, double invT, int hanning, double* win, cplx* post,
+                                  cplx* tw, double* wout) {
+    const int L = Ns / 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= L) {
+        double s, c;
+        sincospi(2.0 * i / Ns, &s, &c);
+        win[i] = hanning ? 0.5 * (1.0 + c) : 1.0;
+    }
+    if (i < L) post[i] = twiddle(i, Ns);
+    if (i < L / 2) tw[i] = twiddle(i, L);
+    if (i < Ns) wout[i] = exp(eta * i * dt) * invT;
+}
+
 __global__ void __launch_bounds__(kFsmTile * 32)
-fsm_c2r_kernel(int Ns, int log2L, double eta, double dt, double invT, int K, const cplx* __restrict__ half,
-               size_t sk, size_t si, int hanning, double* __restrict__ out) {
+fsm_c2r_kernel(int Ns, int log2L, int K, const cplx* __restrict__ half, size_t sk, size_t si,
+               const double* __restrict__ gwin, const cplx* __restrict__ gpost, const cplx* __restrict__ gtw,
+               const double* __restrict__ gwout, double* __restrict__ out) {
     extern __shared__ cplx fsm_sm[];
     const int L = Ns / 2, Nc = L + 1;
-    cplx* tile = fsm_sm;                     // [Nc][kFsmTile]
-    cplx* tw = tile + Nc * kFsmTile;         // [L/2] exp(2πi j/L)
-    cplx* post = tw + L / 2;                 // [L]   exp(2πi k/Ns)
-    cplx* buf = post + L;                    // [kFsmTile][2][L]
+    const int LP = L + L / 8;                  // padded FFT buffer length (index i + i/8)
+    cplx* tile = fsm_sm;                       // [kFsmTile][Nc]  (Nc odd: conflict-free both ways)
+    cplx* tw = tile + Nc * kFsmTile;           // [L/2]
+    cplx* post = tw + L / 2;                   // [L]
+    cplx* buf = post + L;                      // [kFsmTile][2][LP]
+    double* win = reinterpret_cast<double*>(buf + static_cast<size_t>(kFsmTile) * 2 * LP);  // [L+1]
+    double* wout = win + Nc;                   // [Ns]
     const int k0 = blockIdx.x * kFsmTile;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int j = tid; j < L / 2; j += blockDim.x) tw[j] = twiddle(j, L);
-    for (int j = tid; j < L; j += blockDim.x) post[j] = twiddle(j, Ns);
+    for (int j = tid; j < L / 2; j += blockDim.x) tw[j] = gtw[j];
+    for (int j = tid; j < L; j += blockDim.x) post[j] = gpost[j];
+    for (int j = tid; j < Nc; j += blockDim.x) win[j] = gwin[j];
+    for (int j = tid; j < Ns; j += blockDim.x) wout[j] = gwout[j];
     // coalesced tile load: consecutive threads -> consecutive DOFs (stride sk)
     for (int idx = tid; idx < Nc * kFsmTile; idx += blockDim.x) {
         const int i = idx / kFsmTile, d = idx % kFsmTile;
         const int k = k0 + d;
         cplx v = mk(0.0, 0.0);
-        if (k < K) v = half[static_cast<size_t>(k) * sk + static_cast<size_t>(i) * si];
-        tile[i * kFsmTile + d] = v;
+        if (k < K) {
+            const double2 h = __ldcs(reinterpret_cast<const double2*>(half + static_cast<size_t>(k) * sk + static_cast<size_t>(i) * si));
+            v = mk(h.x, h.y);
+        }
+        tile[d * Nc + i] = v;
     }
     __syncthreads();
     const int k = k0 + warp;
     if (k >= K) return;
-    cplx* a = buf + static_cast<size_t>(warp) * 2 * L;
-    cplx* b = a + L;
-    // X_k windowed + conjugate-filled; Z_k = (X_k + conj X_{L-k}) + i w^k (X_k - conj X_{L-k})
+    cplx* a = buf + static_cast<size_t>(warp) * 2 * LP;
+    cplx* b = a + LP;
+    const cplx* my = tile + warp * Nc;
+    // Z_k = (X_k + conj X_{L-k}) + i w^k (X_k - conj X_{L-k}),  X windowed and conjugate-filled
     for (int j = lane; j < L; j += 32) {
-        cplx xk = tile[j * kFsmTile + warp];
-        cplx xm = tile[(L - j) * kFsmTile + warp];
-        if (j == 0) xk.im = 0.0;  // k = 0 forced real (laplace.cpp:80)
-        if (j == 0) xm.im = 0.0;  // X_{N/2} forced real (laplace.cpp:81)
-        if (hanning) {
-            double s, c;
-            sincospi(2.0 * j / Ns, &s, &c);
-            const double wk = 0.5 * (1.0 + c);
-            sincospi(2.0 * (L - j) / Ns, &s, &c);
-            const double wm = 0.5 * (1.0 + c);
-            xk = xk * wk;
-            xm = xm * wm;
-        }
+        cplx xk = my[j];
+        cplx xm = my[L - j];
+        if (j == 0) { xk.im = 0.0; xm.im = 0.0; }  // k = 0 and N/2 forced real (laplace.cpp:80-81)
+        xk = xk * win[j];
+        xm = xm * win[L - j];
         const cplx cm = conjg(xm);
         const cplx sum = xk + cm, dif = xk - cm;
         const cplx p = post[j] * dif;
-        a[j] = mk(sum.re - p.im, sum.im + p.re);  // sum + i * p
+        a[j + (j >> 3)] = mk(sum.re - p.im, sum.im + p.re);
     }
     __syncwarp();
     // radix-2 Stockham inverse FFT of length L (exp(+2πi nk/L), unnormalised)
     int half_len = L / 2;
-    int stride = 1;
     for (int st = 0; st < log2L; ++st) {
+        const int lg = st;  // stride = 2^st
         for (int q = lane; q < L / 2; q += 32) {
-            const int j = q / stride, r = q % stride;  // j-th group, r-th element
-            const cplx u = a[j * stride + r];
-            const cplx v = a[(j + half_len) * stride + r];
-            const cplx w = tw[j * stride];
-            b[2 * j * stride + r] = u + v;
-            b[(2 * j + 1) * stride + r] = (u - v) * w;
+            const int j = q >> lg, r = q & ((1 << lg) - 1);
+            const int i0 = (j << lg) + r, i1 = ((j + half_len) << lg) + r;
+            const int o0 = ((2 * j) << lg) + r, o1 = ((2 * j + 1) << lg) + r;
+            const cplx u = a[i0 + (i0 >> 3)];
+            const cplx v = a[i1 + (i1 >> 3)];
+            const cplx w = tw[j << lg];
+            b[o0 + (o0 >> 3)] = u + v;
+            b[o1 + (o1 >> 3)] = (u - v) * w;
         }
         __syncwarp();
         cplx* t = a;
         a = b;
         b = t;
         half_len >>= 1;
-        stride <<= 1;
     }
     // x[2n] = Re z[n], x[2n+1] = Im z[n]; weight e^{η t}/T
-    double* o = out + static_cast<size_t>(k) * Ns;
+    double2* o = reinterpret_cast<double2*>(out + static_cast<size_t>(k) * Ns);
     for (int n = lane; n < L; n += 32) {
-        const cplx z = a[n];
-        const double t0 = (2 * n) * dt, t1 = (2 * n + 1) * dt;
-        o[2 * n] = z.re * exp(eta * t0) * invT;
-        o[2 * n + 1] = z.im * exp(eta * t1) * invT;
+        const cplx z = a[n + (n >> 3)];
+        __stcs(&o[n], make_double2(z.re * wout[2 * n], z.im * wout[2 * n + 1]));
     }
 }
 
@@ -146,61 +164,91 @@ __device__ __forceinline__ void dmma_r(double& c0, double& c1, double a, double 
 }
 
 // terms: nt entries of (m index, weight); Q = 2*nt padded to 4. E: [Q][T] real.
+// CTA = 64 channels x all T: the residue tile (As) is staged once, the shared
+// exponential table streams through a cp.async double buffer in 64-step chunks.
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
 __global__ void __launch_bounds__(128)
 rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, const double* __restrict__ term_w,
                   const cplx* __restrict__ res /*[m][K]*/, const double* __restrict__ E, double* __restrict__ out) {
-    extern __shared__ double rsm[];
-    double* As = rsm;            // [Q][RS]  (q, channel)
-    double* Bs = rsm + Q * RS;   // [Q][RS]  (q, time)
-    const int k0 = blockIdx.x * RBM, t0 = blockIdx.y * RBN;
+    extern __shared__ __align__(16) double rsm[];
+    double* As = rsm;                 // [Q][RS]  (q, channel)
+    double* Bs0 = rsm + Q * RS;       // [Q][RS]  (q, time) x 2 buffers
+    double* Bs1 = Bs0 + Q * RS;
+    const int k0 = blockIdx.x * RBM;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nchunks = (T + RBN - 1) / RBN;
+    const bool vec = (T % 2 == 0);
+    auto load_e = [&](double* Bs, int t0) {
+        for (int idx = tid; idx < Q * (RBN / 2); idx += blockDim.x) {
+            const int q = idx / (RBN / 2), c = 2 * (idx % (RBN / 2));
+            const int t = t0 + c;
+            if (vec && t + 1 < T) {
+                cp16(&Bs[q * RS + c], &E[static_cast<size_t>(q) * T + t]);
+            } else {
+                Bs[q * RS + c] = t < T ? E[static_cast<size_t>(q) * T + t] : 0.0;
+                Bs[q * RS + c + 1] = t + 1 < T ? E[static_cast<size_t>(q) * T + t + 1] : 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    load_e(Bs0, 0);
     for (int idx = tid; idx < (Q / 2) * RBM; idx += blockDim.x) {
         const int p = idx / RBM, c = idx % RBM;
         const int k = k0 + c;
         double re = 0.0, im = 0.0;
         if (p < nt && k < K) {
-            const cplx r = res[static_cast<size_t>(term_m[p]) * K + k];
-            re = term_w[p] * r.re;
-            im = -term_w[p] * r.im;
+            const double2 r = __ldcs(reinterpret_cast<const double2*>(res) + static_cast<size_t>(term_m[p]) * K + k);
+            re = term_w[p] * r.x;
+            im = -term_w[p] * r.y;
         }
         As[(2 * p) * RS + c] = re;
         As[(2 * p + 1) * RS + c] = im;
     }
-    for (int idx = tid; idx < Q * RBN; idx += blockDim.x) {
-        const int q = idx / RBN, c = idx % RBN;
-        const int t = t0 + c;
-        Bs[q * RS + c] = t < T ? E[static_cast<size_t>(q) * T + t] : 0.0;
-    }
-    __syncthreads();
     const int wm = warp & 1, wn = warp >> 1;
-    double acc[4][4][2] = {};
-    for (int q0 = 0; q0 < Q; q0 += 4) {
-        const int q = q0 + (lane & 3);
-        double fa[4], fb[4];
+    for (int ch = 0; ch < nchunks; ++ch) {
+        double* Bs = (ch & 1) ? Bs1 : Bs0;
+        if (ch + 1 < nchunks) {
+            load_e((ch & 1) ? Bs0 : Bs1, (ch + 1) * RBN);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();
+        double acc[4][4][2] = {};
+        for (int q0 = 0; q0 < Q; q0 += 4) {
+            const int q = q0 + (lane & 3);
+            double fa[4], fb[4];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) fa[mi] = As[q * RS + wm * 32 + mi * 8 + (lane >> 2)];
+            for (int mi = 0; mi < 4; ++mi) fa[mi] = As[q * RS + wm * 32 + mi * 8 + (lane >> 2)];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) fb[ni] = Bs[q * RS + wn * 32 + ni * 8 + (lane >> 2)];
+            for (int ni = 0; ni < 4; ++ni) fb[ni] = Bs[q * RS + wn * 32 + ni * 8 + (lane >> 2)];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma_r(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
-    }
+                for (int ni = 0; ni < 4; ++ni) dmma_r(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
+        }
+        const int t0 = ch * RBN;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-        const int k = k0 + wm * 32 + mi * 8 + (lane >> 2);
-        if (k >= K) continue;
+        for (int mi = 0; mi < 4; ++mi) {
+            const int k = k0 + wm * 32 + mi * 8 + (lane >> 2);
+            if (k >= K) continue;
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            const int t = t0 + wn * 32 + ni * 8 + 2 * (lane & 3);
-            double* o = out + static_cast<size_t>(k) * T + t;
-            if (t + 1 < T && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-                *reinterpret_cast<double2*>(o) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-            } else {
-                if (t < T) o[0] = acc[mi][ni][0];
-                if (t + 1 < T) o[1] = acc[mi][ni][1];
+            for (int ni = 0; ni < 4; ++ni) {
+                const int t = t0 + wn * 32 + ni * 8 + 2 * (lane & 3);
+                double* o = out + static_cast<size_t>(k) * T + t;
+                if (vec && t + 1 < T) {
+                    __stcs(reinterpret_cast<double2*>(o), make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+                } else {
+                    if (t < T) o[0] = acc[mi][ni][0];
+                    if (t + 1 < T) o[1] = acc[mi][ni][1];
+                }
             }
         }
+        __syncthreads();
     }
 }
 
@@ -263,7 +311,7 @@ void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int
     FDS_CUDA(cudaMemcpyAsync(dt, t.data(), T * sizeof(double), cudaMemcpyHostToDevice, st));
     FDS_CUDA(cudaMemcpyAsync(dtp, tp.data(), nt * sizeof(cplx), cudaMemcpyHostToDevice, st));
     FDS_LAUNCH(rat_table_kernel, ceil_div(Q * T, 256), 256, 0, st, Q, nt, T, dtp, dt, dE);
-    const size_t smem = 2 * static_cast<size_t>(Q) * RS * sizeof(double);
+    const size_t smem = 3 * static_cast<size_t>(Q) * RS * sizeof(double);
     if (smem > device_info().smem_optin - 1024) throw ValidationError("rational_invert: model order too large");
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
@@ -271,7 +319,7 @@ void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int
                                       static_cast<int>(smem)));
         attr = smem;
     }
-    dim3 g(ceil_div(K, RBM), ceil_div(T, RBN));
+    dim3 g(ceil_div(K, RBM));
     cudaEvent_t pe;
     profiler().begin(st, kProfRatInv, 0.0, pe);
     FDS_LAUNCH(rat_invert_kernel, g, 128, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev);
@@ -327,7 +375,8 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
     const bool pow2 = (L & (L - 1)) == 0;
     int log2L = 0;
     while ((1 << log2L) < L) ++log2L;
-    const size_t smem = (static_cast<size_t>(L + 1) * kFsmTile + L / 2 + L + static_cast<size_t>(kFsmTile) * 2 * L) * sizeof(cplx);
+    const size_t smem = (static_cast<size_t>(L + 1) * kFsmTile + L / 2 + L + static_cast<size_t>(kFsmTile) * 2 * (L + L / 8)) * sizeof(cplx) +
+                        (static_cast<size_t>(L + 1) + Ns) * sizeof(double);
     cudaEvent_t pe;
     profiler().begin(st, kProfFsm, 0.0, pe);
     if (pow2 && L >= 2 && smem <= device_info().smem_optin - 1024) {
@@ -337,8 +386,16 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
                                           static_cast<int>(smem)));
             attr = smem;
         }
-        FDS_LAUNCH(fsm_c2r_kernel, ceil_div(K, kFsmTile), kFsmTile * 32, smem, st, Ns, log2L, eta, dt, invT, K,
-                   half_dev, sk, si, hanning ? 1 : 0, out_dev);
+        auto& cx = VfContext::get();
+        double* tab = static_cast<double*>(cx.tab2.get(sizeof(double) * (4 * static_cast<size_t>(L) + 4 + Ns)));
+        double* win = tab;
+        cplx* post = reinterpret_cast<cplx*>(win + L + 2);
+        cplx* tw = post + L;
+        double* wout = reinterpret_cast<double*>(tw + L / 2 + 1);
+        FDS_LAUNCH(fsm_tables_kernel, ceil_div(Ns + 1, 256), 256, 0, st, Ns, eta, dt, invT, hanning ? 1 : 0, win, post,
+                   tw, wout);
+        FDS_LAUNCH(fsm_c2r_kernel, ceil_div(K, kFsmTile), kFsmTile * 32, smem, st, Ns, log2L, K, half_dev, sk, si, win,
+                   post, tw, wout, out_dev);
     } else {
         FDS_LAUNCH(fsm_dft_kernel, ceil_div(K * Ns, 256), 256, 0, st, Ns, eta, dt, invT, K, half_dev, sk, si,
                    hanning ? 1 : 0, out_dev);

@@ -297,6 +297,104 @@ vf_residue_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, con
     }
 }
 
+// identify_residues apply on the FP64 tensor pipe: X (M x K) = W (M x 2J) B (2J x K),
+// B[2j + part][k] = (Re, Im) of values[j][k]. CTA: 64 output rows (poles) x 64
+// channels, 4 warps of 32x32, the whole 2J reduction staged in smem.
+constexpr int kRmS = 68;
+__device__ __forceinline__ void dmma_v(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+template <int MT>
+__global__ void __launch_bounds__(128)
+vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
+                      cplx* __restrict__ res) {
+    // Persistent CTAs; W (the shared solve operator, M x 2J) staged once in smem
+    // as the A operand. Each warp owns 32 channels x up to 64 poles; its B
+    // fragments (Re/Im of values[j][k]) are read straight from HBM with a
+    // 4-step register prefetch (each 128 B line fully used), so the kernel
+    // streams values -> residues at HBM rate.
+    extern __shared__ double rsm2[];
+    const int Q = 2 * J, Qp = (Q + 3) & ~3;
+    double* As = rsm2;  // [Qp][kRmS], As[q][m] = W[m][q]  (M <= 64 per launch slice)
+    const int m0 = blockIdx.y * 64;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int idx = tid; idx < Qp * 64; idx += blockDim.x) {
+        const int m = idx / Qp, q = idx % Qp;
+        As[q * kRmS + m] = (m0 + m < M && q < Q) ? W[static_cast<size_t>(m0 + m) * Q + q] : 0.0;
+    }
+    __syncthreads();
+    const int mtiles = min(MT, (M - m0 + 7) / 8);
+    const double* vd = reinterpret_cast<const double*>(vals);
+    const int q_l = lane & 3, n_l = lane >> 2;
+    const int warps_total = gridDim.x * (blockDim.x >> 5);
+    for (int tile = blockIdx.x * (blockDim.x >> 5) + warp; tile * 32 < K; tile += warps_total) {
+        const int kb = tile * 32;
+        double acc[MT][4][2];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        // B fragment element for step q0: q = q0 + q_l -> j = q/2, part = q&1
+        auto bload = [&](int q0, double* fb) {
+            const int q = q0 + q_l;
+            const int j = q >> 1, part = q & 1;
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int k = kb + ni * 8 + n_l;
+                fb[ni] = (q < Q && k < K) ? __ldcs(vd + (static_cast<size_t>(j) * K + k) * 2 + part) : 0.0;
+            }
+        };
+        double fb0[4], fb1[4], fb2[4], fb3[4];
+        bload(0, fb0);
+        bload(4, fb1);
+        bload(8, fb2);
+        bload(12, fb3);
+        for (int q0 = 0; q0 < Qp; q0 += 4) {
+            double fb[4];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                fb[ni] = fb0[ni];
+                fb0[ni] = fb1[ni];
+                fb1[ni] = fb2[ni];
+                fb2[ni] = fb3[ni];
+            }
+            bload(q0 + 16, fb3);
+            const int q = q0 + q_l;
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi) {
+                if (mi < mtiles) {
+                    const double fa = As[q * kRmS + mi * 8 + n_l];
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) dmma_v(acc[mi][ni][0], acc[mi][ni][1], fa, fb[ni]);
+                }
+            }
+        }
+        // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
+        // the partner row sits 4 lanes away in the accumulator fragment.
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+            if (mi >= mtiles) break;
+            const int m = m0 + mi * 8 + n_l;
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double x = acc[mi][ni][e];
+                    const double y = __shfl_xor_sync(0xffffffffu, x, 4);
+                    const int k = kb + ni * 8 + 2 * q_l + e;
+                    if (m >= M || k >= K) continue;
+                    cplx r;
+                    if (m < 2 * P) r = (m % 2 == 0) ? mk(x, y) : mk(y, -x);
+                    else r = mk(x, 0.0);
+                    __stcs(reinterpret_cast<double2*>(res) + static_cast<size_t>(m) * K + k, make_double2(r.re, r.im));
+                }
+        }
+    }
+}
+
 __global__ void vf_rms_kernel(int J, int K, int M, const cplx* __restrict__ vals, const cplx* __restrict__ res,
                               const cplx* __restrict__ invd /*[m][j]*/, double* __restrict__ rms) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -567,10 +665,29 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
                                       static_cast<int>(smem)));
         attr = smem;
     }
-    dim3 g(ceil_div(K, kResThreads), ceil_div(M, kResChunk));
+    const int Qp = (2 * J + 3) & ~3;
+    const size_t msmem = static_cast<size_t>(Qp) * kRmS * sizeof(double);
     cudaEvent_t pe;
     profiler().begin(st, kProfVfResidue, 0.0, pe);
-    FDS_LAUNCH(vf_residue_kernel, g, kResThreads, smem, st, J, K, M, P, values_dev, dW, res_dev);
+    if (msmem <= device_info().smem_optin - 1024) {
+        const int ctas = std::min(ceil_div(K, 128), 4 * device_info().sms);
+        const int mt = std::min(8, ceil_div(M, 8));  // m-tiles of the first (largest) slice
+        auto go = [&](auto kern) {
+            static size_t mattr = 0;
+            if (msmem > 48 * 1024 && msmem > mattr) {
+                FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
+                mattr = msmem;
+            }
+            FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 128, msmem, st, J, K, M, P, values_dev, dW, res_dev);
+        };
+        if (mt <= 2) go(vf_residue_mma_kernel<2>);
+        else if (mt <= 4) go(vf_residue_mma_kernel<4>);
+        else if (mt <= 6) go(vf_residue_mma_kernel<6>);
+        else go(vf_residue_mma_kernel<8>);
+    } else {
+        dim3 g(ceil_div(K, kResThreads), ceil_div(M, kResChunk));
+        FDS_LAUNCH(vf_residue_kernel, g, kResThreads, smem, st, J, K, M, P, values_dev, dW, res_dev);
+    }
     // algorithmic bytes: values 16 J + unique residues 16 M/2 per channel
     profiler().end(st, pe, kProfVfResidue, static_cast<double>(K) * (16.0 * J + 8.0 * M));
     if (rms_dev) {
