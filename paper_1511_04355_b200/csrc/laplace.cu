@@ -18,6 +18,7 @@
 // construction, so the reference's realness check (laplace.cpp:119-121) cannot
 // fire for a conjugate-filled spectrum; it is therefore not re-evaluated.
 #include <cmath>
+#include <math.h>
 
 #include "vf.cuh"
 
@@ -48,7 +49,7 @@ __global__ void fsm_tables_kernel(int Ns, double eta, double dt, double invT, in
         win[i] = hanning ? 0.5 * (1.0 + c) : 1.0;
     }
     if (i < L) post[i] = twiddle(i, Ns);
-    if (i < L / 2) tw[i] = twiddle(i, L);
+    if (i < L) tw[i] = twiddle(i, L);
     if (i < Ns) wout[i] = exp(eta * i * dt) * invT;
 }
 
@@ -126,6 +127,145 @@ fsm_c2r_kernel(int Ns, int log2L, int K, const cplx* __restrict__ half, size_t s
     for (int n = lane; n < L; n += 32) {
         const cplx z = a[n + (n >> 3)];
         __stcs(&o[n], make_double2(z.re * wout[2 * n], z.im * wout[2 * n + 1]));
+    }
+}
+
+// ------------------------------------------------------------------ register FFT (L = 32 R)
+// One warp inverts two DOFs at a time: the pack Z_n, an L-point inverse DFT as
+// R-point DFTs in registers (n = 32 n1 + lane) x twiddle x 32-point DFTs across
+// lanes (xor-shuffle radix-2 stages), and the real unpacking. Spectra are staged
+// per warp in shared memory (2 DOFs x (L+1)); outputs go through a swizzled
+// staging buffer so the global stores are contiguous 16 B per lane.
+__constant__ double c_w16[16][2];  // exp(2πi j/16)
+
+__device__ __forceinline__ int brev5(int x) { return __brev(x) >> 27; }
+
+template <int R>
+__device__ __forceinline__ void reg_dft_inverse(cplx (&y)[R]) {
+    // radix-2 DIF on R registers; twiddle exp(2πi j/(2h)) = c_w16[j * 16/(2h)]
+#pragma unroll
+    for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            if ((j & h) == 0) {
+                const cplx a = y[j], b = y[j + h];
+                y[j] = a + b;
+                const int e = (j & (h - 1)) * (16 / (2 * h));
+                y[j + h] = (a - b) * mk(c_w16[e][0], c_w16[e][1]);
+            }
+        }
+    }
+    // output in bit-reversed register order -> natural
+    cplx t[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        int r = 0;
+#pragma unroll
+        for (int b = 1, q = R / 2; b < R; b <<= 1, q >>= 1)
+            if (j & b) r |= q;
+        t[r] = y[j];
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) y[j] = t[j];
+}
+
+template <int R>
+__global__ void __launch_bounds__(128)
+fsm_warp_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t si, const double* __restrict__ gwin,
+                const cplx* __restrict__ gpost, const cplx* __restrict__ gtw, const double* __restrict__ gwout,
+                double* __restrict__ out) {
+    constexpr int L = 32 * R, Ns = 2 * L, Nc = L + 1;
+    constexpr int OP = L + L / 32;  // swizzled staging length (double2 units)
+    extern __shared__ double fsm_w[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // per-CTA tables
+    double* win = fsm_w;                               // [Nc]
+    double2* wout2 = reinterpret_cast<double2*>(win + Nc + 1);  // [OP] swizzled (w[2k], w[2k+1])
+    cplx* post = reinterpret_cast<cplx*>(wout2 + OP);  // [L]
+    cplx* tile = post + L + warp * (2 * Nc + 2 * OP / 2 + 2);  // per warp: [2][Nc] spectra
+    double2* stg = reinterpret_cast<double2*>(tile + 2 * Nc);  // [OP] output staging
+    for (int j = threadIdx.x; j < Nc; j += blockDim.x) win[j] = gwin[j];
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        post[j] = gpost[j];
+        wout2[j + (j >> 5)] = make_double2(gwout[2 * j], gwout[2 * j + 1]);
+    }
+    __syncthreads();
+    // lane constants: twiddles exp(2πi lane k1 / L) and the 32-point stage twiddles
+    cplx twl[R];
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) twl[k1] = gtw[(lane * k1) % L];
+    cplx tws[5];
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+        const int h = 16 >> st;  // butterfly distance
+        tws[st] = gtw[(lane & (h - 1)) * (L / (2 * h))];
+    }
+    const int br = brev5(lane);
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int pair = blockIdx.x * (blockDim.x >> 5) + warp; 2 * pair < K; pair += nwarps) {
+        const int k0 = 2 * pair;
+        // stage 2 DOFs x Nc spectra (two adjacent DOFs share a 32 B sector in [i][k] layout)
+        for (int q = lane; q < 2 * Nc; q += 32) {
+            const int i = q >> 1, d = q & 1;
+            cplx v = mk(0.0, 0.0);
+            if (k0 + d < K) {
+                const double2 h2 = __ldcs(reinterpret_cast<const double2*>(half + static_cast<size_t>(k0 + d) * sk +
+                                                                          static_cast<size_t>(i) * si));
+                v = mk(h2.x, h2.y);
+            }
+            tile[d * Nc + i] = v;
+        }
+        __syncwarp();
+        for (int d = 0; d < 2; ++d) {
+            if (k0 + d >= K) break;
+            const cplx* X = tile + d * Nc;
+            cplx y[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const int n = lane + 32 * m;
+                cplx xk = X[n] * win[n];
+                cplx xm = X[L - n] * win[L - n];
+                if (n == 0) { xk.im = 0.0; xm.im = 0.0; }  // k = 0 and N/2 forced real
+                const cplx cm = conjg(xm);
+                const cplx sum = xk + cm, dif = xk - cm;
+                const cplx p = post[n] * dif;
+                y[m] = mk(sum.re - p.im, sum.im + p.re);
+            }
+            reg_dft_inverse<R>(y);
+#pragma unroll
+            for (int k1 = 0; k1 < R; ++k1) y[k1] = y[k1] * twl[k1];
+            // 32-point inverse DFT across lanes (DIF, result in bit-reversed lane order)
+#pragma unroll
+            for (int st = 0; st < 5; ++st) {
+                const int h = 16 >> st;
+                const bool upper = (lane & h) != 0;
+#pragma unroll
+                for (int k1 = 0; k1 < R; ++k1) {
+                    const double pr = __shfl_xor_sync(0xffffffffu, y[k1].re, h);
+                    const double pi = __shfl_xor_sync(0xffffffffu, y[k1].im, h);
+                    if (!upper) {
+                        y[k1] = mk(y[k1].re + pr, y[k1].im + pi);
+                    } else {
+                        y[k1] = mk(pr - y[k1].re, pi - y[k1].im) * tws[st];
+                    }
+                }
+            }
+            // lane holds z[k], k = k1 + R * brev5(lane); x[2k] = Re z, x[2k+1] = Im z
+#pragma unroll
+            for (int k1 = 0; k1 < R; ++k1) {
+                const int k = k1 + R * br;
+                const double2 w = wout2[k + (k >> 5)];
+                stg[k + (k >> 5)] = make_double2(y[k1].re * w.x, y[k1].im * w.y);
+            }
+            __syncwarp();
+            double2* o = reinterpret_cast<double2*>(out + static_cast<size_t>(k0 + d) * Ns);
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const int q = lane + 32 * m;
+                __stcs(&o[q], stg[q + (q >> 5)]);
+            }
+            __syncwarp();
+        }
     }
 }
 
@@ -387,15 +527,43 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
             attr = smem;
         }
         auto& cx = VfContext::get();
-        double* tab = static_cast<double*>(cx.tab2.get(sizeof(double) * (4 * static_cast<size_t>(L) + 4 + Ns)));
+        double* tab = static_cast<double*>(cx.tab2.get(sizeof(double) * (5 * static_cast<size_t>(L) + 4 + Ns)));
         double* win = tab;
         cplx* post = reinterpret_cast<cplx*>(win + L + 2);
         cplx* tw = post + L;
-        double* wout = reinterpret_cast<double*>(tw + L / 2 + 1);
+        double* wout = reinterpret_cast<double*>(tw + L);
         FDS_LAUNCH(fsm_tables_kernel, ceil_div(Ns + 1, 256), 256, 0, st, Ns, eta, dt, invT, hanning ? 1 : 0, win, post,
                    tw, wout);
-        FDS_LAUNCH(fsm_c2r_kernel, ceil_div(K, kFsmTile), kFsmTile * 32, smem, st, Ns, log2L, K, half_dev, sk, si, win,
-                   post, tw, wout, out_dev);
+        const int R = L / 32;
+        if (L % 32 == 0 && (R == 1 || R == 2 || R == 4 || R == 8 || R == 16)) {
+            static bool w16 = false;
+            if (!w16) {
+                double h[16][2];
+                for (int j = 0; j < 16; ++j) { h[j][0] = std::cos(2.0 * M_PI * j / 16); h[j][1] = std::sin(2.0 * M_PI * j / 16); }
+                FDS_CUDA(cudaMemcpyToSymbol(c_w16, h, sizeof(h)));
+                w16 = true;
+            }
+            const int OP = L + L / 32;
+            const size_t wsm = (static_cast<size_t>(L + 2) + 2 * OP + 2 * L) * sizeof(double) +
+                               4 * (2 * static_cast<size_t>(L + 1) + OP + 2) * sizeof(cplx);
+            const int ctas = std::min(ceil_div(ceil_div(K, 2), 4), 8 * device_info().sms);
+            auto go = [&](auto kern) {
+                static size_t a = 0;
+                if (wsm > 48 * 1024 && wsm > a) {
+                    FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
+                    a = wsm;
+                }
+                FDS_LAUNCH(kern, ctas, 128, wsm, st, K, half_dev, sk, si, win, post, tw, wout, out_dev);
+            };
+            if (R == 1) go(fsm_warp_kernel<1>);
+            else if (R == 2) go(fsm_warp_kernel<2>);
+            else if (R == 4) go(fsm_warp_kernel<4>);
+            else if (R == 8) go(fsm_warp_kernel<8>);
+            else go(fsm_warp_kernel<16>);
+        } else {
+            FDS_LAUNCH(fsm_c2r_kernel, ceil_div(K, kFsmTile), kFsmTile * 32, smem, st, Ns, log2L, K, half_dev, sk, si,
+                       win, post, tw, wout, out_dev);
+        }
     } else {
         FDS_LAUNCH(fsm_dft_kernel, ceil_div(K * Ns, 256), 256, 0, st, Ns, eta, dt, invT, K, half_dev, sk, si,
                    hanning ? 1 : 0, out_dev);
