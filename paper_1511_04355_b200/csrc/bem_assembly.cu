@@ -14,10 +14,11 @@
 //                    e != c; writes the 3x3 T̂ block of A (planar, column-major)
 //                    and a per-chunk partial of b = Û t.
 //   bem_near_kernel  one warp per listed near/self pair (host-built CSR, same
-//                    d/h rule as the oracle): 4^L x 7 subdivided points or the
-//                    polar self rule (3 x 10 x 10 + exact ln-CPV), lanes split
-//                    the points, shuffle-reduced in a fixed tree; overwrites the
-//                    A block and emits the b correction U_near·t − U_7pt·t.
+//                    d/h rule as the oracle) and 32 frequencies (lane = frequency):
+//                    4^L x 7 subdivided points or the polar self rule
+//                    (3 x 10 x 10 + exact ln-CPV), summed sequentially per lane;
+//                    overwrites the A block and emits the b correction
+//                    U_near·t − U_7pt·t.
 //   bem_rhs_kernel   b[3c+i] = p(s)·(Σ_chunks partial + Σ_near corrections).
 #include "bem.cuh"
 
@@ -141,6 +142,154 @@ bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __rest
 }
 
 // ------------------------------------------------------------------ near / self
+// One warp per listed near/self pair and 32 frequencies: lane b integrates the
+// whole pair for frequency b (the quadrature geometry is warp-uniform), so
+// there is no cross-lane reduction and all 32 lanes do useful work.
+__global__ void __launch_bounds__(128)
+bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __restrict__ trac,
+                int ne, const int* __restrict__ pairs, int npairs, const cplx* __restrict__ svec, int B,
+                double* __restrict__ A, size_t mstride, size_t plane, int ld,
+                cplx* __restrict__ corr, size_t cstride) {
+    const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.y * 32 + lane;
+    if (pair >= npairs) return;
+    const bool active = b < B;
+    const int c = pairs[3 * pair], e = pairs[3 * pair + 1], level = pairs[3 * pair + 2];
+    const cplx s = svec[active ? b : 0];
+    const double* g = geo + (size_t)e * 16;
+    const double x0 = geo[(size_t)c * 16 + 9], x1 = geo[(size_t)c * 16 + 10], x2 = geo[(size_t)c * 16 + 11];
+    const double n[3] = {g[12], g[13], g[14]};
+    const double t[3] = {trac[3 * e], trac[3 * e + 1], trac[3 * e + 2]};
+    cplx T[9], Ut[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) T[i] = mk(0.0, 0.0);
+    Ut[0] = Ut[1] = Ut[2] = mk(0.0, 0.0);
+
+    if (level < 0) {
+        // Self element: polar quadrature about the centroid over the 3 edge
+        // sub-triangles; static antisymmetric T part as the exact CPV.
+        const int NG = BemParams::kSelfGauss;
+        const cplx E10 = mk(P.E10, 0.0), E20 = mk(P.E20, 0.0);
+        for (int edge = 0; edge < 3; ++edge) {
+            const int ia = edge, ib = (edge + 1) % 3;
+            const double Px = g[3 * ia], Py = g[3 * ia + 1], Pz = g[3 * ia + 2];
+            const double Qx = g[3 * ib] - Px, Qy = g[3 * ib + 1] - Py, Qz = g[3 * ib + 2] - Pz;
+            const double L = sqrt(Qx * Qx + Qy * Qy + Qz * Qz);
+            const double cx = g[9], cy = g[10], cz = g[11];
+            const double wx = Px - cx, wy = Py - cy, wz = Pz - cz;
+            const double crx = wy * Qz - wz * Qy, cry = wz * Qx - wx * Qz, crz = wx * Qy - wy * Qx;
+            const double hperp = sqrt(crx * crx + cry * cry + crz * crz) / L;
+            for (int a = 0; a < NG; ++a) {
+                const double ta = P.glx[a];
+                const double dx = wx + ta * Qx, dy = wy + ta * Qy, dz = wz + ta * Qz;
+                const double R = sqrt(dx * dx + dy * dy + dz * dz);
+                const double ev[3] = {dx / R, dy / R, dz / R};
+                const double jt = hperp * L * P.glw[a];
+                const double lnR = log(R) / (R * R) * jt * (1.0 / (4.0 * kPi));
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        T[3 * i + j] = T[3 * i + j] + (E10 * (ev[j] * n[i]) + E20 * (ev[i] * n[j])) * lnR;
+                const double et = ev[0] * t[0] + ev[1] * t[1] + ev[2] * t[2];
+                for (int bq = 0; bq < NG; ++bq) {
+                    const double u = P.glx[bq];
+                    const double rho = R * u;
+                    cplx Aa, Bb, Cc, Dd;
+                    abcd(P, s * (rho * P.inv_cs), Aa, Bb, Cc, Dd);
+                    const double w = jt * P.glw[bq];
+                    const double fu = w * u / rho * P.inv_4pi_mu;
+                    const double ft = w * u / (rho * rho) * (1.0 / (4.0 * kPi));
+                    const cplx dE1 = (Cc - Bb) - E10;
+                    const cplx dE2 = P.lam_over_mu * (Cc - Dd - 2.0 * Bb) - 2.0 * Bb - E20;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] + (Aa * t[i] - Bb * (ev[i] * et)) * fu;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+#pragma unroll
+                        for (int j = 0; j < 3; ++j)
+                            T[3 * i + j] = T[3 * i + j] + (dE1 * (ev[j] * n[i]) + dE2 * (ev[i] * n[j])) * ft;
+                }
+            }
+        }
+    } else {
+        // Near element: 4^level sub-triangles (recursive midpoint split, children
+        // (p0,m01,m20), (m01,p1,m12), (m20,m12,p2), (m01,m12,m20)), 7 points each.
+        const int nsub = 1 << (2 * level);
+        for (int sub = 0; sub < nsub; ++sub) {
+            double p[3][3];
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) p[v][d] = g[3 * v + d];
+            for (int lv = level - 1; lv >= 0; --lv) {
+                const int child = (sub >> (2 * lv)) & 3;
+                double m01[3], m12[3], m20[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    m01[d] = 0.5 * (p[0][d] + p[1][d]);
+                    m12[d] = 0.5 * (p[1][d] + p[2][d]);
+                    m20[d] = 0.5 * (p[2][d] + p[0][d]);
+                }
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    if (child == 0) { p[1][d] = m01[d]; p[2][d] = m20[d]; }
+                    else if (child == 1) { p[0][d] = m01[d]; p[2][d] = m12[d]; }
+                    else if (child == 2) { p[0][d] = m20[d]; p[1][d] = m12[d]; }
+                    else { p[0][d] = m01[d]; p[1][d] = m12[d]; p[2][d] = m20[d]; }
+                }
+            }
+            const double ux = p[1][0] - p[0][0], uy = p[1][1] - p[0][1], uz = p[1][2] - p[0][2];
+            const double vx = p[2][0] - p[0][0], vy = p[2][1] - p[0][1], vz = p[2][2] - p[0][2];
+            const double cx = uy * vz - uz * vy, cy = uz * vx - ux * vz, cz = ux * vy - uy * vx;
+            const double area = 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+            for (int gq = 0; gq < 7; ++gq) {
+                const double l0 = P.r7l[gq][0], l1 = P.r7l[gq][1], l2 = P.r7l[gq][2];
+                const double yx = l0 * p[0][0] + l1 * p[1][0] + l2 * p[2][0];
+                const double yy = l0 * p[0][1] + l1 * p[1][1] + l2 * p[2][1];
+                const double yz = l0 * p[0][2] + l1 * p[1][2] + l2 * p[2][2];
+                accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area, T, Ut);
+            }
+        }
+        // subtract the far kernel's 7-point U·t for this pair (it is in the partials)
+        cplx Tdummy[9];
+        cplx Uf[3] = {mk(0, 0), mk(0, 0), mk(0, 0)};
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Tdummy[i] = mk(0.0, 0.0);
+        for (int gq = 0; gq < 7; ++gq) {
+            const double l0 = P.r7l[gq][0], l1 = P.r7l[gq][1], l2 = P.r7l[gq][2];
+            const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
+            const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
+            const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
+            accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * g[15], Tdummy, Uf);
+        }
+        Ut[0] = Ut[0] - Uf[0];
+        Ut[1] = Ut[1] - Uf[1];
+        Ut[2] = Ut[2] - Uf[2];
+    }
+    if (!active) return;
+    double* Are = A + (size_t)b * mstride;
+    double* Aim = Are + plane;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const size_t col = (size_t)(3 * e + j) * ld + 3 * c;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            cplx v = T[3 * i + j];
+            if (level < 0 && i == j) v.re += 0.5;
+            Are[col + i] = v.re;
+            Aim[col + i] = v.im;
+        }
+    }
+    cplx* cp = corr + (size_t)b * cstride + (size_t)pair * 3;
+    cp[0] = Ut[0];
+    cp[1] = Ut[1];
+    cp[2] = Ut[2];
+}
+
+// Few frequencies (B < 8): one warp per (pair, frequency), lanes split the
+// quadrature points and reduce with shuffles in a fixed tree.
 namespace {
 
 __device__ __forceinline__ void warp_sum(cplx* v, int count) {
@@ -156,7 +305,7 @@ __device__ __forceinline__ void warp_sum(cplx* v, int count) {
 }  // namespace
 
 __global__ void __launch_bounds__(128)
-bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __restrict__ trac,
+bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* __restrict__ trac,
                 int ne, const int* __restrict__ pairs, int npairs, const cplx* __restrict__ svec,
                 double* __restrict__ A, size_t mstride, size_t plane, int ld,
                 cplx* __restrict__ corr, size_t cstride) {
@@ -325,9 +474,15 @@ void bem_assemble(const BemDevice& d, const cplx* svec_dev, int B, double* A, si
     dim3 gf(ceil_div(ne, kFarThreads), nchunks, B);
     FDS_LAUNCH(bem_far_kernel, gf, kFarThreads, 0, st, d.params, d.geo, d.trac, ne, svec_dev, A,
                mstride, plane, ld, d.partial, d.pstride);
-    dim3 gn(ceil_div(d.npairs * 32, 128), B);
-    FDS_LAUNCH(bem_near_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.npairs,
-               svec_dev, A, mstride, plane, ld, d.corr, d.cstride);
+    if (B >= 8) {
+        dim3 gn(ceil_div(d.npairs, 4), ceil_div(B, 32));
+        FDS_LAUNCH(bem_near_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.npairs,
+                   svec_dev, B, A, mstride, plane, ld, d.corr, d.cstride);
+    } else {
+        dim3 gn(ceil_div(d.npairs * 32, 128), B);
+        FDS_LAUNCH(bem_near_pts_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.npairs,
+                   svec_dev, A, mstride, plane, ld, d.corr, d.cstride);
+    }
     dim3 gr(ceil_div(3 * ne, 128), B);
     FDS_LAUNCH(bem_rhs_kernel, gr, 128, 0, st, ne, nchunks, d.partial, d.pstride, d.near_ptr, d.corr,
                d.cstride, svec_dev, rhs, rstride);
