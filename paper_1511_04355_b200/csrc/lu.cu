@@ -574,6 +574,91 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
     }
 }
 
+// ------------------------------------------------------------------ 16-wide sub-panels
+// For batches the 64-wide panel is factored as four 16-wide sub-panels: a
+// 16-wide panel needs a quarter of the on-chip memory per matrix, so ~4x more
+// matrices run their latency-bound column steps concurrently. Between
+// sub-panels the remaining panel columns receive the sub-panel's row swaps, a
+// 16x16 unit-lower solve and a rank-16 update; the 64-wide panel then leaves
+// exactly the LAPACK-within-panel layout the trailing update and lu_solve use.
+constexpr int kSub = 16;
+
+__global__ void __launch_bounds__(64)
+lu_sub_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int ks,
+                        const int* ipiv) {
+    // thread = one column c of the 64-panel outside the current sub-panel
+    const int b = blockIdx.x;
+    const int c = k + threadIdx.x;
+    if (threadIdx.x >= w || (c >= ks && c < ks + kSub)) return;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const size_t cb = static_cast<size_t>(c) * ld;
+    const int* pv = ipiv + static_cast<size_t>(b) * n;
+    for (int i = ks; i < ks + kSub; ++i) {
+        const int r = pv[i];
+        if (r == i) continue;
+        const double tr = Are[cb + i], ti = Aim[cb + i];
+        Are[cb + i] = Are[cb + r];
+        Aim[cb + i] = Aim[cb + r];
+        Are[cb + r] = tr;
+        Aim[cb + r] = ti;
+    }
+    if (c < ks) return;  // columns left of the sub-panel hold L: swaps only
+    // U = L11s^{-1} x on rows ks..ks+15 (unit lower, from columns ks..ks+15)
+    double xr[kSub], xi[kSub];
+#pragma unroll
+    for (int i = 0; i < kSub; ++i) { xr[i] = Are[cb + ks + i]; xi[i] = Aim[cb + ks + i]; }
+#pragma unroll
+    for (int j = 0; j < kSub; ++j) {
+#pragma unroll
+        for (int i = j + 1; i < kSub; ++i) {
+            const size_t li = static_cast<size_t>(ks + j) * ld + ks + i;
+            const double lr = Are[li], lim = Aim[li];
+            xr[i] -= lr * xr[j] - lim * xi[j];
+            xi[i] -= lr * xi[j] + lim * xr[j];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kSub; ++i) { Are[cb + ks + i] = xr[i]; Aim[cb + ks + i] = xi[i]; }
+}
+
+__global__ void __launch_bounds__(128)
+lu_sub_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int ks) {
+    // rows r >= ks+16, columns [ks+16, k+w): A -= L21s (r, ks..ks+15) * U (ks..ks+15, col)
+    __shared__ double ur[kSub][48], ui[kSub][48];
+    const int b = blockIdx.y;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int c0 = ks + kSub, nc = k + w - c0;
+    for (int q = threadIdx.x; q < kSub * nc; q += blockDim.x) {
+        const int t = q % kSub, c = q / kSub;
+        const size_t gi = static_cast<size_t>(c0 + c) * ld + ks + t;
+        ur[t][c] = Are[gi];
+        ui[t][c] = Aim[gi];
+    }
+    __syncthreads();
+    const int r = ks + kSub + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double lr[kSub], li[kSub];
+#pragma unroll
+    for (int t = 0; t < kSub; ++t) {
+        const size_t gi = static_cast<size_t>(ks + t) * ld + r;
+        lr[t] = Are[gi];
+        li[t] = Aim[gi];
+    }
+    for (int c = 0; c < nc; ++c) {
+        const size_t gi = static_cast<size_t>(c0 + c) * ld + r;
+        double ar = Are[gi], ai = Aim[gi];
+#pragma unroll
+        for (int t = 0; t < kSub; ++t) {
+            ar -= lr[t] * ur[t][c] - li[t] * ui[t][c];
+            ai -= lr[t] * ui[t][c] + li[t] * ur[t][c];
+        }
+        Are[gi] = ar;
+        Aim[gi] = ai;
+    }
+}
+
 // ------------------------------------------------------------------ solves
 __global__ void lu_fwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld,
                                     int k, int w, const int* ipiv, cplx* rhs, size_t rstride) {
@@ -729,7 +814,6 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
     int P = ceil_div(rows, rmax);
     if (P > sms) throw NumericError("lu: panel does not fit in on-chip memory");
     const int R = ceil_div(rows, P);
-    const int G = std::max(1, std::min(pb.batch, sms / P));
     const size_t smem = panel_smem(NB, R);
     static size_t attr_smem = 0;
     if (smem > attr_smem) {
@@ -737,6 +821,10 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
                                       static_cast<int>(smem)));
         attr_smem = smem;
     }
+    int per_sm = 1;
+    FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_kernel<NB>, kPanelThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    const int G = std::max(1, std::min(pb.batch, (sms * per_sm) / P));
     ws.ensure(G, P, NB);
     FDS_CUDA(cudaMemsetAsync(ws.counters, 0, G * sizeof(unsigned), st));
     double* A = pb.A;
@@ -815,6 +903,18 @@ bool use_calu() {
     return v;
 }
 
+// 16-wide sub-panels pay off when several matrices share the GPU (more of
+// them fit on chip at once); a single matrix keeps the 64-wide panel.
+// FDSWEEP_SUBPANEL=0/1 overrides.
+bool use_subpanels(const LuProblem& pb) {
+    static const int env = [] {
+        const char* e = std::getenv("FDSWEEP_SUBPANEL");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (env >= 0) return env != 0;
+    return pb.batch >= 4;
+}
+
 }  // namespace
 
 int lu_panel_width(int n) {
@@ -832,6 +932,23 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
         const int w = std::min(nb, pb.n - k);
         if (use_calu()) {
             calu_panel_step(pb, ws.calu, k, w, st);
+            trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
+        } else if (nb == 64 && w == 64 && use_subpanels(pb)) {
+            cudaEvent_t pe;
+            profiler().begin(st, kProfLuPanel, 0.0, pe);
+            const bool keep = profiler().enabled;
+            profiler().enabled = false;  // account the sub-steps as one panel
+            for (int ks = k; ks < k + 64; ks += kSub) {
+                panel_step<kSub>(pb, ws, ks, kSub, st);
+                FDS_LAUNCH(lu_sub_swap_trsm_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
+                           w, ks, pb.ipiv);
+                if (ks + kSub < k + 64) {
+                    dim3 g(ceil_div(pb.n - ks - kSub, 128), pb.batch);
+                    FDS_LAUNCH(lu_sub_gemm_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks);
+                }
+            }
+            profiler().enabled = keep;
+            profiler().end(st, pe, kProfLuPanel, 8.0 * (pb.n - k) * w * w / 2.0 * pb.batch);
             trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
         } else if (nb == 64) {
             panel_step<64>(pb, ws, k, w, st);

@@ -30,6 +30,18 @@ def test_zgesv_batch_matches_lapack(n):
         assert rel_l2(x[b], np.linalg.solve(A[b], rhs[b])) < 1e-10
 
 
+@pytest.mark.parametrize("n", [64, 200, 517])
+def test_zgesv_batched_subpanels(n):
+    """batch >= 4 takes the 16-wide sub-panel path (random matrices: heavy pivoting)."""
+    rng = np.random.default_rng(100 + n)
+    B = 6
+    A = rng.normal(size=(B, n, n)) + 1j * rng.normal(size=(B, n, n))
+    rhs = rng.normal(size=(B, n)) + 1j * rng.normal(size=(B, n))
+    x = zgesv_batch(A, rhs)
+    for b in range(B):
+        assert rel_l2(x[b], np.linalg.solve(A[b], rhs[b])) < 1e-10
+
+
 def test_zgesv_large_needs_pivoting():
     rng = np.random.default_rng(7)
     n = 700
