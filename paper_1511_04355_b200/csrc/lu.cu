@@ -282,7 +282,9 @@ lu_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int 
 constexpr int GBM = 64, GBN = 64, GBK = 16, GSTAGES = 2;
 constexpr int GAS = GBM + 4;  // A tile row stride (doubles) ≡ 4 (mod 16): conflict-free fragments
 constexpr int GBS = GBK + 4;  // B tile row stride
-constexpr int kGemmThreads = 128;
+constexpr int kGemmThreads = 256;
+constexpr int GWM = 2, GWN = 4;                      // warp grid over the 64x64 tile
+constexpr int GMI = GBM / GWM / 8, GNI = GBN / GWN / 8;  // 8x8 DMMA tiles per warp
 constexpr int kGemmSmemDoubles = GSTAGES * 2 * (GBK * GAS + GBN * GBS);
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -308,7 +310,7 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
     const int m0 = k + w + blockIdx.x * GBM;  // first row of this tile
     const int n0 = k + w + blockIdx.y * GBN;  // first column
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp % GWM, wn = warp / GWM;
     auto As = [&](int st, int pl) { return gsm + (st * 2 + pl) * (GBK * GAS); };
     auto Bs = [&](int st, int pl) { return gsm + GSTAGES * 2 * (GBK * GAS) + (st * 2 + pl) * (GBN * GBS); };
 
@@ -340,15 +342,15 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
     cp_async_commit();
     // Accumulators start from C (loads overlap the first A/B stage); the
     // mainloop subtracts L21 U12 and the epilogue is a plain store.
-    double acr[4][4][2], aci[4][4][2];
+    double acr[GMI][GNI][2], aci[GMI][GNI][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-        const int row = m0 + wm * 32 + mi * 8 + (lane >> 2);
+    for (int mi = 0; mi < GMI; ++mi) {
+        const int row = m0 + wm * (GBM / GWM) + mi * 8 + (lane >> 2);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < GNI; ++ni)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int col = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+                const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
                 const size_t gi = static_cast<size_t>(col) * ld + row;
                 acr[mi][ni][e] = Are[gi];
                 aci[mi][ni][e] = Aim[gi];
@@ -366,34 +368,34 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
         const double* bi = Bs(st, 1);
 #pragma unroll
         for (int k4 = 0; k4 < GBK; k4 += 4) {
-            double na_r[4], fa_i[4], na_i[4], fb_r[4], fb_i[4];
+            double na_r[GMI], fa_i[GMI], na_i[GMI], fb_r[GNI], fb_i[GNI];
             const int kr = k4 + (lane & 3);
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) {
-                const int m = wm * 32 + mi * 8 + (lane >> 2);
+            for (int mi = 0; mi < GMI; ++mi) {
+                const int m = wm * (GBM / GWM) + mi * 8 + (lane >> 2);
                 na_r[mi] = -ar[kr * GAS + m];
                 fa_i[mi] = ai[kr * GAS + m];
                 na_i[mi] = -fa_i[mi];
             }
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int nn = wn * 32 + ni * 8 + (lane >> 2);
+            for (int ni = 0; ni < GNI; ++ni) {
+                const int nn = wn * (GBN / GWN) + ni * 8 + (lane >> 2);
                 fb_r[ni] = br[nn * GBS + kr];
                 fb_i[ni] = bi[nn * GBS + kr];
             }
             // C - (ar + i ai)(br + i bi): two passes over the 16 tiles so that the
             // two products accumulated into one register pair are 32 DMMAs apart.
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < GMI; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) {
+                for (int ni = 0; ni < GNI; ++ni) {
                     dmma(acr[mi][ni][0], acr[mi][ni][1], na_r[mi], fb_r[ni]);
                     dmma(aci[mi][ni][0], aci[mi][ni][1], na_r[mi], fb_i[ni]);
                 }
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < GMI; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) {
+                for (int ni = 0; ni < GNI; ++ni) {
                     dmma(acr[mi][ni][0], acr[mi][ni][1], fa_i[mi], fb_i[ni]);
                     dmma(aci[mi][ni][0], aci[mi][ni][1], na_i[mi], fb_r[ni]);
                 }
@@ -402,13 +404,13 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
     }
     // epilogue: store C - L21 U12
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-        const int row = m0 + wm * 32 + mi * 8 + (lane >> 2);
+    for (int mi = 0; mi < GMI; ++mi) {
+        const int row = m0 + wm * (GBM / GWM) + mi * 8 + (lane >> 2);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < GNI; ++ni) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int col = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+                const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
                 if (row < n && col < n) {
                     const size_t gi = static_cast<size_t>(col) * ld + row;
                     Are[gi] = acr[mi][ni][e];
