@@ -905,16 +905,16 @@ bool use_calu() {
     return v;
 }
 
-// 16-wide sub-panels pay off when several matrices share the GPU (more of
-// them fit on chip at once); a single matrix keeps the 64-wide panel.
-// FDSWEEP_SUBPANEL=0/1 overrides.
+// 16-wide sub-panels: for batches ~4x more matrices fit on chip at once
+// (cfg2 panel 225 -> 77 ms); for a single matrix the narrower rank-1 updates
+// still win (N=15360 panel 107 -> 97 ms). FDSWEEP_SUBPANEL=0/1 overrides.
 bool use_subpanels(const LuProblem& pb) {
     static const int env = [] {
         const char* e = std::getenv("FDSWEEP_SUBPANEL");
         return e ? std::atoi(e) : -1;
     }();
     if (env >= 0) return env != 0;
-    return pb.batch >= 4;
+    return pb.batch >= 1;
 }
 
 }  // namespace
