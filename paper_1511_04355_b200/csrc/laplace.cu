@@ -182,8 +182,8 @@ fsm_warp_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t si, cons
     double* win = fsm_w;                               // [Nc]
     double2* wout2 = reinterpret_cast<double2*>(win + Nc + 1);  // [OP] swizzled (w[2k], w[2k+1])
     cplx* post = reinterpret_cast<cplx*>(wout2 + OP);  // [L]
-    cplx* tile = post + L + warp * (2 * Nc + 2 * OP / 2 + 2);  // per warp: [2][Nc] spectra
-    double2* stg = reinterpret_cast<double2*>(tile + 2 * Nc);  // [OP] output staging
+    cplx* wbase = post + L + warp * (4 * Nc + OP + 2);  // per warp: 2 buffers x [2][Nc] spectra + staging
+    double2* stg = reinterpret_cast<double2*>(wbase + 4 * Nc);  // [OP] output staging
     for (int j = threadIdx.x; j < Nc; j += blockDim.x) win[j] = gwin[j];
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
         post[j] = gpost[j];
@@ -202,18 +202,30 @@ fsm_warp_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t si, cons
     }
     const int br = brev5(lane);
     const int nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int pair = blockIdx.x * (blockDim.x >> 5) + warp; 2 * pair < K; pair += nwarps) {
-        const int k0 = 2 * pair;
-        // stage 2 DOFs x Nc spectra (two adjacent DOFs share a 32 B sector in [i][k] layout)
+    // stage 2 DOFs x Nc spectra with cp.async (two adjacent DOFs share a 32 B
+    // sector in the [i][k] layout); the next pair streams in while this one computes
+    auto stage = [&](int pr, cplx* buf) {
+        const int kk0 = 2 * pr;
         for (int q = lane; q < 2 * Nc; q += 32) {
             const int i = q >> 1, d = q & 1;
-            cplx v = mk(0.0, 0.0);
-            if (k0 + d < K) {
-                const double2 h2 = __ldcs(reinterpret_cast<const double2*>(half + static_cast<size_t>(k0 + d) * sk +
-                                                                          static_cast<size_t>(i) * si));
-                v = mk(h2.x, h2.y);
-            }
-            tile[d * Nc + i] = v;
+            const bool ok = kk0 + d < K;
+            const cplx* src = ok ? half + static_cast<size_t>(kk0 + d) * sk + static_cast<size_t>(i) * si : half;
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(buf + d * Nc + i));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    int pair = blockIdx.x * (blockDim.x >> 5) + warp;
+    int bufi = 0;
+    if (2 * pair < K) stage(pair, wbase);
+    for (; 2 * pair < K; pair += nwarps, bufi ^= 1) {
+        const int k0 = 2 * pair;
+        cplx* tile = wbase + bufi * 2 * Nc;
+        if (2 * (pair + nwarps) < K) {
+            stage(pair + nwarps, wbase + (bufi ^ 1) * 2 * Nc);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncwarp();
         for (int d = 0; d < 2; ++d) {
@@ -545,7 +557,7 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
             }
             const int OP = L + L / 32;
             const size_t wsm = (static_cast<size_t>(L + 2) + 2 * OP + 2 * L) * sizeof(double) +
-                               4 * (2 * static_cast<size_t>(L + 1) + OP + 2) * sizeof(cplx);
+                               4 * (4 * static_cast<size_t>(L + 1) + OP + 2) * sizeof(cplx);
             const int ctas = std::min(ceil_div(ceil_div(K, 2), 4), 8 * device_info().sms);
             auto go = [&](auto kern) {
                 static size_t a = 0;

@@ -627,7 +627,7 @@ lu_sub_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, 
 __global__ void __launch_bounds__(128)
 lu_sub_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int ks) {
     // rows r >= ks+16, columns [ks+16, k+w): A -= L21s (r, ks..ks+15) * U (ks..ks+15, col)
-    __shared__ double ur[kSub][48], ui[kSub][48];
+    __shared__ double ur[kSub][64 - kSub], ui[kSub][64 - kSub];
     const int b = blockIdx.y;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;

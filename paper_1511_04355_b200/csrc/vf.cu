@@ -307,6 +307,9 @@ __device__ __forceinline__ void dmma_v(double& c0, double& c1, double a, double 
         : "d"(a), "d"(b));
 }
 
+constexpr int kResNI = 2;  // 8-channel sub-tiles per warp (16 channels): low registers, many warps
+constexpr int kResPF = 8;  // q-steps of B fragments prefetched per warp
+
 template <int MT>
 __global__ void __launch_bounds__(128)
 vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
@@ -330,45 +333,43 @@ vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
     const double* vd = reinterpret_cast<const double*>(vals);
     const int q_l = lane & 3, n_l = lane >> 2;
     const int warps_total = gridDim.x * (blockDim.x >> 5);
-    for (int tile = blockIdx.x * (blockDim.x >> 5) + warp; tile * 32 < K; tile += warps_total) {
-        const int kb = tile * 32;
-        double acc[MT][4][2];
+    for (int tile = blockIdx.x * (blockDim.x >> 5) + warp; tile * (8 * kResNI) < K; tile += warps_total) {
+        const int kb = tile * (8 * kResNI);
+        double acc[MT][kResNI][2];
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+            for (int ni = 0; ni < kResNI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
         // B fragment element for step q0: q = q0 + q_l -> j = q/2, part = q&1
         auto bload = [&](int q0, double* fb) {
             const int q = q0 + q_l;
             const int j = q >> 1, part = q & 1;
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
+            for (int ni = 0; ni < kResNI; ++ni) {
                 const int k = kb + ni * 8 + n_l;
                 fb[ni] = (q < Q && k < K) ? __ldcs(vd + (static_cast<size_t>(j) * K + k) * 2 + part) : 0.0;
             }
         };
-        double fb0[4], fb1[4], fb2[4], fb3[4];
-        bload(0, fb0);
-        bload(4, fb1);
-        bload(8, fb2);
-        bload(12, fb3);
-        for (int q0 = 0; q0 < Qp; q0 += 4) {
-            double fb[4];
+        // register ring of kResPF B-fragment steps in flight
+        double ring[kResPF][kResNI];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                fb[ni] = fb0[ni];
-                fb0[ni] = fb1[ni];
-                fb1[ni] = fb2[ni];
-                fb2[ni] = fb3[ni];
+        for (int p = 0; p < kResPF; ++p) bload(4 * p, ring[p]);
+        for (int q0 = 0; q0 < Qp; q0 += 4) {
+            double fb[kResNI];
+#pragma unroll
+            for (int ni = 0; ni < kResNI; ++ni) {
+                fb[ni] = ring[0][ni];
+#pragma unroll
+                for (int p = 0; p + 1 < kResPF; ++p) ring[p][ni] = ring[p + 1][ni];
             }
-            bload(q0 + 16, fb3);
+            bload(q0 + 4 * kResPF, ring[kResPF - 1]);
             const int q = q0 + q_l;
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi) {
                 if (mi < mtiles) {
                     const double fa = As[q * kRmS + mi * 8 + n_l];
 #pragma unroll
-                    for (int ni = 0; ni < 4; ++ni) dmma_v(acc[mi][ni][0], acc[mi][ni][1], fa, fb[ni]);
+                    for (int ni = 0; ni < kResNI; ++ni) dmma_v(acc[mi][ni][0], acc[mi][ni][1], fa, fb[ni]);
                 }
             }
         }
@@ -379,7 +380,7 @@ vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
             if (mi >= mtiles) break;
             const int m = m0 + mi * 8 + n_l;
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni)
+            for (int ni = 0; ni < kResNI; ++ni)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const double x = acc[mi][ni][e];
@@ -670,7 +671,7 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
     cudaEvent_t pe;
     profiler().begin(st, kProfVfResidue, 0.0, pe);
     if (msmem <= device_info().smem_optin - 1024) {
-        const int ctas = std::min(ceil_div(K, 128), 4 * device_info().sms);
+        const int ctas = std::min(ceil_div(K, 4 * 8 * kResNI), 8 * device_info().sms);
         const int mt = std::min(8, ceil_div(M, 8));  // m-tiles of the first (largest) slice
         auto go = [&](auto kern) {
             static size_t mattr = 0;
