@@ -809,7 +809,7 @@ int panel_rows_max() {
 }
 
 template <int NB>
-void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t st) {
+void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t st, bool coop = true) {
     const int sms = device_info().sms;
     const int rows = pb.n - k;
     const int rmax = panel_rows_max<NB>();
@@ -840,14 +840,24 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
     void* args[] = {&A, &mstride, &plane, &n, &ld, &batch, &kk, &ww, &PP, &RR, &GG, &ipiv, &info, &slots, &counters};
     cudaEvent_t pe;
     profiler().begin(st, kProfLuPanel, 0.0, pe);
-    FDS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_panel_kernel<NB>), dim3(G * P),
-                                         dim3(kPanelThreads), args, smem, st));
+    if (coop) {
+        FDS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_panel_kernel<NB>), dim3(G * P),
+                                             dim3(kPanelThreads), args, smem, st));
+    } else {
+        // Pipelined mode: launched next to the other half-batch's GEMM on a
+        // high-priority stream. G*P never exceeds what an idle GPU holds, and the
+        // concurrent GEMM CTAs always retire, so every group's CTAs become
+        // resident eventually; the CTA scheduler places these first.
+        lu_panel_kernel<NB><<<G * P, kPanelThreads, smem, st>>>(A, mstride, plane, n, ld, batch, kk, ww, PP, RR, GG,
+                                                                ipiv, info, slots, counters);
+        FDS_CUDA(cudaGetLastError());
+    }
     profiler().end(st, pe, kProfLuPanel, 8.0 * rows * w * w / 2.0 * pb.batch);
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 template <int NB>
-void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv) {
+void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv) {
     const int rest = pb.n - k - w;
     if (rest <= 0) return;
     static bool attr_set = false;
@@ -855,8 +865,6 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* l
     if (!attr_set) {
         FDS_CUDA(cudaFuncSetAttribute(lu_swap_trsm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
-        FDS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kGemmSmemDoubles * sizeof(double))));
         attr_set = true;
     }
     cudaEvent_t te;
@@ -881,6 +889,17 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* l
                    w, pb.ipiv);
     }
     profiler().end(st, te, kProfLuTrsm, 4.0 * w * w * rest * pb.batch);
+}
+
+void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
+    const int rest = pb.n - k - w;
+    if (rest <= 0) return;
+    static bool gset = false;
+    if (!gset) {
+        FDS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kGemmSmemDoubles * sizeof(double))));
+        gset = true;
+    }
     dim3 gg(ceil_div(rest, GBM), ceil_div(rest, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
@@ -888,6 +907,12 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* l
                pb.plane, pb.n, pb.ld, k, w);
     // algorithmic flops of A22 -= L21 U12 (complex): 8 * rest^2 * w per matrix
     profiler().end(st, ge, kProfLuGemm, 8.0 * rest * rest * w * pb.batch);
+}
+
+template <int NB>
+void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv) {
+    trsm_step<NB>(pb, k, w, st, linv);
+    gemm_step(pb, k, w, st);
 }
 
 }  // namespace
@@ -927,8 +952,92 @@ int lu_panel_width(int n) {
     return ceil_div(n, panel_rows_max<64>()) <= sms ? 64 : 32;
 }
 
+namespace {
+
+void subpanel_block(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t st, bool coop) {
+    cudaEvent_t pe;
+    profiler().begin(st, kProfLuPanel, 0.0, pe);
+    const bool keep = profiler().enabled;
+    profiler().enabled = false;  // account the sub-steps as one panel
+    for (int ks = k; ks < k + 64; ks += kSub) {
+        panel_step<kSub>(pb, ws, ks, kSub, st, coop);
+        FDS_LAUNCH(lu_sub_swap_trsm_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks,
+                   pb.ipiv);
+        if (ks + kSub < k + 64) {
+            dim3 g(ceil_div(pb.n - ks - kSub, 128), pb.batch);
+            FDS_LAUNCH(lu_sub_gemm_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks);
+        }
+    }
+    profiler().enabled = keep;
+    profiler().end(st, pe, kProfLuPanel, 8.0 * (pb.n - k) * w * w / 2.0 * pb.batch);
+}
+
+bool use_pipeline(const LuProblem& pb) {
+    static const int env = [] {
+        const char* e = std::getenv("FDSWEEP_PIPELINE");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (env >= 0) return env != 0 && pb.batch >= 2;
+    // Off by default: measured on B200 the co-scheduled panels slow the GEMM
+    // half (RF/smem sharing) more than they hide (cfg2 LU 745 -> 789 ms).
+    return false;
+}
+
+// Opt-in (FDSWEEP_PIPELINE=1). Batched factorization as two half-batches in flight: the panels and
+// swap+TRSM of one half run on a high-priority stream while the other half's
+// trailing GEMM occupies the tensor pipes on a low-priority stream, so the
+// latency-bound panel work hides behind the compute-bound GEMM.
+void lu_factor_pipelined(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
+    static cudaStream_t s_hi = nullptr, s_lo = nullptr;
+    static cudaEvent_t ev[8];
+    if (!s_hi) {
+        int lo = 0, hi = 0;
+        FDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FDS_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, hi));
+        FDS_CUDA(cudaStreamCreateWithPriority(&s_lo, cudaStreamNonBlocking, lo));
+        for (auto& e : ev) FDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaEvent_t ev_start = ev[0], ev_hi_end = ev[1], ev_lo_end = ev[2];
+    cudaEvent_t ev_trsm[2] = {ev[3], ev[4]}, ev_gemm[2] = {ev[5], ev[6]};
+    const int b0 = pb.batch / 2;
+    LuProblem ph[2] = {pb, pb};
+    ph[0].batch = b0;
+    ph[1].batch = pb.batch - b0;
+    ph[1].A = pb.A + static_cast<size_t>(b0) * pb.mstride;
+    ph[1].ipiv = pb.ipiv + static_cast<size_t>(b0) * pb.n;
+    ph[1].info = pb.info + b0;
+    double* linv_all = ws.linv(pb.batch);
+    double* linv[2] = {linv_all, linv_all + static_cast<size_t>(b0) * 2 * 64 * 64};
+    FDS_CUDA(cudaEventRecord(ev_start, st));
+    FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_start, 0));
+    FDS_CUDA(cudaStreamWaitEvent(s_lo, ev_start, 0));
+    for (int k = 0; k < pb.n; k += 64) {
+        const int w = std::min(64, pb.n - k);
+        for (int h = 0; h < 2; ++h) {
+            if (k > 0) FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_gemm[h], 0));
+            if (w == 64) subpanel_block(ph[h], ws, k, w, s_hi, false);
+            else panel_step<64>(ph[h], ws, k, w, s_hi, false);
+            trsm_step<64>(ph[h], k, w, s_hi, linv[h]);
+            FDS_CUDA(cudaEventRecord(ev_trsm[h], s_hi));
+            FDS_CUDA(cudaStreamWaitEvent(s_lo, ev_trsm[h], 0));
+            gemm_step(ph[h], k, w, s_lo);
+            FDS_CUDA(cudaEventRecord(ev_gemm[h], s_lo));
+        }
+    }
+    FDS_CUDA(cudaEventRecord(ev_hi_end, s_hi));
+    FDS_CUDA(cudaEventRecord(ev_lo_end, s_lo));
+    FDS_CUDA(cudaStreamWaitEvent(st, ev_hi_end, 0));
+    FDS_CUDA(cudaStreamWaitEvent(st, ev_lo_end, 0));
+}
+
+}  // namespace
+
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     FDS_CUDA(cudaMemsetAsync(pb.info, 0, pb.batch * sizeof(int), st));
+    if (!use_calu() && lu_panel_width(pb.n) == 64 && use_pipeline(pb)) {
+        lu_factor_pipelined(pb, ws, st);
+        return;
+    }
     const int nb = lu_panel_width(pb.n);
     for (int k = 0; k < pb.n; k += nb) {
         const int w = std::min(nb, pb.n - k);
@@ -936,21 +1045,7 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
             calu_panel_step(pb, ws.calu, k, w, st);
             trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
         } else if (nb == 64 && w == 64 && use_subpanels(pb)) {
-            cudaEvent_t pe;
-            profiler().begin(st, kProfLuPanel, 0.0, pe);
-            const bool keep = profiler().enabled;
-            profiler().enabled = false;  // account the sub-steps as one panel
-            for (int ks = k; ks < k + 64; ks += kSub) {
-                panel_step<kSub>(pb, ws, ks, kSub, st);
-                FDS_LAUNCH(lu_sub_swap_trsm_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
-                           w, ks, pb.ipiv);
-                if (ks + kSub < k + 64) {
-                    dim3 g(ceil_div(pb.n - ks - kSub, 128), pb.batch);
-                    FDS_LAUNCH(lu_sub_gemm_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks);
-                }
-            }
-            profiler().enabled = keep;
-            profiler().end(st, pe, kProfLuPanel, 8.0 * (pb.n - k) * w * w / 2.0 * pb.batch);
+            subpanel_block(pb, ws, k, w, st, true);
             trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
         } else if (nb == 64) {
             panel_step<64>(pb, ws, k, w, st);
