@@ -323,7 +323,7 @@ __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, const double* __restrict__ term_w,
                   const cplx* __restrict__ res /*[m][K]*/, const double* __restrict__ E, double* __restrict__ out) {
     extern __shared__ __align__(16) double rsm[];
@@ -360,7 +360,7 @@ rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, c
         As[(2 * p) * RS + c] = re;
         As[(2 * p + 1) * RS + c] = im;
     }
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps, 32 channels x 16 steps each
     for (int ch = 0; ch < nchunks; ++ch) {
         double* Bs = (ch & 1) ? Bs1 : Bs0;
         if (ch + 1 < nchunks) {
@@ -370,18 +370,18 @@ rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, c
             asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();
-        double acc[4][4][2] = {};
+        double acc[4][2][2] = {};
         for (int q0 = 0; q0 < Q; q0 += 4) {
             const int q = q0 + (lane & 3);
-            double fa[4], fb[4];
+            double fa[4], fb[2];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) fa[mi] = As[q * RS + wm * 32 + mi * 8 + (lane >> 2)];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) fb[ni] = Bs[q * RS + wn * 32 + ni * 8 + (lane >> 2)];
+            for (int ni = 0; ni < 2; ++ni) fb[ni] = Bs[q * RS + wn * 16 + ni * 8 + (lane >> 2)];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma_r(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
+                for (int ni = 0; ni < 2; ++ni) dmma_r(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
         }
         const int t0 = ch * RBN;
 #pragma unroll
@@ -389,8 +389,8 @@ rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, c
             const int k = k0 + wm * 32 + mi * 8 + (lane >> 2);
             if (k >= K) continue;
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int t = t0 + wn * 32 + ni * 8 + 2 * (lane & 3);
+            for (int ni = 0; ni < 2; ++ni) {
+                const int t = t0 + wn * 16 + ni * 8 + 2 * (lane & 3);
                 double* o = out + static_cast<size_t>(k) * T + t;
                 if (vec && t + 1 < T) {
                     __stcs(reinterpret_cast<double2*>(o), make_double2(acc[mi][ni][0], acc[mi][ni][1]));
@@ -474,7 +474,7 @@ void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int
     dim3 g(ceil_div(K, RBM));
     cudaEvent_t pe;
     profiler().begin(st, kProfRatInv, 0.0, pe);
-    FDS_LAUNCH(rat_invert_kernel, g, 128, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev);
+    FDS_LAUNCH(rat_invert_kernel, g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev);
     // algorithmic FP64 work: 2 * Q * T per channel (2*M*T for M/2 pairs)
     profiler().end(st, pe, kProfRatInv, 2.0 * (2.0 * nt) * T * static_cast<double>(K));
 }
