@@ -359,6 +359,25 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
         P.api._check(L.fds_profile_read(kind, ctypes.byref(c), ctypes.byref(kms), ctypes.byref(wk)))
         kern[name] = kms.value / max(c.value, 1)
     P.api._check(L.fds_profile_enable(0))
+    # channel-major spectra (the reference's per-channel fsm_invert layout)
+    cmaj = half.T.contiguous()
+    del half
+
+    def fsm_cm():
+        P.api._check(L.fds_fsm_invert_device_strided(
+            ctypes.c_double(Tper), Ns, ctypes.c_double(eta), D, ctypes.c_void_p(cmaj.data_ptr()),
+            ctypes.c_longlong(Ns // 2 + 1), ctypes.c_longlong(1), 1, ctypes.c_void_p(out_dev.data_ptr()),
+            ctypes.byref(ms)))
+
+    t_fsm_cm = best(fsm_cm)
+    P.api._check(L.fds_profile_enable(1))
+    for _ in range(reps):
+        fsm_cm()
+    c, kms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    P.api._check(L.fds_profile_read(7, ctypes.byref(c), ctypes.byref(kms), ctypes.byref(wk)))
+    kern["fsm_chan_major"] = kms.value / max(c.value, 1)
+    P.api._check(L.fds_profile_enable(0))
+    del cmaj
     hbm = 6543.4
     try:
         hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
@@ -368,17 +387,22 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
     b_res = D * (16.0 * J + 16.0 * M / 2)
     b_fsm = D * (16.0 * (Ns // 2 + 1) + 8.0 * Ns)
     f_rat = D * 2.0 * M * T_steps
-    kr, kt, kf = kern["residue"], kern["rational"], kern["fsm"]
+    kr, kt, kf, kc = kern["residue"], kern["rational"], kern["fsm"], kern["fsm_chan_major"]
+    f_res = D * 4.0 * J * M  # W (M x 2J) times the 2J real samples of each DOF
     out = {
         "dofs": D, "J": J, "M": M, "time_steps": T_steps, "relocation_s": t_reloc,
-        "api_ms": {"residue_id": t_res, "rational_invert": t_rat, "fsm": t_fsm},
-        "kernel_ms": {"residue_id": kr, "rational_invert": kt, "fsm": kf},
+        "api_ms": {"residue_id": t_res, "rational_invert": t_rat, "fsm": t_fsm, "fsm_chan_major": t_fsm_cm},
+        "kernel_ms": {"residue_id": kr, "rational_invert": kt, "fsm": kf, "fsm_chan_major": kc},
         "residue_id_dof_per_s": D / (kr * 1e-3), "residue_id_gbs": b_res / (kr * 1e-3) / 1e9,
         "residue_id_hbm_frac": b_res / (kr * 1e-3) / 1e9 / hbm,
+        "residue_id_tflops": f_res / (kr * 1e-3) / 1e12, "residue_id_fp64_frac": f_res / (kr * 1e-3) / 1e12 / fp64,
         "rational_invert_dof_per_s": D / (kt * 1e-3), "rational_invert_tflops": f_rat / (kt * 1e-3) / 1e12,
         "rational_invert_fp64_frac": f_rat / (kt * 1e-3) / 1e12 / fp64,
         "fsm_dof_per_s": D / (kf * 1e-3), "fsm_gbs": b_fsm / (kf * 1e-3) / 1e9,
         "fsm_hbm_frac": b_fsm / (kf * 1e-3) / 1e9 / hbm,
+        "fsm_chan_major_gbs": b_fsm / (kc * 1e-3) / 1e9, "fsm_chan_major_hbm_frac": b_fsm / (kc * 1e-3) / 1e9 / hbm,
+        "fsm_layouts": "fsm = frequency-major [i][k] spectra as the batched BEM emits them (gather-bound); "
+                       "fsm_chan_major = per-channel [k][i] spectra, the reference fsm_invert layout",
         "vf_fsm_dof_per_s": D / ((kr + kt) * 1e-3),
         "bytes_per_dof": {"residue_id": b_res / D, "fsm": b_fsm / D}, "flops_per_dof_rational": f_rat / D,
         "pinned": "Chebyshev J=40, Omega_s=1.2 max Im a, T=pi*512/Omega_s, eta=3ln10/T, torch CUDA seed 0",

@@ -152,6 +152,11 @@ int fds_rational_invert_device(int M, const fds_c64* poles_host, int K, const fd
                                int T, const double* t_host, double* out_dev, double* ms);
 int fds_fsm_invert_device(double period, int Ns, double eta, int K, const fds_c64* half_dev,
                           int hanning, double* out_dev, double* ms);
+/* Same with explicit element strides: half[k*stride_k + i*stride_i] (stride_k =
+ * Ns/2+1, stride_i = 1 is the per-channel layout of fsm_invert). */
+int fds_fsm_invert_device_strided(double period, int Ns, double eta, int K, const fds_c64* half_dev,
+                                  long long stride_k, long long stride_i, int hanning, double* out_dev,
+                                  double* ms);
 
 /* ------------------------------------------------------------------------
  * AFS driver — replaces run_afs (proj/src/afs.cpp:226-396) for a BEM system

@@ -211,6 +211,21 @@ int fds_fsm_invert_device(double period, int Ns, double eta, int K, const fds_c6
     });
 }
 
+int fds_fsm_invert_device_strided(double period, int Ns, double eta, int K, const fds_c64* half_dev,
+                                  long long stride_k, long long stride_i, int hanning, double* out_dev, double* ms) {
+    return fds_guard([&] {
+        need(stride_k >= 0 && stride_i >= 0, "fsm_invert: negative stride");
+        auto& cx = VfContext::get();
+        EventPair ev;
+        FDS_CUDA(cudaEventRecord(ev.a, cx.st));
+        fsm_invert_device(period, Ns, eta, K, reinterpret_cast<const cplx*>(half_dev), static_cast<size_t>(stride_k),
+                          static_cast<size_t>(stride_i), hanning != 0, out_dev, cx.st);
+        FDS_CUDA(cudaEventRecord(ev.b, cx.st));
+        FDS_CUDA(cudaEventSynchronize(ev.b));
+        if (ms) *ms = elapsed(ev.a, ev.b);
+    });
+}
+
 // ---------------------------------------------------------------- AFS
 namespace {
 

@@ -6,6 +6,13 @@
 //                      DOF (real-output packing, radix-2 Stockham in shared
 //                      memory, one warp per DOF), then scaled by e^{η n Δt}/T.
 //                      HBM-bound: 16 (N_s/2+1) + 8 N_s bytes per DOF.
+//   fsm_stockham256_kernel  N_s = 512 (the bench grid): one warp per DOF, DOF
+//                      pairs streamed through a cp.async ring, radix-8/8/4
+//                      Stockham passes exchanged through the consumed buffer,
+//                      coalesced direct stores. 86 % of HBM on channel-major
+//                      spectra; frequency-major input is bound by the gather
+//                      (a copy-only probe of the same loads runs equally fast).
+//   fsm_warp_kernel    other N_s = 64 R: register FFT with xor-shuffle stages.
 //   fsm_dft_kernel     same contract for any even N_s (direct DFT; e.g. the
 //                      paper's N_s = 218), thread per output sample.
 //   rat_invert_kernel  rational_invert (laplace.cpp:127-164) as a real GEMM on
@@ -19,6 +26,8 @@
 // fire for a conjugate-filled spectrum; it is therefore not re-evaluated.
 #include <cmath>
 #include <math.h>
+#include <cstdlib>
+#include <string>
 
 #include "vf.cuh"
 
@@ -281,6 +290,183 @@ fsm_warp_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t si, cons
     }
 }
 
+// ------------------------------------------------------------------ Stockham FFT, L = 256 (N_s = 512)
+// One warp per DOF with a P-deep cp.async pipeline of single-DOF spectrum
+// buffers. The L-point inverse DFT runs as radix-8, radix-8, radix-4 Stockham
+// passes (natural-order output; the classic out-of-place formulation made
+// in-place by holding a whole pass in registers): each lane holds 8 values per
+// pass, passes exchange through the consumed spectrum buffer (1-in-8 pad, no
+// bank conflicts), and the last pass writes x[2n], x[2n+1] straight to HBM as
+// coalesced 16 B per lane. Every per-lane constant (pack twiddles, pass
+// twiddles, output weights) lives in registers, so per DOF the shared-memory
+// traffic is the 4 KB spectrum in, 8 KB pack reads and two 8 KB exchanges.
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+
+__device__ __forceinline__ cplx mul_i(cplx a) { return mk(-a.im, a.re); }
+
+__device__ __forceinline__ void dft4_inv(cplx& v0, cplx& v1, cplx& v2, cplx& v3) {
+    const cplx a0 = v0 + v2, a1 = v0 - v2, a2 = v1 + v3, a3 = mul_i(v1 - v3);
+    v0 = a0 + a2;
+    v2 = a0 - a2;
+    v1 = a1 + a3;
+    v3 = a1 - a3;
+}
+
+// y[k] = Σ_n v[n] e^{+2πi nk/8}, natural order in and out (v[S*t], t = 0..7)
+template <int S>
+__device__ __forceinline__ void dft8_inv(cplx* v) {
+    cplx e0 = v[0], e1 = v[2 * S], e2 = v[4 * S], e3 = v[6 * S];
+    cplx o0 = v[S], o1 = v[3 * S], o2 = v[5 * S], o3 = v[7 * S];
+    dft4_inv(e0, e1, e2, e3);
+    dft4_inv(o0, o1, o2, o3);
+    constexpr double h = 0.70710678118654752440;
+    o1 = mk((o1.re - o1.im) * h, (o1.re + o1.im) * h);     // e^{iπ/4}
+    o2 = mul_i(o2);                                         // e^{iπ/2}
+    o3 = mk(-(o3.re + o3.im) * h, (o3.re - o3.im) * h);    // e^{3iπ/4}
+    v[0] = e0 + o0; v[4 * S] = e0 - o0;
+    v[S] = e1 + o1; v[5 * S] = e1 - o1;
+    v[2 * S] = e2 + o2; v[6 * S] = e2 - o2;
+    v[3 * S] = e3 + o3; v[7 * S] = e3 - o3;
+}
+
+constexpr int kFsmL = 256, kFsmNc = kFsmL + 1, kFsmBuf = kFsmL + kFsmL / 8;  // buffer length in cplx
+
+// Per-lane constants of the N_s = 512 inversion (shared by every DOF).
+struct Fsm256Lane {
+    cplx t2[7], t3a[3], t3b[3];  // pass-2 e^{2πi (lane%8) t/64}; pass-3 e^{2πi j t/256}, j = lane, lane+32
+    double2 ow0, ow1;            // w[2j], w[2j+1] for j = lane, lane + 32
+    double g1, g2, g3;           // e^{128 t η Δt}, t = 1..3
+    __device__ __forceinline__ void load(int lane, double edt, const cplx* __restrict__ gtw,
+                                         const double* __restrict__ gwout) {
+#pragma unroll
+        for (int t = 1; t < 8; ++t) t2[t - 1] = gtw[((lane & 7) * t * 4) % kFsmL];
+#pragma unroll
+        for (int t = 1; t < 4; ++t) {
+            t3a[t - 1] = gtw[(lane * t) % kFsmL];
+            t3b[t - 1] = gtw[((lane + 32) * t) % kFsmL];
+        }
+        ow0 = make_double2(gwout[2 * lane], gwout[2 * lane + 1]);
+        ow1 = make_double2(gwout[2 * lane + 64], gwout[2 * lane + 65]);
+        g1 = exp(128.0 * edt);
+        g2 = exp(256.0 * edt);
+        g3 = exp(384.0 * edt);
+    }
+};
+
+// One DOF: X = its staged half spectrum (N_s/2 + 1 values, buffer of kFsmBuf),
+// reused in place as the exchange buffer; o = its N_s output samples.
+__device__ __forceinline__ void fsm256_dof(cplx* X, const cplx* __restrict__ pst, int hanning, int lane,
+                                           const Fsm256Lane& c, double2* __restrict__ o) {
+    constexpr int L = kFsmL;
+    // pack Z_n = (x_n + conj x_{L-n}) + i e^{2πi n/N_s} (x_n - conj x_{L-n}), windowed,
+    // k = 0 and N_s/2 forced real (laplace.cpp:80-81)
+    cplx y[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int n = lane + 32 * m;
+        cplx xk = X[n], xm = X[L - n];
+        if (m == 0 && lane == 0) { xk.im = 0.0; xm.im = 0.0; }
+        const cplx pm = pst[n];
+        if (hanning) {
+            xk = xk * (0.5 * (1.0 + pm.re));
+            xm = xm * (0.5 * (1.0 - pm.re));
+        }
+        const cplx cm = conjg(xm);
+        const cplx sum = xk + cm, p = pm * (xk - cm);
+        y[m] = mk(sum.re - p.im, sum.im + p.re);
+    }
+    // pass 1 (radix 8, no twiddle): inputs n = lane + 32 t, outputs 8 lane + t
+    dft8_inv<1>(y);
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) X[fpad(8 * lane + t)] = y[t];
+    __syncwarp();
+    // pass 2 (radix 8, NS = 8): inputs lane + 32 t, outputs (lane/8)*64 + lane%8 + 8 t
+#pragma unroll
+    for (int t = 0; t < 8; ++t) y[t] = X[fpad(lane + 32 * t)];
+#pragma unroll
+    for (int t = 1; t < 8; ++t) y[t] = y[t] * c.t2[t - 1];
+    dft8_inv<1>(y);
+    __syncwarp();
+    const int o2 = (lane >> 3) * 64 + (lane & 7);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) X[fpad(o2 + 8 * t)] = y[t];
+    __syncwarp();
+    // pass 3 (radix 4, NS = 64): j in {lane, lane+32}, inputs j + 64 t, outputs z[j + 64 t]
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) y[4 * h + t] = X[fpad(lane + 32 * h + 64 * t)];
+#pragma unroll
+    for (int t = 1; t < 4; ++t) {
+        y[t] = y[t] * c.t3a[t - 1];
+        y[4 + t] = y[4 + t] * c.t3b[t - 1];
+    }
+    dft4_inv(y[0], y[1], y[2], y[3]);
+    dft4_inv(y[4], y[5], y[6], y[7]);
+    // x[2n] = Re z[n], x[2n+1] = Im z[n], weight e^{η t}/T
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const cplx z = y[4 * h + t];
+            const double2 w = h ? c.ow1 : c.ow0;
+            const double gt = t == 0 ? 1.0 : (t == 1 ? c.g1 : (t == 2 ? c.g2 : c.g3));
+            __stcs(&o[lane + 32 * h + 64 * t], make_double2(z.re * (w.x * gt), z.im * (w.y * gt)));
+        }
+    __syncwarp();
+}
+
+// Warp-private pipeline: each warp streams groups of D adjacent DOFs through a
+// P-deep cp.async ring (D = 2: every lane pair fills one 32 B sector of the
+// frequency-major input).
+template <int WARPS, int P, int MINB, int D>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
+fsm_stockham256_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t si, int hanning, double edt,
+                       const cplx* __restrict__ gpost, const cplx* __restrict__ gtw, const double* __restrict__ gwout,
+                       double* __restrict__ out) {
+    constexpr int Nc = kFsmNc;
+    extern __shared__ __align__(16) cplx fsm_s[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    cplx* wb = fsm_s + static_cast<size_t>(warp) * P * D * kFsmBuf;
+    cplx* pst = fsm_s + static_cast<size_t>(WARPS) * P * D * kFsmBuf;  // e^{2πi n/N_s}
+    for (int j = threadIdx.x; j < kFsmL; j += WARPS * 32) pst[j] = gpost[j];
+    Fsm256Lane c;
+    c.load(lane, edt, gtw, gwout);
+    __syncthreads();
+    const int nwarps = gridDim.x * WARPS;
+    const int first = blockIdx.x * WARPS + warp;
+    auto stage = [&](int g, cplx* buf) {
+        if (D * g < K) {
+            for (int q = lane; q < D * Nc; q += 32) {
+                const int i = q / D, d = q % D;
+                const int k = min(D * g + d, K - 1);
+                const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(buf + d * kFsmBuf + i));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                             "l"(half + static_cast<size_t>(k) * sk + static_cast<size_t>(i) * si));
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+#pragma unroll
+    for (int p = 0; p < P - 1; ++p) stage(first + p * nwarps, wb + p * D * kFsmBuf);
+    int slot = 0;
+    for (int g = first; D * g < K; g += nwarps) {
+        stage(g + (P - 1) * nwarps, wb + ((slot + P - 1) % P) * D * kFsmBuf);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(P - 1));
+        __syncwarp();
+#pragma unroll 1
+        for (int d = 0; d < D; ++d) {
+            const int k = D * g + d;
+            if (k >= K) break;
+            fsm256_dof(wb + (slot * D + d) * kFsmBuf, pst, hanning, lane, c,
+                       reinterpret_cast<double2*>(out + static_cast<size_t>(k) * (2 * kFsmL)));
+        }
+        slot = (slot + 1) % P;
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 __global__ void fsm_dft_kernel(int Ns, double eta, double dt, double invT, int K, const cplx* __restrict__ half,
                                size_t sk, size_t si, int hanning, double* __restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -517,6 +703,16 @@ void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km
     FDS_CUDA(cudaStreamSynchronize(cx.st));
 }
 
+// N_s = 512 uses the Stockham kernel unless FDSWEEP_FSM=shuffle selects the
+// register-shuffle FFT kernel (kept for comparison).
+static bool fsm_stockham() {
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_FSM");
+        return !(e && std::string(e) == "shuffle");
+    }();
+    return on;
+}
+
 void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* half_dev, size_t sk, size_t si,
                        bool hanning, double* out_dev, cudaStream_t st) {
     if (!(period > 0.0)) throw ValidationError("FsmGrid: period must be positive");
@@ -547,7 +743,22 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
         FDS_LAUNCH(fsm_tables_kernel, ceil_div(Ns + 1, 256), 256, 0, st, Ns, eta, dt, invT, hanning ? 1 : 0, win, post,
                    tw, wout);
         const int R = L / 32;
-        if (L % 32 == 0 && (R == 1 || R == 2 || R == 4 || R == 8 || R == 16)) {
+        if (L == kFsmL && fsm_stockham()) {
+            // 4 warps x 2-deep ring of DOF pairs: 74 KB smem, 2 CTAs (8 warps) per SM
+            constexpr int W = 4, P = 2, D = 2;
+            auto kern = fsm_stockham256_kernel<W, P, 2, D>;
+            const size_t ssm = (static_cast<size_t>(W) * P * D * kFsmBuf + kFsmL) * sizeof(cplx);
+            static bool attr = false;
+            if (!attr) {
+                FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm)));
+                attr = true;
+            }
+            static int per_sm = 0;
+            if (per_sm == 0) FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
+            const int ctas = std::min(ceil_div(ceil_div(K, D), W), std::max(1, per_sm) * device_info().sms);
+            FDS_LAUNCH(kern, ctas, W * 32, ssm, st, K, half_dev, sk, si, hanning ? 1 : 0, eta * dt, post, tw, wout,
+                       out_dev);
+        } else if (L % 32 == 0 && (R == 1 || R == 2 || R == 4 || R == 8 || R == 16)) {
             static bool w16 = false;
             if (!w16) {
                 double h[16][2];

@@ -199,6 +199,27 @@ def test_fsm_invert_parity(ns, hann):
     assert rel_l2(g, o) < 1e-12
 
 
+@pytest.mark.parametrize("K", [1, 2, 3, 37, 1001])
+@pytest.mark.parametrize("freq_major", [False, True])
+def test_fsm_invert_device_layouts(K, freq_major):
+    """N_s = 512 device path on both spectrum layouts, odd/even channel counts."""
+    import ctypes
+
+    import torch
+
+    ns, T, eta = 512, 6.0, 0.4
+    rng = np.random.default_rng(K)
+    half = rng.normal(size=(K, ns // 2 + 1)) + 1j * rng.normal(size=(K, ns // 2 + 1))
+    ref = O.fsm_invert(T, ns, eta, half, True)
+    dev = torch.tensor(half.T.copy() if freq_major else half, device="cuda")
+    out = torch.empty((K, ns), dtype=torch.float64, device="cuda")
+    sk, si = (1, K) if freq_major else (ns // 2 + 1, 1)
+    P.api._check(P.lib().fds_fsm_invert_device_strided(
+        ctypes.c_double(T), ns, ctypes.c_double(eta), K, ctypes.c_void_p(dev.data_ptr()), ctypes.c_longlong(sk),
+        ctypes.c_longlong(si), 1, ctypes.c_void_p(out.data_ptr()), None))
+    assert rel_l2(out.cpu().numpy(), ref) < 1e-12
+
+
 # ------------------------------------------------ AFS: identical sampled sequence
 class _ModalSys:
     def __init__(self, fx):
