@@ -308,71 +308,85 @@ __device__ __forceinline__ void dmma_v(double& c0, double& c1, double a, double 
 }
 
 constexpr int kResNI = 2;  // 8-channel sub-tiles per warp (16 channels): low registers, many warps
-constexpr int kResPF = 8;  // q-steps of B fragments prefetched per warp
 
-template <int MT>
-__global__ void __launch_bounds__(128)
+// Steps (4 q values each) per channel tile, padded to a multiple of the prefetch depth.
+__host__ __device__ inline int res_steps(int J, int PF) { return ((J + 1) / 2 + PF - 1) / PF * PF; }
+
+template <int MT, int PF>
+__global__ void __launch_bounds__(128, 4)
 vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
                       cplx* __restrict__ res) {
     // Persistent CTAs; W (the shared solve operator, M x 2J) staged once in smem
-    // as the A operand. Each warp owns 32 channels x up to 64 poles; its B
-    // fragments (Re/Im of values[j][k]) are read straight from HBM with a
-    // 4-step register prefetch (each 128 B line fully used), so the kernel
-    // streams values -> residues at HBM rate.
+    // as the A operand, zero past row M and past column 2J (the padded steps).
+    // Each warp owns 16 channels x 8 MT poles per tile; its B fragments (Re/Im
+    // of values[j][k]) come straight from HBM through a register ring of PF
+    // steps that runs ACROSS tiles: the last chunk of a tile prefetches the
+    // first chunk of the warp's next tile, so HBM latency is never exposed at
+    // tile boundaries. Each load instruction covers whole 128 B lines.
     extern __shared__ double rsm2[];
-    const int Q = 2 * J, Qp = (Q + 3) & ~3;
-    double* As = rsm2;  // [Qp][kRmS], As[q][m] = W[m][q]  (M <= 64 per launch slice)
+    const int Q = 2 * J, Sp = res_steps(J, PF), Qs = 4 * Sp, chunks = Sp / PF;
+    double* As = rsm2;  // [Qs][kRmS], As[q][m] = W[m][q]  (M <= 64 per launch slice)
     const int m0 = blockIdx.y * 64;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int idx = tid; idx < Qp * 64; idx += blockDim.x) {
-        const int m = idx / Qp, q = idx % Qp;
+    for (int idx = tid; idx < Qs * 64; idx += blockDim.x) {
+        const int m = idx / Qs, q = idx % Qs;
         As[q * kRmS + m] = (m0 + m < M && q < Q) ? W[static_cast<size_t>(m0 + m) * Q + q] : 0.0;
     }
     __syncthreads();
-    const int mtiles = min(MT, (M - m0 + 7) / 8);
     const double* vd = reinterpret_cast<const double*>(vals);
     const int q_l = lane & 3, n_l = lane >> 2;
+    const int j0 = q_l >> 1, part = q_l & 1;
+    const double* Al = As + q_l * kRmS + n_l;
     const int warps_total = gridDim.x * (blockDim.x >> 5);
-    for (int tile = blockIdx.x * (blockDim.x >> 5) + warp; tile * (8 * kResNI) < K; tile += warps_total) {
+    const size_t row2 = 2 * static_cast<size_t>(K);  // doubles per value row j
+    // lane's channel columns of a tile (clamped: ragged columns are computed, not stored)
+    auto cols = [&](int tile, const double* (&bc)[kResNI]) {
+#pragma unroll
+        for (int ni = 0; ni < kResNI; ++ni)
+            bc[ni] = vd + static_cast<size_t>(min(tile * (8 * kResNI) + ni * 8 + n_l, K - 1)) * 2 + part;
+    };
+    // step st reads value row j = 2 st + j0 (clamped: rows past J meet zero columns of W)
+    auto bload = [&](const double* (&bc)[kResNI], int st, double (&fb)[kResNI]) {
+        const size_t off = static_cast<size_t>(min(2 * st + j0, J - 1)) * row2;
+#pragma unroll
+        for (int ni = 0; ni < kResNI; ++ni) fb[ni] = __ldcs(bc[ni] + off);
+    };
+    int tile = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (tile * (8 * kResNI) >= K) return;
+    const double* bc[kResNI];
+    cols(tile, bc);
+    double ring[PF][kResNI];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) bload(bc, p, ring[p]);
+    for (; tile * (8 * kResNI) < K; tile += warps_total) {
         const int kb = tile * (8 * kResNI);
         double acc[MT][kResNI][2];
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
             for (int ni = 0; ni < kResNI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-        // B fragment element for step q0: q = q0 + q_l -> j = q/2, part = q&1
-        auto bload = [&](int q0, double* fb) {
-            const int q = q0 + q_l;
-            const int j = q >> 1, part = q & 1;
+        for (int c = 0; c < chunks; ++c) {
+            // prefetch target: the next chunk of this tile, or chunk 0 of the next tile
+            const bool last = c + 1 == chunks;
+            const int nc = last ? 0 : c + 1;
+            const bool more = !last || (tile + warps_total) * (8 * kResNI) < K;
+            if (last) cols(tile + warps_total, bc);
 #pragma unroll
-            for (int ni = 0; ni < kResNI; ++ni) {
-                const int k = kb + ni * 8 + n_l;
-                fb[ni] = (q < Q && k < K) ? __ldcs(vd + (static_cast<size_t>(j) * K + k) * 2 + part) : 0.0;
-            }
-        };
-        // register ring of kResPF B-fragment steps in flight
-        double ring[kResPF][kResNI];
+            for (int p = 0; p < PF; ++p) {
+                double fb[kResNI];
 #pragma unroll
-        for (int p = 0; p < kResPF; ++p) bload(4 * p, ring[p]);
-        for (int q0 = 0; q0 < Qp; q0 += 4) {
-            double fb[kResNI];
+                for (int ni = 0; ni < kResNI; ++ni) fb[ni] = ring[p][ni];
+                if (more) bload(bc, nc * PF + p, ring[p]);
+                const double* a = Al + 4 * (c * PF + p) * kRmS;
 #pragma unroll
-            for (int ni = 0; ni < kResNI; ++ni) {
-                fb[ni] = ring[0][ni];
-#pragma unroll
-                for (int p = 0; p + 1 < kResPF; ++p) ring[p][ni] = ring[p + 1][ni];
-            }
-            bload(q0 + 4 * kResPF, ring[kResPF - 1]);
-            const int q = q0 + q_l;
-#pragma unroll
-            for (int mi = 0; mi < MT; ++mi) {
-                if (mi < mtiles) {
-                    const double fa = As[q * kRmS + mi * 8 + n_l];
+                for (int mi = 0; mi < MT; ++mi) {
+                    const double fa = a[mi * 8];
 #pragma unroll
                     for (int ni = 0; ni < kResNI; ++ni) dmma_v(acc[mi][ni][0], acc[mi][ni][1], fa, fb[ni]);
                 }
             }
         }
+        const int mtiles = min(MT, (M - m0 + 7) / 8);
         // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
         // the partner row sits 4 lanes away in the accumulator fragment.
 #pragma unroll
@@ -666,8 +680,8 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
                                       static_cast<int>(smem)));
         attr = smem;
     }
-    const int Qp = (2 * J + 3) & ~3;
-    const size_t msmem = static_cast<size_t>(Qp) * kRmS * sizeof(double);
+    const int PF = (((J + 1) / 2) % 5 == 0) ? 5 : 4;  // prefetch depth dividing the step count when possible
+    const size_t msmem = static_cast<size_t>(4 * res_steps(J, PF)) * kRmS * sizeof(double);
     cudaEvent_t pe;
     profiler().begin(st, kProfVfResidue, 0.0, pe);
     if (msmem <= device_info().smem_optin - 1024) {
@@ -681,10 +695,17 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
             }
             FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 128, msmem, st, J, K, M, P, values_dev, dW, res_dev);
         };
-        if (mt <= 2) go(vf_residue_mma_kernel<2>);
-        else if (mt <= 4) go(vf_residue_mma_kernel<4>);
-        else if (mt <= 6) go(vf_residue_mma_kernel<6>);
-        else go(vf_residue_mma_kernel<8>);
+        if (PF == 5) {
+            if (mt <= 2) go(vf_residue_mma_kernel<2, 5>);
+            else if (mt <= 4) go(vf_residue_mma_kernel<4, 5>);
+            else if (mt <= 6) go(vf_residue_mma_kernel<6, 5>);
+            else go(vf_residue_mma_kernel<8, 5>);
+        } else {
+            if (mt <= 2) go(vf_residue_mma_kernel<2, 4>);
+            else if (mt <= 4) go(vf_residue_mma_kernel<4, 4>);
+            else if (mt <= 6) go(vf_residue_mma_kernel<6, 4>);
+            else go(vf_residue_mma_kernel<8, 4>);
+        }
     } else {
         dim3 g(ceil_div(K, kResThreads), ceil_div(M, kResChunk));
         FDS_LAUNCH(vf_residue_kernel, g, kResThreads, smem, st, J, K, M, P, values_dev, dW, res_dev);
