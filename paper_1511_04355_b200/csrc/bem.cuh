@@ -15,7 +15,7 @@ struct BemParams {
     static constexpr int kTerms = 16;
     static constexpr double kSeriesR2 = 0.09;  // |z| < 0.3 -> Taylor branch
     static constexpr int kSelfGauss = 10;
-    double mu, lambda, lam_over_mu, cs, inv_cs, k, inv_4pi_mu;
+    double mu, lambda, lam_over_mu, cs, inv_cs, k, inv_k, inv_4pi_mu;
     double E10, E20;  // static (z=0) values of C-B and (λ/μ)(C-D-2B)-2B
     double ta[kTerms], tb[kTerms], tc[kTerms], td[kTerms];
     double r7l[7][3], r7w[7];

@@ -28,9 +28,23 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 
-__device__ __forceinline__ void abcd(const BemParams& P, cplx z, cplx& A, cplx& B, cplx& C, cplx& D) {
+// Frequency-dependent scalars of one kernel evaluation: A, B and the three
+// combinations the traction kernel needs, CB = C−B, G = C−D−2B, B4 = 4B−2D.
+// Far branch in closed form with E2 = e^{−z}, E1 = k² e^{−kz}, P2 = 1/z + 1/z²,
+// P1 = 1/x + 1/x² (x = kz):
+//   A  = (1+P2)E2 − P1 E1            B  = (1+3P2)E2 − (1+3P1)E1
+//   CB = 2(1+3P1)E1 − (z+3+6P2)E2     G  = −(1+x)E1   (the E2 terms cancel exactly)
+//   B4 = (2z+12+30P2)E2 − (2x+12+30P1)E1
+// which is the oracle's A..D algebra regrouped (one complex reciprocal instead
+// of two, and the G cancellation done symbolically).
+struct KTerms {
+    cplx A, B, CB, G, B4;
+};
+
+__device__ __forceinline__ KTerms kterms(const BemParams& P, cplx z) {
+    KTerms o;
     if (abs2(z) < BemParams::kSeriesR2) {
-        A = B = C = D = mk(0.0, 0.0);
+        cplx A = mk(0.0, 0.0), B = A, C = A, D = A;
 #pragma unroll
         for (int m = BemParams::kTerms - 1; m >= 0; --m) {
             A = A * z + P.ta[m];
@@ -38,49 +52,132 @@ __device__ __forceinline__ void abcd(const BemParams& P, cplx z, cplx& A, cplx& 
             C = C * z + P.tc[m];
             D = D * z + P.td[m];
         }
-        return;
+        o.A = A;
+        o.B = B;
+        o.CB = C - B;
+        o.G = C - D - 2.0 * B;
+        o.B4 = 4.0 * B - 2.0 * D;
+        return o;
     }
-    const cplx x1 = z * P.k;
-    const cplx e2 = cexpd(-z), e1 = cexpd(-x1);
-    const cplx iz = crecip(z), iz2 = iz * iz;
-    const cplx ix = crecip(x1), ix2 = ix * ix;
-    const double k2 = P.k * P.k;
-    A = (mk(1.0, 0.0) + iz + iz2) * e2 - k2 * ((ix + ix2) * e1);
-    const cplx q2 = mk(1.0, 0.0) + 3.0 * iz + 3.0 * iz2;
-    const cplx q1 = mk(1.0, 0.0) + 3.0 * ix + 3.0 * ix2;
-    B = q2 * e2 - k2 * (q1 * e1);
-    C = -((z + 2.0 + 3.0 * iz + 3.0 * iz2) * e2) + k2 * (q1 * e1);
-    D = -((z + 4.0 + 9.0 * iz + 9.0 * iz2) * e2) + k2 * ((x1 + 4.0 + 9.0 * ix + 9.0 * ix2) * e1);
+    const double k = P.k, ik = P.inv_k;
+    const cplx x1 = z * k;
+    const double d = 1.0 / abs2(z);
+    const cplx iz = mk(z.re * d, -z.im * d);
+    const cplx iz2 = iz * iz;
+    const cplx P2 = iz + iz2;
+    const cplx P1 = iz * ik + iz2 * (ik * ik);
+    const cplx E2 = cexpd(-z);
+    const cplx E1 = cexpd(-x1) * (k * k);
+    const cplx q1E1 = (3.0 * P1 + 1.0) * E1;
+    o.A = (P2 + 1.0) * E2 - P1 * E1;
+    o.B = (3.0 * P2 + 1.0) * E2 - q1E1;
+    o.CB = 2.0 * q1E1 - (z + 6.0 * P2 + 3.0) * E2;
+    o.G = -((x1 + 1.0) * E1);
+    o.B4 = (2.0 * z + 30.0 * P2 + 12.0) * E2 - (2.0 * x1 + 30.0 * P1 + 12.0) * E1;
+    return o;
 }
 
-// Accumulates w*T (9 complex, row-major i*3+j) and w*(U·t) (3 complex).
-__device__ __forceinline__ void accumulate_ut(const BemParams& P, double rx, double ry, double rz,
-                                              const double n[3], const double t[3], cplx s,
-                                              double w, cplx T[9], cplx Ut[3]) {
+// Quadrature-point sums over one flat source element (n constant):
+//   T_ij = δij S0 + n_i Sj + Ei n_j + Bij,   (U·t)_i = SA t_i − SB_i
+// with S0 = Σ cb r,n, Sj = Σ cb e_j, Ei = Σ e4 e_i, Bij = Σ b4 r,n e_i e_j,
+// SA = Σ A fu, SB_i = Σ B fu (e·t) e_i — 17 complex sums per point instead of
+// the 12 complex 3-term updates of the assembled blocks.
+struct KAcc {
+    cplx s0, sj[3], ei[3], bij[6], sa, sb[3];
+    __device__ __forceinline__ void zero() {
+        s0 = sa = mk(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) sj[i] = ei[i] = sb[i] = mk(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) bij[i] = mk(0.0, 0.0);
+    }
+    // displacement part: A, B with weight fu, unit vector e, e·t
+    __device__ __forceinline__ void add_u(const KTerms& k, const double e[3], double fu, double et) {
+        sa = sa + k.A * fu;
+        const cplx bf = k.B * (fu * et);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) sb[i] = sb[i] + bf * e[i];
+    }
+    __device__ __forceinline__ void add(const BemParams& P, const KTerms& k, const double e[3], double rn,
+                                        double fu, double ft, double et) {
+        const cplx cb = k.CB * ft;
+        const cplx e4 = (P.lam_over_mu * k.G - 2.0 * k.B) * ft;
+        const cplx b4 = k.B4 * (ft * rn);
+        s0 = s0 + cb * rn;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            sj[i] = sj[i] + cb * e[i];
+            ei[i] = ei[i] + e4 * e[i];
+        }
+        bij[0] = bij[0] + b4 * (e[0] * e[0]);
+        bij[1] = bij[1] + b4 * (e[0] * e[1]);
+        bij[2] = bij[2] + b4 * (e[0] * e[2]);
+        bij[3] = bij[3] + b4 * (e[1] * e[1]);
+        bij[4] = bij[4] + b4 * (e[1] * e[2]);
+        bij[5] = bij[5] + b4 * (e[2] * e[2]);
+        add_u(k, e, fu, et);
+    }
+    // T (row-major i*3+j) and U·t of the element
+    __device__ __forceinline__ void finish(const double n[3], const double t[3], cplx T[9], cplx Ut[3]) const {
+        constexpr int bidx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                cplx v = sj[j] * n[i] + ei[i] * n[j] + bij[bidx[i][j]];
+                if (i == j) v = v + s0;
+                T[3 * i + j] = v;
+            }
+            Ut[i] = sa * t[i] - sb[i];
+        }
+    }
+};
+
+// One regular quadrature point y (relative position r = y − x) of weight w.
+__device__ __forceinline__ void kpoint(const BemParams& P, KAcc& acc, double rx, double ry, double rz,
+                                       const double n[3], const double t[3], cplx s, double w) {
     const double r2 = rx * rx + ry * ry + rz * rz;
     const double r = sqrt(r2);
     const double ir = 1.0 / r;
     const double e[3] = {rx * ir, ry * ir, rz * ir};
     const double rn = e[0] * n[0] + e[1] * n[1] + e[2] * n[2];
-    cplx A, B, C, D;
-    abcd(P, s * (r * P.inv_cs), A, B, C, D);
+    const KTerms k = kterms(P, s * (r * P.inv_cs));
     const double fu = w * ir * P.inv_4pi_mu;
     const double ft = w * ir * ir * (1.0 / (4.0 * kPi));
-    const cplx cb = (C - B) * ft;
-    const cplx e4 = (P.lam_over_mu * (C - D - 2.0 * B) - 2.0 * B) * ft;  // coefficient of e_i n_j
-    const cplx b4 = (4.0 * B - 2.0 * D) * ft;                              // of e_i e_j r,n
-    // U·t = (A t − B e (e·t)) fu
     const double et = e[0] * t[0] + e[1] * t[1] + e[2] * t[2];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] + (A * t[i] - B * (e[i] * et)) * fu;
+    acc.add(P, k, e, rn, fu, ft, et);
+}
+
+// Displacement-only point (the far 7-point U·t a near pair must cancel).
+__device__ __forceinline__ void kpoint_u(const BemParams& P, KAcc& acc, double rx, double ry, double rz,
+                                         const double t[3], cplx s, double w) {
+    const double r = sqrt(rx * rx + ry * ry + rz * rz);
+    const double ir = 1.0 / r;
+    const double e[3] = {rx * ir, ry * ir, rz * ir};
+    const KTerms k = kterms(P, s * (r * P.inv_cs));
+    acc.add_u(k, e, w * ir * P.inv_4pi_mu, e[0] * t[0] + e[1] * t[1] + e[2] * t[2]);
+}
+
+// Self-element polar point: the static CPV part E10/E20 is integrated exactly
+// elsewhere, so only the dynamic remainder (CB − E10, λ/μ G − 2B − E20) is summed.
+__device__ __forceinline__ void kpoint_self(const BemParams& P, KAcc& acc, const KTerms& k, const double ev[3],
+                                            double fu, double ft, double et) {
+    const cplx dE1 = (k.CB - mk(P.E10, 0.0)) * ft;
+    const cplx dE2 = (P.lam_over_mu * k.G - 2.0 * k.B - mk(P.E20, 0.0)) * ft;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
+        acc.sj[i] = acc.sj[i] + dE1 * ev[i];
+        acc.ei[i] = acc.ei[i] + dE2 * ev[i];
+    }
+    acc.add_u(k, ev, fu, et);
+}
+
+// Exact ln-CPV static part along one polar ray: T += (E10 e_j n_i + E20 e_i n_j) lnR.
+__device__ __forceinline__ void kpoint_cpv(const BemParams& P, KAcc& acc, const double ev[3], double lnR) {
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const double dij = (i == j) ? rn : 0.0;
-            T[3 * i + j] = T[3 * i + j] + cb * (dij + e[j] * n[i]) + e4 * (e[i] * n[j]) +
-                           b4 * (e[i] * e[j] * rn);
-        }
+    for (int i = 0; i < 3; ++i) {
+        acc.sj[i].re += P.E10 * lnR * ev[i];
+        acc.ei[i].re += P.E20 * lnR * ev[i];
     }
 }
 
@@ -113,17 +210,20 @@ bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __rest
         const double* g = sg[el];
         const double n[3] = {g[12], g[13], g[14]};
         const double t[3] = {st[el][0], st[el][1], st[el][2]};
-        cplx T[9];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) T[i] = mk(0.0, 0.0);
+        KAcc acc;
+        acc.zero();
 #pragma unroll
         for (int q = 0; q < 7; ++q) {
             const double l0 = P.r7l[q][0], l1 = P.r7l[q][1], l2 = P.r7l[q][2];
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
             const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
             const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
-            accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[q] * g[15], T, Ut);
+            kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[q] * g[15]);
         }
+        cplx T[9], Ue[3];
+        acc.finish(n, t, T, Ue);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] + Ue[i];
         // A[(3e+j)*ld + 3c+i]
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
@@ -162,15 +262,13 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
     const double n[3] = {g[12], g[13], g[14]};
     const double t[3] = {trac[3 * e], trac[3 * e + 1], trac[3 * e + 2]};
     cplx T[9], Ut[3];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) T[i] = mk(0.0, 0.0);
-    Ut[0] = Ut[1] = Ut[2] = mk(0.0, 0.0);
+    KAcc acc;
+    acc.zero();
 
     if (level < 0) {
         // Self element: polar quadrature about the centroid over the 3 edge
         // sub-triangles; static antisymmetric T part as the exact CPV.
         const int NG = BemParams::kSelfGauss;
-        const cplx E10 = mk(P.E10, 0.0), E20 = mk(P.E20, 0.0);
         for (int edge = 0; edge < 3; ++edge) {
             const int ia = edge, ib = (edge + 1) % 3;
             const double Px = g[3 * ia], Py = g[3 * ia + 1], Pz = g[3 * ia + 2];
@@ -187,32 +285,19 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
                 const double ev[3] = {dx / R, dy / R, dz / R};
                 const double jt = hperp * L * P.glw[a];
                 const double lnR = log(R) / (R * R) * jt * (1.0 / (4.0 * kPi));
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-#pragma unroll
-                    for (int j = 0; j < 3; ++j)
-                        T[3 * i + j] = T[3 * i + j] + (E10 * (ev[j] * n[i]) + E20 * (ev[i] * n[j])) * lnR;
+                kpoint_cpv(P, acc, ev, lnR);
                 const double et = ev[0] * t[0] + ev[1] * t[1] + ev[2] * t[2];
                 for (int bq = 0; bq < NG; ++bq) {
                     const double u = P.glx[bq];
                     const double rho = R * u;
-                    cplx Aa, Bb, Cc, Dd;
-                    abcd(P, s * (rho * P.inv_cs), Aa, Bb, Cc, Dd);
+                    const KTerms k = kterms(P, s * (rho * P.inv_cs));
                     const double w = jt * P.glw[bq];
-                    const double fu = w * u / rho * P.inv_4pi_mu;
-                    const double ft = w * u / (rho * rho) * (1.0 / (4.0 * kPi));
-                    const cplx dE1 = (Cc - Bb) - E10;
-                    const cplx dE2 = P.lam_over_mu * (Cc - Dd - 2.0 * Bb) - 2.0 * Bb - E20;
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] + (Aa * t[i] - Bb * (ev[i] * et)) * fu;
-#pragma unroll
-                    for (int i = 0; i < 3; ++i)
-#pragma unroll
-                        for (int j = 0; j < 3; ++j)
-                            T[3 * i + j] = T[3 * i + j] + (dE1 * (ev[j] * n[i]) + dE2 * (ev[i] * n[j])) * ft;
+                    kpoint_self(P, acc, k, ev, w * u / rho * P.inv_4pi_mu, w * u / (rho * rho) * (1.0 / (4.0 * kPi)),
+                                et);
                 }
             }
         }
+        acc.finish(n, t, T, Ut);
     } else {
         // Near element: 4^level sub-triangles (recursive midpoint split, children
         // (p0,m01,m20), (m01,p1,m12), (m20,m12,p2), (m01,m12,m20)), 7 points each.
@@ -249,24 +334,22 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
                 const double yx = l0 * p[0][0] + l1 * p[1][0] + l2 * p[2][0];
                 const double yy = l0 * p[0][1] + l1 * p[1][1] + l2 * p[2][1];
                 const double yz = l0 * p[0][2] + l1 * p[1][2] + l2 * p[2][2];
-                accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area, T, Ut);
+                kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area);
             }
         }
         // subtract the far kernel's 7-point U·t for this pair (it is in the partials)
-        cplx Tdummy[9];
-        cplx Uf[3] = {mk(0, 0), mk(0, 0), mk(0, 0)};
-#pragma unroll
-        for (int i = 0; i < 9; ++i) Tdummy[i] = mk(0.0, 0.0);
+        KAcc accf;
+        accf.zero();
         for (int gq = 0; gq < 7; ++gq) {
             const double l0 = P.r7l[gq][0], l1 = P.r7l[gq][1], l2 = P.r7l[gq][2];
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
             const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
             const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
-            accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * g[15], Tdummy, Uf);
+            kpoint_u(P, accf, yx - x0, yy - x1, yz - x2, t, s, P.r7w[gq] * g[15]);
         }
-        Ut[0] = Ut[0] - Uf[0];
-        Ut[1] = Ut[1] - Uf[1];
-        Ut[2] = Ut[2] - Uf[2];
+        acc.finish(n, t, T, Ut);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] - (accf.sa * t[i] - accf.sb[i]);
     }
     if (!active) return;
     double* Are = A + (size_t)b * mstride;
@@ -320,16 +403,14 @@ bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* _
     const double n[3] = {g[12], g[13], g[14]};
     const double t[3] = {trac[3 * e], trac[3 * e + 1], trac[3 * e + 2]};
     cplx T[9], Ut[3];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) T[i] = mk(0.0, 0.0);
-    Ut[0] = Ut[1] = Ut[2] = mk(0.0, 0.0);
+    KAcc acc;
+    acc.zero();
 
     if (level < 0) {
         // Self element: polar quadrature about the centroid over the 3 edge
         // sub-triangles; static antisymmetric T part as the exact CPV.
         const int NG = BemParams::kSelfGauss;
         const int npts = 3 * NG * NG;
-        const cplx E10 = mk(P.E10, 0.0), E20 = mk(P.E20, 0.0);
         for (int q = lane; q < npts; q += 32) {
             const int edge = q / (NG * NG), a = (q / NG) % NG, bq = q % NG;
             const int ia = edge, ib = (edge + 1) % 3;
@@ -345,32 +426,15 @@ bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* _
             const double R = sqrt(dx * dx + dy * dy + dz * dz);
             const double ev[3] = {dx / R, dy / R, dz / R};
             const double jt = hperp * L * P.glw[a];
-            if (bq == 0) {
-                const double lnR = log(R) / (R * R) * jt * (1.0 / (4.0 * kPi));
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-#pragma unroll
-                    for (int j = 0; j < 3; ++j)
-                        T[3 * i + j] = T[3 * i + j] + (E10 * (ev[j] * n[i]) + E20 * (ev[i] * n[j])) * lnR;
-            }
+            if (bq == 0) kpoint_cpv(P, acc, ev, log(R) / (R * R) * jt * (1.0 / (4.0 * kPi)));
             const double u = P.glx[bq];
             const double rho = R * u;
-            cplx Aa, Bb, Cc, Dd;
-            abcd(P, s * (rho * P.inv_cs), Aa, Bb, Cc, Dd);
+            const KTerms k = kterms(P, s * (rho * P.inv_cs));
             const double w = jt * P.glw[bq];
-            const double fu = w * u / rho * P.inv_4pi_mu;
-            const double ft = w * u / (rho * rho) * (1.0 / (4.0 * kPi));
-            const cplx dE1 = (Cc - Bb) - E10;
-            const cplx dE2 = P.lam_over_mu * (Cc - Dd - 2.0 * Bb) - 2.0 * Bb - E20;
             const double et = ev[0] * t[0] + ev[1] * t[1] + ev[2] * t[2];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] + (Aa * t[i] - Bb * (ev[i] * et)) * fu;
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j)
-                    T[3 * i + j] = T[3 * i + j] + (dE1 * (ev[j] * n[i]) + dE2 * (ev[i] * n[j])) * ft;
+            kpoint_self(P, acc, k, ev, w * u / rho * P.inv_4pi_mu, w * u / (rho * rho) * (1.0 / (4.0 * kPi)), et);
         }
+        acc.finish(n, t, T, Ut);
     } else {
         // Near element: 4^level sub-triangles (recursive midpoint split, children
         // (p0,m01,m20), (m01,p1,m12), (m20,m12,p2), (m01,m12,m20)), 7 points each.
@@ -409,22 +473,20 @@ bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* _
             const double yx = l0 * p[0][0] + l1 * p[1][0] + l2 * p[2][0];
             const double yy = l0 * p[0][1] + l1 * p[1][1] + l2 * p[2][1];
             const double yz = l0 * p[0][2] + l1 * p[1][2] + l2 * p[2][2];
-            accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area, T, Ut);
+            kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area);
         }
+        acc.finish(n, t, T, Ut);
         // subtract the far kernel's 7-point U·t for this pair (it is in the partials)
         if (lane < 7) {
-            cplx Tdummy[9];
-            cplx Uf[3] = {mk(0, 0), mk(0, 0), mk(0, 0)};
+            KAcc accf;
+            accf.zero();
             const double l0 = P.r7l[lane][0], l1 = P.r7l[lane][1], l2 = P.r7l[lane][2];
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
             const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
             const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
+            kpoint_u(P, accf, yx - x0, yy - x1, yz - x2, t, s, P.r7w[lane] * g[15]);
 #pragma unroll
-            for (int i = 0; i < 9; ++i) Tdummy[i] = mk(0.0, 0.0);
-            accumulate_ut(P, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[lane] * g[15], Tdummy, Uf);
-            Ut[0] = Ut[0] - Uf[0];
-            Ut[1] = Ut[1] - Uf[1];
-            Ut[2] = Ut[2] - Uf[2];
+            for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] - (accf.sa * t[i] - accf.sb[i]);
         }
     }
     warp_sum(T, 9);
@@ -472,8 +534,13 @@ void bem_assemble(const BemDevice& d, const cplx* svec_dev, int B, double* A, si
     const int ne = d.ne;
     const int nchunks = ceil_div(ne, kFarChunk);
     dim3 gf(ceil_div(ne, kFarThreads), nchunks, B);
+    cudaEvent_t pe;
+    profiler().begin(st, kProfAsmFar, 0.0, pe);
     FDS_LAUNCH(bem_far_kernel, gf, kFarThreads, 0, st, d.params, d.geo, d.trac, ne, svec_dev, A,
                mstride, plane, ld, d.partial, d.pstride);
+    // work unit: kernel evaluations (7 points per far pair and frequency)
+    profiler().end(st, pe, kProfAsmFar, 7.0 * ne * (ne - 1.0) * B);
+    profiler().begin(st, kProfAsmNear, 0.0, pe);
     if (B >= 8) {
         dim3 gn(ceil_div(d.npairs, 4), ceil_div(B, 32));
         FDS_LAUNCH(bem_near_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.npairs,
@@ -483,6 +550,7 @@ void bem_assemble(const BemDevice& d, const cplx* svec_dev, int B, double* A, si
         FDS_LAUNCH(bem_near_pts_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.npairs,
                    svec_dev, A, mstride, plane, ld, d.corr, d.cstride);
     }
+    profiler().end(st, pe, kProfAsmNear, static_cast<double>(d.npairs) * B);
     dim3 gr(ceil_div(3 * ne, 128), B);
     FDS_LAUNCH(bem_rhs_kernel, gr, 128, 0, st, ne, nchunks, d.partial, d.pstride, d.near_ptr, d.corr,
                d.cstride, svec_dev, rhs, rstride);

@@ -119,6 +119,7 @@ BemParams make_bem_params(double mu, double nu, double rho) {
     P.inv_cs = 1.0 / P.cs;
     const double cp = std::sqrt((P.lambda + 2.0 * mu) / rho);
     P.k = P.cs / cp;
+    P.inv_k = cp / P.cs;
     P.inv_4pi_mu = 1.0 / (4.0 * pi * mu);
     double fact[BemParams::kTerms + 3];
     fact[0] = 1.0;
