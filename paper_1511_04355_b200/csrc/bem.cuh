@@ -32,6 +32,7 @@ struct BemDevice {
     double* trac = nullptr;   // [ne][3]
     int* pairs = nullptr;     // [npairs][3]: c, e, level (-1 = self)
     int* near_ptr = nullptr;  // [ne+1] CSR by c into pairs
+    int* order = nullptr;     // [npairs] near-kernel processing order (costliest first)
     int npairs = 0;
     cplx* partial = nullptr;  // [B][nchunks][3ne]
     size_t pstride = 0;

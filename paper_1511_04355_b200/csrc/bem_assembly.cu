@@ -184,7 +184,7 @@ __device__ __forceinline__ void kpoint_cpv(const BemParams& P, KAcc& acc, const 
 }  // namespace
 
 // ------------------------------------------------------------------ far field
-__global__ void __launch_bounds__(kFarThreads)
+__global__ void __launch_bounds__(kFarThreads, 3)
 bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __restrict__ trac,
                int ne, const cplx* __restrict__ svec, double* __restrict__ A, size_t mstride,
                size_t plane, int ld, cplx* __restrict__ partial, size_t pstride) {
@@ -212,7 +212,7 @@ bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __rest
         const double t[3] = {st[el][0], st[el][1], st[el][2]};
         KAcc acc;
         acc.zero();
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < 7; ++q) {
             const double l0 = P.r7l[q][0], l1 = P.r7l[q][1], l2 = P.r7l[q][2];
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
@@ -245,15 +245,16 @@ bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __rest
 // One warp per listed near/self pair and 32 frequencies: lane b integrates the
 // whole pair for frequency b (the quadrature geometry is warp-uniform), so
 // there is no cross-lane reduction and all 32 lanes do useful work.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 3)
 bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __restrict__ trac,
-                int ne, const int* __restrict__ pairs, int npairs, const cplx* __restrict__ svec, int B,
-                double* __restrict__ A, size_t mstride, size_t plane, int ld,
+                int ne, const int* __restrict__ pairs, const int* __restrict__ order, int npairs,
+                const cplx* __restrict__ svec, int B, double* __restrict__ A, size_t mstride, size_t plane, int ld,
                 cplx* __restrict__ corr, size_t cstride) {
-    const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.y * 32 + lane;
-    if (pair >= npairs) return;
+    if (slot >= npairs) return;
+    const int pair = order[slot];
     const bool active = b < B;
     const int c = pairs[3 * pair], e = pairs[3 * pair + 1], level = pairs[3 * pair + 2];
     const cplx s = svec[active ? b : 0];
@@ -287,6 +288,7 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
                 const double lnR = log(R) / (R * R) * jt * (1.0 / (4.0 * kPi));
                 kpoint_cpv(P, acc, ev, lnR);
                 const double et = ev[0] * t[0] + ev[1] * t[1] + ev[2] * t[2];
+#pragma unroll 1
                 for (int bq = 0; bq < NG; ++bq) {
                     const double u = P.glx[bq];
                     const double rho = R * u;
@@ -329,6 +331,7 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
             const double vx = p[2][0] - p[0][0], vy = p[2][1] - p[0][1], vz = p[2][2] - p[0][2];
             const double cx = uy * vz - uz * vy, cy = uz * vx - ux * vz, cz = ux * vy - uy * vx;
             const double area = 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+#pragma unroll 1
             for (int gq = 0; gq < 7; ++gq) {
                 const double l0 = P.r7l[gq][0], l1 = P.r7l[gq][1], l2 = P.r7l[gq][2];
                 const double yx = l0 * p[0][0] + l1 * p[1][0] + l2 * p[2][0];
@@ -340,6 +343,7 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
         // subtract the far kernel's 7-point U·t for this pair (it is in the partials)
         KAcc accf;
         accf.zero();
+#pragma unroll 1
         for (int gq = 0; gq < 7; ++gq) {
             const double l0 = P.r7l[gq][0], l1 = P.r7l[gq][1], l2 = P.r7l[gq][2];
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
@@ -543,7 +547,7 @@ void bem_assemble(const BemDevice& d, const cplx* svec_dev, int B, double* A, si
     profiler().begin(st, kProfAsmNear, 0.0, pe);
     if (B >= 8) {
         dim3 gn(ceil_div(d.npairs, 4), ceil_div(B, 32));
-        FDS_LAUNCH(bem_near_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.npairs,
+        FDS_LAUNCH(bem_near_kernel, gn, 128, 0, st, d.params, d.geo, d.trac, ne, d.pairs, d.order, d.npairs,
                    svec_dev, B, A, mstride, plane, ld, d.corr, d.cstride);
     } else {
         dim3 gn(ceil_div(d.npairs * 32, 128), B);

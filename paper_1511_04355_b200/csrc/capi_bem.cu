@@ -238,6 +238,17 @@ int fds_bem_create(const fds_bem_desc* d, fds_bem** out) {
             FDS_CUDA(cudaMemcpy(h->dev.trac, d->traction, 3 * h->ne * sizeof(double), cudaMemcpyHostToDevice));
             FDS_CUDA(cudaMemcpy(h->dev.pairs, pairs.data(), pairs.size() * sizeof(int), cudaMemcpyHostToDevice));
             FDS_CUDA(cudaMemcpy(h->dev.near_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+            // near-kernel processing order: costliest pairs first (self polar rule,
+            // then deepest subdivision), so warps sharing a CTA carry equal work
+            {
+                const int np = h->dev.npairs;
+                std::vector<int> order(np);
+                for (int q = 0; q < np; ++q) order[q] = q;
+                auto cost = [&](int q) { const int lv = pairs[3 * q + 2]; return lv < 0 ? 1 << 20 : 1 << (2 * lv); };
+                std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+                FDS_CUDA(cudaMalloc(&h->dev.order, std::max(np, 1) * sizeof(int)));
+                FDS_CUDA(cudaMemcpy(h->dev.order, order.data(), np * sizeof(int), cudaMemcpyHostToDevice));
+            }
             FDS_CUDA(cudaMemcpy(h->chan, chans.data(), chans.size() * sizeof(int), cudaMemcpyHostToDevice));
         } catch (...) {
             fds_bem_destroy(h);
@@ -252,7 +263,7 @@ int fds_bem_destroy(fds_bem* h) {
     auto fr = [](void* p) { if (p) cudaFree(p); };
     if (h->st) cudaStreamSynchronize(h->st);
     fr(h->A); fr(h->ipiv); fr(h->info); fr(h->rhs); fr(h->svec); fr(h->out); fr(h->chan);
-    fr(h->dev.geo); fr(h->dev.trac); fr(h->dev.pairs); fr(h->dev.near_ptr); fr(h->dev.partial); fr(h->dev.corr);
+    fr(h->dev.geo); fr(h->dev.trac); fr(h->dev.pairs); fr(h->dev.order); fr(h->dev.near_ptr); fr(h->dev.partial); fr(h->dev.corr);
     h->ws.release();
     for (auto e : h->ev) if (e) cudaEventDestroy(e);
     if (h->st) cudaStreamDestroy(h->st);
