@@ -662,95 +662,161 @@ lu_sub_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k
 }
 
 // ------------------------------------------------------------------ solves
-__global__ void lu_fwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld,
-                                    int k, int w, const int* ipiv, cplx* rhs, size_t rstride) {
-    __shared__ cplx y[64];
-    const int b = blockIdx.x;
+// Blocked substitution, one 64-wide block column per step (the factor's panel
+// width). Panel kernels: one CTA of 64 threads per matrix; thread i holds row i
+// of the diagonal block in registers, so the serial triangular recurrence only
+// waits on one barrier per column. GEMV kernels: 32-row slabs x 8 column
+// groups per CTA, so even a single matrix puts ~25 warps of loads on every SM.
+constexpr int kSolveW = 64;
+
+__global__ void __launch_bounds__(kSolveW)
+lu_fwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, const int* ipiv,
+                    cplx* rhs, size_t rstride) {
+    __shared__ cplx y[kSolveW], ext[kSolveW];
+    __shared__ int pvs[kSolveW];
+    const int b = blockIdx.x, tid = threadIdx.x;
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     cplx* x = rhs + static_cast<size_t>(b) * rstride;
-    const int tid = threadIdx.x;
+    const int* pv = ipiv + static_cast<size_t>(b) * n;
+    // row tid of the unit-lower diagonal block, L[tid][j] for j < tid
+    double lr[kSolveW - 1], li[kSolveW - 1];
+#pragma unroll
+    for (int j = 0; j < kSolveW - 1; ++j) {
+        lr[j] = li[j] = 0.0;
+        if (j < tid && tid < w) {
+            const size_t gi = static_cast<size_t>(k + j) * ld + k + tid;
+            lr[j] = Are[gi];
+            li[j] = Aim[gi];
+        }
+    }
+    // row interchanges of this block (LAPACK order): the block segment and the
+    // rows below it that the pivots name are staged in smem, swapped by one
+    // thread in order, and written back (each outside row by its first slot)
+    int r = -1;
+    if (tid < w) {
+        r = pv[k + tid];
+        pvs[tid] = r;
+        y[tid] = x[k + tid];
+        if (r >= k + w) ext[tid] = x[r];
+    }
+    __syncthreads();
     if (tid == 0) {
-        const int* pv = ipiv + static_cast<size_t>(b) * n;
-        for (int c = k; c < k + w; ++c) {
-            const int r = pv[c];
-            if (r != c) { const cplx t = x[c]; x[c] = x[r]; x[r] = t; }
+        for (int c = 0; c < w; ++c) {
+            const int rc = pvs[c];
+            if (rc == k + c) continue;
+            if (rc < k + w) {
+                const cplx t = y[c]; y[c] = y[rc - k]; y[rc - k] = t;
+            } else {
+                int slot = 0;
+                while (pvs[slot] != rc) ++slot;
+                const cplx t = y[c]; y[c] = ext[slot]; ext[slot] = t;
+            }
         }
     }
     __syncthreads();
-    if (tid < w) y[tid] = x[k + tid];
-    __syncthreads();
-    for (int j = 0; j < w - 1; ++j) {
+    if (tid < w && r >= k + w) {
+        bool first = true;
+        for (int c = 0; c < tid; ++c) first = first && pvs[c] != r;
+        if (first) x[r] = ext[tid];
+    }
+    // unit-lower solve
+    cplx yt = tid < w ? y[tid] : mk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < kSolveW - 1; ++j) {
+        if (j >= w - 1) break;
+        __syncthreads();
+        const cplx yj = y[j];
         if (tid > j && tid < w) {
-            const size_t gi = static_cast<size_t>(k + j) * ld + k + tid;
-            y[tid] = y[tid] - mk(Are[gi], Aim[gi]) * y[j];
+            yt = yt - mk(lr[j], li[j]) * yj;
+            y[tid] = yt;
         }
-        __syncthreads();
     }
-    if (tid < w) x[k + tid] = y[tid];
+    if (tid < w) x[k + tid] = yt;
 }
 
-__global__ void lu_fwd_gemv_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k,
-                                   int w, cplx* rhs, size_t rstride) {
-    __shared__ cplx y[64];
+// x[r] -= A[r][k:k+w] y for a 32-row slab per CTA: warp g sums columns
+// 8g..8g+7 for the slab's 32 consecutive rows (coalesced), then the 8 partial
+// sums are reduced through smem in a fixed order.
+constexpr int kGemvRows = 32, kGemvGroups = kSolveW / 8;
+
+template <bool FWD>
+__global__ void __launch_bounds__(kGemvRows * kGemvGroups)
+lu_gemv_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, cplx* rhs,
+               size_t rstride) {
+    __shared__ cplx y[kSolveW];
+    __shared__ cplx part[kGemvGroups][kGemvRows];
     const int b = blockIdx.y;
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     cplx* x = rhs + static_cast<size_t>(b) * rstride;
-    if (threadIdx.x < w) y[threadIdx.x] = x[k + threadIdx.x];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    if (threadIdx.x < kSolveW) y[threadIdx.x] = threadIdx.x < w ? x[k + threadIdx.x] : mk(0.0, 0.0);
     __syncthreads();
-    const int r = k + w + blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    cplx acc = mk(0.0, 0.0);
-    for (int j = 0; j < w; ++j) {
-        const size_t gi = static_cast<size_t>(k + j) * ld + r;
-        acc = acc + mk(Are[gi], Aim[gi]) * y[j];
+    const int r = (FWD ? k + w : 0) + blockIdx.x * kGemvRows + lane;
+    const bool ok = FWD ? r < n : r < k;
+    double ar = 0.0, ai = 0.0;
+    if (ok) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int j = 8 * g + jj;
+            if (j < w) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + r;
+                const double mr = Are[gi], mi = Aim[gi];
+                ar += mr * y[j].re - mi * y[j].im;
+                ai += mr * y[j].im + mi * y[j].re;
+            }
+        }
     }
-    x[r] = x[r] - acc;
+    part[g][lane] = mk(ar, ai);
+    __syncthreads();
+    if (g == 0 && ok) {
+        cplx acc = part[0][lane];
+#pragma unroll
+        for (int q = 1; q < kGemvGroups; ++q) acc = acc + part[q][lane];
+        x[r] = x[r] - acc;
+    }
 }
 
-__global__ void lu_bwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld,
-                                    int k, int w, cplx* rhs, size_t rstride) {
-    __shared__ cplx y[64];
-    const int b = blockIdx.x;
+__global__ void __launch_bounds__(kSolveW)
+lu_bwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, cplx* rhs,
+                    size_t rstride) {
+    __shared__ cplx y[kSolveW];
+    const int b = blockIdx.x, tid = threadIdx.x;
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     cplx* x = rhs + static_cast<size_t>(b) * rstride;
-    const int tid = threadIdx.x;
-    if (tid < w) y[tid] = x[k + tid];
-    __syncthreads();
-    for (int j = w - 1; j >= 0; --j) {
-        if (tid == j) {
-            const size_t gi = static_cast<size_t>(k + j) * ld + k + j;
-            y[j] = cdiv(y[j], mk(Are[gi], Aim[gi]));
+    // row tid of the upper diagonal block, U[tid][j] for j >= tid
+    double ur[kSolveW], ui[kSolveW];
+#pragma unroll
+    for (int j = 0; j < kSolveW; ++j) {
+        ur[j] = ui[j] = 0.0;
+        if (j >= tid && j < w) {
+            const size_t gi = static_cast<size_t>(k + j) * ld + k + tid;
+            ur[j] = Are[gi];
+            ui[j] = Aim[gi];
         }
+    }
+    cplx diag = mk(1.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < kSolveW; ++j)
+        if (j == tid) diag = mk(ur[j], ui[j]);
+    cplx yt = tid < w ? x[k + tid] : mk(0.0, 0.0);
+    if (tid == w - 1) yt = cdiv(yt, diag);
+    if (tid < w) y[tid] = yt;
+    // column j final (divided) at the top of its step; row j-1 divides right after its last update
+#pragma unroll
+    for (int j = kSolveW - 1; j >= 1; --j) {
+        if (j >= w) continue;
         __syncthreads();
+        const cplx yj = y[j];
         if (tid < j) {
-            const size_t gi = static_cast<size_t>(k + j) * ld + k + tid;
-            y[tid] = y[tid] - mk(Are[gi], Aim[gi]) * y[j];
+            yt = yt - mk(ur[j], ui[j]) * yj;
+            if (tid == j - 1) yt = cdiv(yt, diag);
+            y[tid] = yt;
         }
-        __syncthreads();
     }
-    if (tid < w) x[k + tid] = y[tid];
-}
-
-__global__ void lu_bwd_gemv_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k,
-                                   int w, cplx* rhs, size_t rstride) {
-    __shared__ cplx y[64];
-    const int b = blockIdx.y;
-    const double* Are = A + static_cast<size_t>(b) * mstride;
-    const double* Aim = Are + plane;
-    cplx* x = rhs + static_cast<size_t>(b) * rstride;
-    if (threadIdx.x < w) y[threadIdx.x] = x[k + threadIdx.x];
-    __syncthreads();
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= k) return;
-    cplx acc = mk(0.0, 0.0);
-    for (int j = 0; j < w; ++j) {
-        const size_t gi = static_cast<size_t>(k + j) * ld + r;
-        acc = acc + mk(Are[gi], Aim[gi]) * y[j];
-    }
-    x[r] = x[r] - acc;
+    if (tid < w) x[k + tid] = yt;
 }
 
 // ------------------------------------------------------------------ host
@@ -1061,23 +1127,23 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st) {
     const int nb = lu_panel_width(pb.n);
     for (int k = 0; k < pb.n; k += nb) {
         const int w = std::min(nb, pb.n - k);
-        FDS_LAUNCH(lu_fwd_panel_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
+        FDS_LAUNCH(lu_fwd_panel_kernel, pb.batch, kSolveW, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
                    pb.ipiv, rhs, rstride);
         const int rest = pb.n - k - w;
         if (rest > 0) {
-            dim3 g(ceil_div(rest, 128), pb.batch);
-            FDS_LAUNCH(lu_fwd_gemv_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, rhs,
+            dim3 g(ceil_div(rest, kGemvRows), pb.batch);
+            FDS_LAUNCH(lu_gemv_kernel<true>, g, kGemvRows * kGemvGroups, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, rhs,
                        rstride);
         }
     }
     const int last = ((pb.n - 1) / nb) * nb;
     for (int k = last; k >= 0; k -= nb) {
         const int w = std::min(nb, pb.n - k);
-        FDS_LAUNCH(lu_bwd_panel_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
+        FDS_LAUNCH(lu_bwd_panel_kernel, pb.batch, kSolveW, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w,
                    rhs, rstride);
         if (k > 0) {
-            dim3 g(ceil_div(k, 128), pb.batch);
-            FDS_LAUNCH(lu_bwd_gemv_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, rhs,
+            dim3 g(ceil_div(k, kGemvRows), pb.batch);
+            FDS_LAUNCH(lu_gemv_kernel<false>, g, kGemvRows * kGemvGroups, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, rhs,
                        rstride);
         }
     }
