@@ -422,73 +422,159 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
 }
 
 // ------------------------------------------------------------------ TRSM via L11^{-1} (DMMA)
-// U12 = L11^{-1} P A12: the unit-lower 64x64 inverse is formed once per panel
-// and matrix (lu_l11_inverse_kernel), then every 64-column strip applies the
-// panel's row swaps in shared memory and multiplies by L11^{-1} on the FP64
-// tensor pipe (lu_swap_apply_kernel), replacing 63 dependent sweeps per strip.
-__global__ void __launch_bounds__(64)
-lu_l11_inverse_kernel(const double* A, size_t mstride, size_t plane, int ld, int k, double* linv) {
+// U12 = L11^{-1} P A12: per panel and matrix, lu_l11_inverse_kernel forms the
+// unit-lower 64x64 inverse and resolves the panel's 64 sequential row swaps
+// into one gather (source row of every panel row and of every outside row a
+// pivot names); lu_swap_apply_kernel then permutes each 64-column strip with
+// independent loads and multiplies by L11^{-1} on the FP64 tensor pipe.
+constexpr size_t kLinvStride = 2 * 64 * 64 + 128;  // doubles per matrix: Linv planes + swap map (ints)
+constexpr int kInvThreads = 256;
+
+// Sources are "virtual" indices into V = [panel rows k..k+63, erow[0..next)]:
+// v < 64 is panel row k + v, v >= 64 is outside row erow[v - 64].
+struct SwapMap {  // lives in the int tail of a matrix's kLinvStride record
+    int psrc[64];     // source (virtual) of panel row k + c
+    int next;         // outside rows touched
+    int erow[64];     // those rows
+    int esrc[64];     // and their sources (virtual)
+};
+static_assert(sizeof(SwapMap) <= 128 * sizeof(double), "swap map record");
+
+__global__ void __launch_bounds__(kInvThreads)
+lu_l11_inverse_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k, const int* ipiv,
+                      double* linv) {
     extern __shared__ double ism[];
-    double* lre = ism;              // [col m][row i], stride 65
-    double* lim = lre + 64 * 65;
-    double* xre = lim + 64 * 65;    // [row i][col c], stride 65
-    double* xim = xre + 64 * 65;
-    const int b = blockIdx.x, c = threadIdx.x;
+    double (*lre)[65] = reinterpret_cast<double (*)[65]>(ism);             // L[i][m]
+    double (*lim)[65] = reinterpret_cast<double (*)[65]>(ism + 64 * 65);
+    double (*xre)[65] = reinterpret_cast<double (*)[65]>(ism + 2 * 64 * 65);  // published rows of X = L^{-1}
+    double (*xim)[65] = reinterpret_cast<double (*)[65]>(ism + 3 * 64 * 65);
+    const int b = blockIdx.x, t = threadIdx.x;
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
-    for (int q = c; q < 64 * 64; q += 64) {
-        const int j = q / 64, i = q % 64;
-        const size_t gi = static_cast<size_t>(k + j) * ld + k + i;
-        lre[j * 65 + i] = Are[gi];
-        lim[j * 65 + i] = Aim[gi];
+    for (int q = t; q < 64 * 64; q += kInvThreads) {
+        const int m = q / 64, i = q % 64;
+        const size_t gi = static_cast<size_t>(k + m) * ld + k + i;
+        lre[i][m] = Are[gi];
+        lim[i][m] = Aim[gi];
+    }
+    double* rec = linv + static_cast<size_t>(b) * kLinvStride;
+    __shared__ int pvs[64], psrc[64];
+    if (t < 64) {
+        pvs[t] = ipiv[static_cast<size_t>(b) * n + k + t];
+        psrc[t] = k + t;
     }
     __syncthreads();
-    // column c of X = L^{-1}: X[c][c] = 1, X[i][c] = -sum_{m=c}^{i-1} L[i][m] X[m][c]
-    for (int i = 0; i < 64; ++i) {
-        double sr = 0.0, si = 0.0;
-        if (i > c) {
-            for (int m = c; m < i; ++m) {
-                const double a = lre[m * 65 + i], bb = lim[m * 65 + i];
-                const double yr = xre[m * 65 + c], yi = xim[m * 65 + c];
-                sr += a * yr - bb * yi;
-                si += a * yi + bb * yr;
+    if (t < 32) {  // warp 0: sequential LAPACK swaps -> gather map (outside rows held by lanes)
+        int er0 = -1, er1 = -1, es0 = 0, es1 = 0, ne = 0;
+        for (int c = 0; c < 64; ++c) {
+            const int r = pvs[c];
+            if (r == k + c) continue;
+            if (r < k + 64) {
+                if (t == 0) { const int tmp = psrc[c]; psrc[c] = psrc[r - k]; psrc[r - k] = tmp; }
+            } else {
+                const unsigned lo = __ballot_sync(0xffffffffu, er0 == r), hi = __ballot_sync(0xffffffffu, er1 == r);
+                int j = lo ? __ffs(lo) - 1 : (hi ? 32 + __ffs(hi) - 1 : ne);
+                if (j == ne) {  // first time this row is named
+                    if (t == (j & 31)) { if (j < 32) { er0 = r; es0 = r; } else { er1 = r; es1 = r; } }
+                    ++ne;
+                }
+                if (t == (j & 31)) {
+                    int& es = j < 32 ? es0 : es1;
+                    const int tmp = psrc[c]; psrc[c] = es; es = tmp;
+                }
             }
-            sr = -sr;
-            si = -si;
-        } else if (i == c) {
-            sr = 1.0;
+            __syncwarp();
         }
-        xre[i * 65 + c] = sr;
-        xim[i * 65 + c] = si;
+        // rows -> virtual indices (outside rows by their slot)
+        __shared__ int erow_s[64];
+        if (t < ne) erow_s[t] = er0;
+        if (t + 32 < ne) erow_s[t + 32] = er1;
+        __syncwarp();
+        auto virt = [&](int row) {
+            if (row < k + 64) return row - k;
+            int j = 0;
+            while (erow_s[j] != row) ++j;
+            return 64 + j;
+        };
+        SwapMap* sm = reinterpret_cast<SwapMap*>(rec + 2 * 64 * 64);
+        sm->psrc[t] = virt(psrc[t]);
+        sm->psrc[t + 32] = virt(psrc[t + 32]);
+        if (t == 0) sm->next = ne;
+        if (t < ne) { sm->erow[t] = er0; sm->esrc[t] = virt(es0); }
+        if (t + 32 < ne) { sm->erow[t + 32] = er1; sm->esrc[t + 32] = virt(es1); }
     }
-    double* out = linv + static_cast<size_t>(b) * 2 * 64 * 64;
-    for (int i = 0; i < 64; ++i) {
-        out[c * 64 + i] = xre[i * 65 + c];  // [col c][row i]
-        out[64 * 64 + c * 64 + i] = xim[i * 65 + c];
+    // right-looking inverse: thread t owns row i = t/4, columns c = t%4 + 4q of X
+    const int i = t >> 2, c0 = t & 3;
+    double vr[16], vi[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        vr[q] = (c0 + 4 * q == i) ? 1.0 : 0.0;
+        vi[q] = 0.0;
+    }
+    __syncthreads();
+    for (int m = 0; m < 63; ++m) {
+        if (i == m) {  // row m is final: publish it
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                xre[m][c0 + 4 * q] = vr[q];
+                xim[m][c0 + 4 * q] = vi[q];
+            }
+        }
+        __syncthreads();
+        if (i > m) {
+            const double a = lre[i][m], bb = lim[i][m];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int c = c0 + 4 * q;
+                if (c <= m) {
+                    const double yr = xre[m][c], yi = xim[m][c];
+                    vr[q] -= a * yr - bb * yi;
+                    vi[q] -= a * yi + bb * yr;
+                }
+            }
+        }
+    }
+    // Linv stored [col c][row i]
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int c = c0 + 4 * q;
+        rec[c * 64 + i] = vr[q];
+        rec[64 * 64 + c * 64 + i] = vi[q];
     }
 }
 
 constexpr int SAS = 68;  // padded smem stride (≡ 4 mod 16 doubles)
 
 __global__ void __launch_bounds__(128)
-lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const int* ipiv,
-                     const double* linv) {
+lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv) {
     extern __shared__ __align__(16) double ssm[];
     double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
     double* Li = Lr + 64 * SAS;
     double* Xr = Li + 64 * SAS;       // [n][kk]
     double* Xi = Xr + 64 * SAS;
+    double* Er = Xi + 64 * SAS;       // [n][j] original values of the outside rows
+    double* Ei = Er + 64 * 65;
+    __shared__ SwapMap map;
     const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
     const int col0 = k + 64 + blockIdx.x * 64;
     const int ncols = min(64, n - col0);
-    const double* L = linv + static_cast<size_t>(b) * 2 * 64 * 64;
+    const double* rec = linv + static_cast<size_t>(b) * kLinvStride;
+    const double* L = rec;
+    {
+        const int* src = reinterpret_cast<const int*>(rec + 2 * 64 * 64);
+        int* dst = reinterpret_cast<int*>(&map);
+        for (int q = tid; q < static_cast<int>(sizeof(SwapMap) / sizeof(int)); q += blockDim.x) dst[q] = src[q];
+    }
     for (int q = tid; q < 64 * 64; q += blockDim.x) {
         const int kk = q / 64, m = q % 64;
         Lr[kk * SAS + m] = L[kk * 64 + m];
         Li[kk * SAS + m] = L[64 * 64 + kk * 64 + m];
     }
+    __syncthreads();
+    const int ne = map.next;
+    // V = original panel rows (coalesced) and outside rows (one element per column)
     for (int q = tid; q < 64 * 64; q += blockDim.x) {
         const int nn = q / 64, kk = q % 64;
         double vr = 0.0, vi = 0.0;
@@ -500,28 +586,47 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         Xr[nn * SAS + kk] = vr;
         Xi[nn * SAS + kk] = vi;
     }
+    for (int q = tid; q < 64 * ne; q += blockDim.x) {
+        const int nn = q / ne, j = q % ne;
+        double vr = 0.0, vi = 0.0;
+        if (nn < ncols) {
+            const size_t gi = static_cast<size_t>(col0 + nn) * ld + map.erow[j];
+            vr = Are[gi];
+            vi = Aim[gi];
+        }
+        Er[nn * 65 + j] = vr;
+        Ei[nn * 65 + j] = vi;
+    }
     __syncthreads();
-    if (tid < ncols) {  // the panel's sequential row swaps, one column per thread
-        const size_t colbase = static_cast<size_t>(col0 + tid) * ld;
-        const int* pv = ipiv + static_cast<size_t>(b) * n;
-        for (int c = k; c < k + 64; ++c) {
-            const int r = pv[c];
-            if (r == c) continue;
-            const int lc = c - k;
-            if (r < k + 64) {
-                const int lr = r - k;
-                double t0 = Xr[tid * SAS + lc], t1 = Xi[tid * SAS + lc];
-                Xr[tid * SAS + lc] = Xr[tid * SAS + lr];
-                Xi[tid * SAS + lc] = Xi[tid * SAS + lr];
-                Xr[tid * SAS + lr] = t0;
-                Xi[tid * SAS + lr] = t1;
-            } else {
-                const double gr = Are[colbase + r], gi = Aim[colbase + r];
-                Are[colbase + r] = Xr[tid * SAS + lc];
-                Aim[colbase + r] = Xi[tid * SAS + lc];
-                Xr[tid * SAS + lc] = gr;
-                Xi[tid * SAS + lc] = gi;
-            }
+    auto vget = [&](int nn, int v, double& vr, double& vi) {
+        if (v < 64) { vr = Xr[nn * SAS + v]; vi = Xi[nn * SAS + v]; }
+        else { vr = Er[nn * 65 + v - 64]; vi = Ei[nn * 65 + v - 64]; }
+    };
+    // outside rows receive their sources
+    for (int q = tid; q < 64 * ne; q += blockDim.x) {
+        const int nn = q / ne, j = q % ne;
+        if (nn < ncols) {
+            double vr, vi;
+            vget(nn, map.esrc[j], vr, vi);
+            const size_t gi = static_cast<size_t>(col0 + nn) * ld + map.erow[j];
+            Are[gi] = vr;
+            Aim[gi] = vi;
+        }
+    }
+    // panel rows permuted in place through registers
+    {
+        double pr[32], pi[32];
+#pragma unroll
+        for (int p = 0; p < 32; ++p) {
+            const int q = tid + 128 * p, nn = q / 64, kk = q % 64;
+            vget(nn, map.psrc[kk], pr[p], pi[p]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < 32; ++p) {
+            const int q = tid + 128 * p, nn = q / 64, kk = q % 64;
+            Xr[nn * SAS + kk] = pr[p];
+            Xi[nn * SAS + kk] = pi[p];
         }
     }
     __syncthreads();
@@ -838,7 +943,7 @@ void LuWorkspace::ensure(int groups, int P, int nb) {
 double* LuWorkspace::linv(int batch) {
     if (batch > linv_cap) {
         if (linv_buf) cudaFree(linv_buf);
-        FDS_CUDA(cudaMalloc(&linv_buf, static_cast<size_t>(batch) * 2 * 64 * 64 * sizeof(double)));
+        FDS_CUDA(cudaMalloc(&linv_buf, static_cast<size_t>(batch) * kLinvStride * sizeof(double)));
         linv_cap = batch;
     }
     return linv_buf;
@@ -936,7 +1041,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
     cudaEvent_t te;
     profiler().begin(st, kProfLuTrsm, 0.0, te);
     if (NB == 64 && w == 64) {
-        const size_t asmem = 4 * 64 * SAS * sizeof(double);
+        const size_t asmem = (4 * 64 * SAS + 2 * 64 * 65) * sizeof(double);
         const size_t ismem = 4 * 64 * 65 * sizeof(double);
         static bool aset = false;
         if (!aset) {
@@ -946,9 +1051,10 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
                                           static_cast<int>(ismem)));
             aset = true;
         }
-        FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, 64, ismem, st, pb.A, pb.mstride, pb.plane, pb.ld, k, linv);
+        FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, kInvThreads, ismem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
+                   pb.ipiv, linv);
         FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, 64), pb.batch), 128, asmem, st, pb.A, pb.mstride,
-                   pb.plane, pb.n, pb.ld, k, pb.ipiv, linv);
+                   pb.plane, pb.n, pb.ld, k, linv);
     } else {
         dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
         FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, kTrsmThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
@@ -1073,7 +1179,7 @@ void lu_factor_pipelined(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) 
     ph[1].ipiv = pb.ipiv + static_cast<size_t>(b0) * pb.n;
     ph[1].info = pb.info + b0;
     double* linv_all = ws.linv(pb.batch);
-    double* linv[2] = {linv_all, linv_all + static_cast<size_t>(b0) * 2 * 64 * 64};
+    double* linv[2] = {linv_all, linv_all + static_cast<size_t>(b0) * kLinvStride};
     FDS_CUDA(cudaEventRecord(ev_start, st));
     FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_start, 0));
     FDS_CUDA(cudaStreamWaitEvent(s_lo, ev_start, 0));
