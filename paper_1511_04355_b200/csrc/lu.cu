@@ -503,43 +503,74 @@ lu_l11_inverse_kernel(const double* A, size_t mstride, size_t plane, int n, int 
         if (t < ne) { sm->erow[t] = er0; sm->esrc[t] = virt(es0); }
         if (t + 32 < ne) { sm->erow[t + 32] = er1; sm->esrc[t + 32] = virt(es1); }
     }
-    // right-looking inverse: thread t owns row i = t/4, columns c = t%4 + 4q of X
-    const int i = t >> 2, c0 = t & 3;
-    double vr[16], vi[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        vr[q] = (c0 + 4 * q == i) ? 1.0 : 0.0;
-        vi[q] = 0.0;
+    // blocked inverse, 16x16 blocks D_I on the diagonal:
+    //   X_II = D_I^{-1} (warp I, lane = column, in registers)
+    //   X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ   for I = 1..3, J < I (block rows in order)
+    double (*tre)[17] = reinterpret_cast<double (*)[17]>(ism + 4 * 64 * 65);  // [3 * 16][17] scratch
+    double (*tim)[17] = reinterpret_cast<double (*)[17]>(ism + 4 * 64 * 65 + 48 * 17);
+    const int warp = t >> 5, lane = t & 31;
+    for (int q = t; q < 64 * 64; q += kInvThreads) {  // X = 0 (upper blocks stay zero)
+        xre[q / 64][q % 64] = 0.0;
+        xim[q / 64][q % 64] = 0.0;
     }
     __syncthreads();
-    for (int m = 0; m < 63; ++m) {
-        if (i == m) {  // row m is final: publish it
+    if (warp < 4 && lane < 16) {
+        const int o = 16 * warp, c = lane;
+        double xr[16], xi[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                xre[m][c0 + 4 * q] = vr[q];
-                xim[m][c0 + 4 * q] = vi[q];
-            }
-        }
-        __syncthreads();
-        if (i > m) {
-            const double a = lre[i][m], bb = lim[i][m];
+        for (int i = 0; i < 16; ++i) {
+            double sr = 0.0, si = 0.0;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int c = c0 + 4 * q;
-                if (c <= m) {
-                    const double yr = xre[m][c], yi = xim[m][c];
-                    vr[q] -= a * yr - bb * yi;
-                    vi[q] -= a * yi + bb * yr;
+            for (int m = 0; m < i; ++m) {
+                if (m >= c) {
+                    const double a = lre[o + i][o + m], bb = lim[o + i][o + m];
+                    sr += a * xr[m] - bb * xi[m];
+                    si += a * xi[m] + bb * xr[m];
                 }
             }
+            xr[i] = i < c ? 0.0 : (i == c ? 1.0 : -sr);
+            xi[i] = i <= c ? 0.0 : -si;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            xre[o + i][o + c] = xr[i];
+            xim[o + i][o + c] = xi[i];
         }
     }
-    // Linv stored [col c][row i]
+    __syncthreads();
+    const int r = t >> 4, c = t & 15;
+    for (int I = 1; I < 4; ++I) {
+        for (int J = 0; J < I; ++J) {  // T_J = sum_K L_IK X_KJ
+            double sr = 0.0, si = 0.0;
+            for (int kk = 16 * J; kk < 16 * I; ++kk) {
+                const double a = lre[16 * I + r][kk], bb = lim[16 * I + r][kk];
+                const double yr = xre[kk][16 * J + c], yi = xim[kk][16 * J + c];
+                sr += a * yr - bb * yi;
+                si += a * yi + bb * yr;
+            }
+            tre[16 * J + r][c] = sr;
+            tim[16 * J + r][c] = si;
+        }
+        __syncthreads();
+        for (int J = 0; J < I; ++J) {  // X_IJ = -X_II T_J
+            double sr = 0.0, si = 0.0;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int c = c0 + 4 * q;
-        rec[c * 64 + i] = vr[q];
-        rec[64 * 64 + c * 64 + i] = vi[q];
+            for (int kk = 0; kk < 16; ++kk) {
+                const double a = xre[16 * I + r][16 * I + kk], bb = xim[16 * I + r][16 * I + kk];
+                const double yr = tre[16 * J + kk][c], yi = tim[16 * J + kk][c];
+                sr += a * yr - bb * yi;
+                si += a * yi + bb * yr;
+            }
+            xre[16 * I + r][16 * J + c] = -sr;
+            xim[16 * I + r][16 * J + c] = -si;
+        }
+        __syncthreads();
+    }
+    // Linv stored [col c][row i]
+    for (int q = t; q < 64 * 64; q += kInvThreads) {
+        const int cc = q / 64, i = q % 64;
+        rec[cc * 64 + i] = xre[i][cc];
+        rec[64 * 64 + cc * 64 + i] = xim[i][cc];
     }
 }
 
@@ -1042,7 +1073,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
     profiler().begin(st, kProfLuTrsm, 0.0, te);
     if (NB == 64 && w == 64) {
         const size_t asmem = (4 * 64 * SAS + 2 * 64 * 65) * sizeof(double);
-        const size_t ismem = 4 * 64 * 65 * sizeof(double);
+        const size_t ismem = (4 * 64 * 65 + 2 * 48 * 17) * sizeof(double);
         static bool aset = false;
         if (!aset) {
             FDS_CUDA(cudaFuncSetAttribute(lu_swap_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
