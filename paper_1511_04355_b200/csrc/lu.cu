@@ -20,7 +20,13 @@
 //                        double-buffered smem, bank-conflict-free padded layouts.
 // Row swaps are LAPACK-style inside a panel and LINPACK-style across panels
 // (earlier L columns are not permuted); lu_solve applies them in that order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <climits>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 #include <string>
 
@@ -403,6 +409,155 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
         __syncthreads();
     }
     // epilogue: store C - L21 U12
+#pragma unroll
+    for (int mi = 0; mi < GMI; ++mi) {
+        const int row = m0 + wm * (GBM / GWM) + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < GNI; ++ni) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
+                if (row < n && col < n) {
+                    const size_t gi = static_cast<size_t>(col) * ld + row;
+                    Are[gi] = acr[mi][ni][e];
+                    Aim[gi] = aci[mi][ni][e];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ TMA-fed trailing GEMM
+// Same tile, warp layout and DMMA schedule as lu_gemm_kernel, for full 64-wide
+// panels: one thread issues cp.async.bulk.tensor loads of the L21 / U12 k-chunks
+// (both planes) into the double buffer and the CTA waits on an mbarrier with
+// the transaction byte count. The TMA boxes over-read 4 rows (A: 68 x 16) and
+// 4 k-rows (B: 20 x 64) so that the dense box lands in exactly the padded,
+// bank-conflict-free layouts of the cp.async kernel (strides 68 and 20).
+constexpr int kTmaABox0 = GAS, kTmaBBox0 = GBS;
+constexpr unsigned kTmaStageBytes = 2u * (GBK * GAS + GBN * GBS) * sizeof(double);
+constexpr size_t kTmaSmemPad = 128 + GSTAGES * sizeof(uint64_t);
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0),
+        "r"(c1), "r"(c2), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 2)
+lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* A,
+                   size_t mstride, size_t plane, int n, int ld, int k) {
+    // TMA destinations need 128 B alignment: round the dynamic base up (the
+    // launch requests kTmaSmemPad extra bytes); the mbarriers sit after the tiles
+    extern __shared__ double gsm_raw[];
+    const unsigned raw = static_cast<unsigned>(__cvta_generic_to_shared(gsm_raw));
+    double* gsm = gsm_raw + ((128u - (raw & 127u)) & 127u) / sizeof(double);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + kGemmSmemDoubles);
+    constexpr int w = 64, nk = w / GBK;
+    const int b = blockIdx.z;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int m0 = k + w + blockIdx.x * GBM;
+    const int n0 = k + w + blockIdx.y * GBN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % GWM, wn = warp / GWM;
+    auto As = [&](int st, int pl) { return gsm + (st * 2 + pl) * (GBK * GAS); };
+    auto Bs = [&](int st, int pl) { return gsm + GSTAGES * 2 * (GBK * GAS) + (st * 2 + pl) * (GBN * GBS); };
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < GSTAGES; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int st, int kc) {  // thread 0 only
+        mbar_expect_tx(&bar[st], kTmaStageBytes);
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl) {
+            tma_load_3d(As(st, pl), &tmA, &bar[st], m0, k + kc * GBK, 2 * b + pl);
+            tma_load_3d(Bs(st, pl), &tmB, &bar[st], k + kc * GBK, n0, 2 * b + pl);
+        }
+    };
+    if (tid == 0) issue(0, 0);
+    double acr[GMI][GNI][2], aci[GMI][GNI][2];
+#pragma unroll
+    for (int mi = 0; mi < GMI; ++mi) {
+        const int row = m0 + wm * (GBM / GWM) + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < GNI; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
+                const size_t gi = static_cast<size_t>(col) * ld + row;
+                acr[mi][ni][e] = Are[gi];
+                aci[mi][ni][e] = Aim[gi];
+            }
+    }
+#pragma unroll 1
+    for (int kc = 0; kc < nk; ++kc) {
+        if (tid == 0 && kc + 1 < nk) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of the slot
+            issue((kc + 1) % GSTAGES, kc + 1);
+        }
+        const int st = kc % GSTAGES;
+        mbar_wait(&bar[st], (kc / GSTAGES) & 1);
+        const double* ar = As(st, 0);
+        const double* ai = As(st, 1);
+        const double* br = Bs(st, 0);
+        const double* bi = Bs(st, 1);
+#pragma unroll
+        for (int k4 = 0; k4 < GBK; k4 += 4) {
+            double na_r[GMI], fa_i[GMI], na_i[GMI], fb_r[GNI], fb_i[GNI];
+            const int kr = k4 + (lane & 3);
+#pragma unroll
+            for (int mi = 0; mi < GMI; ++mi) {
+                const int m = wm * (GBM / GWM) + mi * 8 + (lane >> 2);
+                na_r[mi] = -ar[kr * GAS + m];
+                fa_i[mi] = ai[kr * GAS + m];
+                na_i[mi] = -fa_i[mi];
+            }
+#pragma unroll
+            for (int ni = 0; ni < GNI; ++ni) {
+                const int nn = wn * (GBN / GWN) + ni * 8 + (lane >> 2);
+                fb_r[ni] = br[nn * GBS + kr];
+                fb_i[ni] = bi[nn * GBS + kr];
+            }
+#pragma unroll
+            for (int mi = 0; mi < GMI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < GNI; ++ni) {
+                    dmma(acr[mi][ni][0], acr[mi][ni][1], na_r[mi], fb_r[ni]);
+                    dmma(aci[mi][ni][0], aci[mi][ni][1], na_r[mi], fb_i[ni]);
+                }
+#pragma unroll
+            for (int mi = 0; mi < GMI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < GNI; ++ni) {
+                    dmma(acr[mi][ni][0], acr[mi][ni][1], fa_i[mi], fb_i[ni]);
+                    dmma(aci[mi][ni][0], aci[mi][ni][1], na_i[mi], fb_r[ni]);
+                }
+        }
+        __syncthreads();
+    }
 #pragma unroll
     for (int mi = 0; mi < GMI; ++mi) {
         const int row = m0 + wm * (GBM / GWM) + mi * 8 + (lane >> 2);
@@ -1094,6 +1249,53 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
     profiler().end(st, te, kProfLuTrsm, 4.0 * w * w * rest * pb.batch);
 }
 
+// Tensor maps of a batch (rows x columns x planes, planes = 2 per matrix), cached
+// per (base pointer, ld, batch): the box of A (L21 chunk) and of B (U12 chunk).
+struct TmaMaps {
+    CUtensorMap a, b;
+};
+
+bool use_tma_gemm() {
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_GEMM");
+        return !(e && std::string(e) == "cpasync");
+    }();
+    return on;
+}
+
+const TmaMaps& tma_maps(const LuProblem& pb) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, size_t>, TmaMaps> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(static_cast<const void*>(pb.A), pb.ld, pb.batch, pb.plane);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        FDS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (pb.mstride != 2 * pb.plane) throw ValidationError("lu: TMA path needs re/im planes back to back");
+    TmaMaps m{};
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(pb.ld), static_cast<cuuint64_t>(pb.ld),
+                                static_cast<cuuint64_t>(2) * pb.batch};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pb.ld) * sizeof(double), pb.plane * sizeof(double)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint32_t boxa[3] = {static_cast<cuuint32_t>(kTmaABox0), GBK, 1};
+    const cuuint32_t boxb[3] = {static_cast<cuuint32_t>(kTmaBBox0), GBN, 1};
+    auto enc = [&](CUtensorMap* t, const cuuint32_t* box) {
+        const CUresult r = encode(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, pb.A, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    };
+    enc(&m.a, boxa);
+    enc(&m.b, boxb);
+    return cache.emplace(key, m).first->second;
+}
+
 void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
     const int rest = pb.n - k - w;
     if (rest <= 0) return;
@@ -1106,8 +1308,21 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
     dim3 gg(ceil_div(rest, GBM), ceil_div(rest, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
-    FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
-               pb.plane, pb.n, pb.ld, k, w);
+    if (w == 64 && use_tma_gemm()) {
+        static bool tset = false;
+        if (!tset) {
+            FDS_CUDA(cudaFuncSetAttribute(lu_gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kGemmSmemDoubles * sizeof(double) + kTmaSmemPad)));
+            tset = true;
+        }
+        const TmaMaps& tm = tma_maps(pb);
+        FDS_LAUNCH(lu_gemm_tma_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st, tm.a,
+                   tm.b, pb.A,
+                   pb.mstride, pb.plane, pb.n, pb.ld, k);
+    } else {
+        FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
+                   pb.plane, pb.n, pb.ld, k, w);
+    }
     // algorithmic flops of A22 -= L21 U12 (complex): 8 * rest^2 * w per matrix
     profiler().end(st, ge, kProfLuGemm, 8.0 * rest * rest * w * pb.batch);
 }
