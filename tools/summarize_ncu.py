@@ -54,7 +54,7 @@ if __name__ == "__main__":
                "kernels": f}, open(f"profiles/{tag}_lu_gemm_ncu_full.json", "w"), indent=1)
     g = f[0]
     traffic = (float(g["dram__bytes_read.sum"]) + float(g["dram__bytes_write.sum"])) * 1e9  # GB -> bytes
-    json.dump({"lu_gemm_kernel": {"bytes_per_launch": traffic, "launch": "31st lu_gemm launch (k = 30*64) of cfg2",
+    json.dump({"lu_gemm_tma_kernel": {"bytes_per_launch": traffic, "launch": "31st lu_gemm launch (k = 30*64) of cfg2",
                                   "gpu_time_ms": float(g["gpu__time_duration.sum"])}},
               open("profiles/ncu_traffic.json", "w"), indent=1)
     print(json.dumps(summ, indent=0)[:1500])
