@@ -1351,23 +1351,26 @@ bool use_calu() {
 // 16-wide sub-panels: for batches ~4x more matrices fit on chip at once
 // (cfg2 panel 225 -> 77 ms); for a single matrix the narrower rank-1 updates
 // still win (N=15360 panel 107 -> 97 ms). FDSWEEP_SUBPANEL=0/1 overrides.
-bool use_subpanels(const LuProblem& pb) {
+bool subpanels_enabled() {
     static const int env = [] {
         const char* e = std::getenv("FDSWEEP_SUBPANEL");
         return e ? std::atoi(e) : -1;
     }();
-    if (env >= 0) return env != 0;
-    return pb.batch >= 1;
+    return env != 0;
 }
+
+bool use_subpanels(const LuProblem&) { return subpanels_enabled(); }
 
 }  // namespace
 
 int lu_panel_width(int n) {
-    // NB = 64; the GEPP panel falls back to 32 when a 64-wide panel of one
-    // matrix cannot live in the SMs' shared memory.
+    // NB = 64; the panel must fit one matrix's rows in the SMs' shared memory:
+    // as 16-wide sub-panels (default) or as one 64-wide GEPP panel; otherwise 32.
     if (use_calu()) return 64;
     const int sms = device_info().sms;
-    return ceil_div(n, panel_rows_max<64>()) <= sms ? 64 : 32;
+    if (ceil_div(n, panel_rows_max<64>()) <= sms) return 64;
+    if (subpanels_enabled() && ceil_div(n, panel_rows_max<kSub>()) <= sms) return 64;
+    return 32;
 }
 
 namespace {
