@@ -308,13 +308,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 2)
-lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w) {
+lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int c0) {
     extern __shared__ __align__(16) double gsm[];
     const int b = blockIdx.z;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
     const int m0 = k + w + blockIdx.x * GBM;  // first row of this tile
-    const int n0 = k + w + blockIdx.y * GBN;  // first column
+    const int n0 = c0 + blockIdx.y * GBN;  // first column (c0 >= k + w)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp % GWM, wn = warp / GWM;
     auto As = [&](int st, int pl) { return gsm + (st * 2 + pl) * (GBK * GAS); };
@@ -466,7 +466,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 
 __global__ void __launch_bounds__(kGemmThreads, 2)
 lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* A,
-                   size_t mstride, size_t plane, int n, int ld, int k) {
+                   size_t mstride, size_t plane, int n, int ld, int k, int c0) {
     // TMA destinations need 128 B alignment: round the dynamic base up (the
     // launch requests kTmaSmemPad extra bytes); the mbarriers sit after the tiles
     extern __shared__ double gsm_raw[];
@@ -478,7 +478,7 @@ lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
     const int m0 = k + w + blockIdx.x * GBM;
-    const int n0 = k + w + blockIdx.y * GBN;
+    const int n0 = c0 + blockIdx.y * GBN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp % GWM, wn = warp / GWM;
     auto As = [&](int st, int pl) { return gsm + (st * 2 + pl) * (GBK * GAS); };
@@ -1296,16 +1296,20 @@ const TmaMaps& tma_maps(const LuProblem& pb) {
     return cache.emplace(key, m).first->second;
 }
 
-void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
+// A22[:, c0:c1) -= L21 U12[:, c0:c1) for the rows below the panel (c0 >= k + w).
+void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, int c1 = -1) {
     const int rest = pb.n - k - w;
     if (rest <= 0) return;
+    if (c0 < 0) c0 = k + w;
+    if (c1 < 0) c1 = pb.n;
+    if (c1 <= c0) return;
     static bool gset = false;
     if (!gset) {
         FDS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kGemmSmemDoubles * sizeof(double))));
         gset = true;
     }
-    dim3 gg(ceil_div(rest, GBM), ceil_div(rest, GBN), pb.batch);
+    dim3 gg(ceil_div(rest, GBM), ceil_div(c1 - c0, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
     if (w == 64 && use_tma_gemm()) {
@@ -1318,13 +1322,13 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st) {
         const TmaMaps& tm = tma_maps(pb);
         FDS_LAUNCH(lu_gemm_tma_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st, tm.a,
                    tm.b, pb.A,
-                   pb.mstride, pb.plane, pb.n, pb.ld, k);
+                   pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
     } else {
         FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
-                   pb.plane, pb.n, pb.ld, k, w);
+                   pb.plane, pb.n, pb.ld, k, w, c0);
     }
     // algorithmic flops of A22 -= L21 U12 (complex): 8 * rest^2 * w per matrix
-    profiler().end(st, ge, kProfLuGemm, 8.0 * rest * rest * w * pb.batch);
+    profiler().end(st, ge, kProfLuGemm, 8.0 * rest * (c1 - c0) * w * pb.batch);
 }
 
 template <int NB>
@@ -1451,12 +1455,68 @@ void lu_factor_pipelined(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) 
     FDS_CUDA(cudaStreamWaitEvent(st, ev_lo_end, 0));
 }
 
+int lookahead_mode() {
+    static const int env = [] {
+        const char* e = std::getenv("FDSWEEP_LOOKAHEAD");
+        return e ? std::atoi(e) : -1;
+    }();
+    return env;
+}
+
+bool use_lookahead(const LuProblem& pb) {
+    const int env = lookahead_mode();
+    if (env >= 0) return env != 0;
+    return pb.batch == 1;
+}
+
+// Look-ahead: the trailing update of step k is split into the next panel's
+// 64 columns and the rest; the next panel (16-wide sub-panels, plain launch on
+// a high-priority stream) factors while the rest of the GEMM runs, so the
+// latency-bound column steps hide behind the tensor-pipe work. The next
+// step's swap+TRSM waits for both (same stream order as the serial schedule).
+void lu_factor_lookahead(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
+    static cudaStream_t s_hi = nullptr;
+    static cudaEvent_t ev_a = nullptr, ev_p = nullptr;
+    if (!s_hi) {
+        int lo = 0, hi = 0;
+        FDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FDS_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, hi));
+        FDS_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
+        FDS_CUDA(cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming));
+    }
+    double* linv = ws.linv(pb.batch);
+    subpanel_block(pb, ws, 0, 64, st, true);
+    for (int k = 0; k < pb.n; k += 64) {
+        const int w = std::min(64, pb.n - k);
+        trsm_step<64>(pb, k, w, st, linv);
+        const int nx = k + w;
+        if (nx >= pb.n) break;
+        const int wn = std::min(64, pb.n - nx);
+        if (wn == 64) {
+            gemm_step(pb, k, w, st, nx, nx + 64);
+            FDS_CUDA(cudaEventRecord(ev_a, st));
+            FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_a, 0));
+            subpanel_block(pb, ws, nx, 64, s_hi, false);
+            FDS_CUDA(cudaEventRecord(ev_p, s_hi));
+            gemm_step(pb, k, w, st, nx + 64, pb.n);
+            FDS_CUDA(cudaStreamWaitEvent(st, ev_p, 0));
+        } else {
+            gemm_step(pb, k, w, st);
+            panel_step<64>(pb, ws, nx, wn, st);
+        }
+    }
+}
+
 }  // namespace
 
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     FDS_CUDA(cudaMemsetAsync(pb.info, 0, pb.batch * sizeof(int), st));
     if (!use_calu() && lu_panel_width(pb.n) == 64 && use_pipeline(pb)) {
         lu_factor_pipelined(pb, ws, st);
+        return;
+    }
+    if (!use_calu() && lu_panel_width(pb.n) == 64 && subpanels_enabled() && pb.n >= 128 && use_lookahead(pb)) {
+        lu_factor_lookahead(pb, ws, st);
         return;
     }
     const int nb = lu_panel_width(pb.n);
