@@ -1466,7 +1466,10 @@ int lookahead_mode() {
 bool use_lookahead(const LuProblem& pb) {
     const int env = lookahead_mode();
     if (env >= 0) return env != 0;
-    return pb.batch == 1;
+    // measured: single N = 15360 399 -> 368 ms; N = 36864 4.33 -> 4.45 s (the
+    // panel share is small there and the co-running panel costs GEMM slots);
+    // batched N = 3840 x 129 697 -> 731 ms
+    return pb.batch == 1 && pb.n <= 24576;
 }
 
 // Look-ahead: the trailing update of step k is split into the next panel's
