@@ -1,0 +1,31 @@
+// "bem" systems of the fdsweep_b200 CLI on the B200 library: one device
+// handle per system (fds_bem_create), contour batches through
+// fds_bem_evaluate_batch (batched assembly + LU + solve).
+#include "cli_bem.hpp"
+#include "fdsweep_b200_shim.hpp"
+
+namespace fdsweep::cli {
+
+std::unique_ptr<FrequencySystem> make_bem_system(const BemSpec& spec) {
+    b200::BemMesh m;
+    m.vertices = spec.vertices;
+    m.triangles = spec.triangles;
+    m.shear_modulus = spec.shear_modulus;
+    m.poisson_ratio = spec.poisson_ratio;
+    m.density = spec.density;
+    m.traction = spec.traction;
+    m.channels = spec.channels;
+    return std::make_unique<b200::BemSystem>(m);
+}
+
+std::vector<std::vector<Complex>> evaluate_many(const FrequencySystem& system, std::span<const Complex> s) {
+    if (const auto* bem = dynamic_cast<const b200::BemSystem*>(&system)) return bem->evaluate_batch(s);
+    std::vector<std::vector<Complex>> out;
+    out.reserve(s.size());
+    for (const Complex z : s) out.push_back(system.evaluate(z));
+    return out;
+}
+
+const char* solver_name() { return "b200"; }
+
+}  // namespace fdsweep::cli
