@@ -79,6 +79,7 @@ class BemSystem : public FrequencySystem {
         check(fds_bem_evaluate(h_.get(), fds_c64{s.real(), s.imag()}, c(out.data())));
         return out;
     }
+    fds_bem* handle() const { return h_.get(); }
     // B independent solves in one batched assembly + LU (e.g. the FSM contour).
     std::vector<std::vector<Complex>> evaluate_batch(std::span<const Complex> s) const {
         std::vector<Complex> flat(s.size() * desc_.channel_count);
@@ -96,6 +97,70 @@ class BemSystem : public FrequencySystem {
     std::unique_ptr<fds_bem, Del> h_;
     SystemDescriptor desc_;
 };
+
+// run_afs (afs.cpp:226-396) of a BemSystem on the library's own driver: the J0
+// initial frequencies are one batched solve and the fits stay on the device.
+// Same AfsResult as the reference driver (identical sampled frequencies; see
+// tests/test_gpu_vf.py and tests/test_cli.py).
+inline AfsResult run_afs_bem(const BemSystem& sys, const AfsConfig& cfg) {
+    const int K = sys.descriptor().channel_count;
+    fds_afs_config a{};
+    a.initial_count = cfg.initial_count;
+    a.alpha_high = cfg.alpha_high;
+    a.alpha_low = cfg.alpha_low;
+    a.e1_threshold = cfg.e1_threshold;
+    a.e2_threshold = cfg.e2_threshold;
+    a.validation_steps = cfg.validation_steps;
+    a.n_orf = static_cast<int>(cfg.orf_indices.size());
+    a.orf_indices = cfg.orf_indices.data();
+    a.n_test = static_cast<int>(cfg.test_indices.size());
+    a.test_indices = cfg.test_indices.data();
+    a.omega_max = cfg.omega_max;
+    a.eta = cfg.eta;
+    a.period = cfg.period;
+    a.grid_points = cfg.grid_points;
+    a.time_points = cfg.time_points;
+    a.max_iterations = cfg.max_iterations;
+    a.seed = cfg.seed;
+    a.n_relocations = cfg.n_relocations;
+    const int cap = cfg.initial_count + cfg.max_iterations + cfg.validation_steps + 16;
+    std::vector<Complex> s(cap), vals(static_cast<size_t>(cap) * K), poles(cap), res(static_cast<size_t>(cap) * K);
+    std::vector<double> hist(static_cast<size_t>(cap) * 8);
+    fds_afs_summary sm{};
+    check(fds_run_afs_bem(sys.handle(), &a, cap, c(s.data()), c(vals.data()), hist.data(), c(poles.data()),
+                          c(res.data()), &sm));
+    AfsResult r;
+    r.n_c = sm.n_c;
+    r.converged = sm.converged != 0;
+    r.solver_calls = sm.solver_calls;
+    r.seed = cfg.seed;
+    for (int j = 0; j < sm.n_c; ++j)
+        r.samples.push_back(FrequencySample{s[j], std::vector<Complex>(vals.begin() + static_cast<size_t>(j) * K,
+                                                                       vals.begin() + static_cast<size_t>(j + 1) * K)});
+    const int M = sm.order;
+    r.model_high.poles.assign(poles.begin(), poles.begin() + M);
+    for (int k = 0; k < K; ++k)
+        r.model_high.residues.emplace_back(res.begin() + static_cast<size_t>(k) * M,
+                                           res.begin() + static_cast<size_t>(k + 1) * M);
+    r.model_high.channel_labels = sys.descriptor().channel_labels;
+    for (int i = 0; i < sm.n_history; ++i) {
+        const double* h = &hist[8 * static_cast<size_t>(i)];
+        AfsIteration it;
+        it.sample_count = static_cast<int>(h[0]);
+        it.order_high = static_cast<int>(h[1]);
+        it.order_low = static_cast<int>(h[2]);
+        if (h[3] != 0.0) it.s_new = Complex(h[4], h[5]);
+        it.e1 = h[6];
+        it.e2 = h[7];
+        r.history.push_back(it);
+    }
+    r.orf_indices = cfg.orf_indices;
+    if (cfg.test_indices.empty())
+        for (int k = 0; k < K; ++k) r.test_indices.push_back(k);
+    else
+        r.test_indices = cfg.test_indices;
+    return r;
+}
 
 inline std::vector<Complex> relocate_poles(std::span<const FrequencySample> samples,
                                            std::span<const Complex> poles, RelocationStats* stats = nullptr) {

@@ -17,11 +17,13 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <optional>
 #include <span>
 #include <string>
 #include <tuple>
 #include <vector>
 
+#include "fdsweep/afs.hpp"
 #include "fdsweep/systems.hpp"
 #include "fdsweep/types.hpp"
 
@@ -42,6 +44,28 @@ std::unique_ptr<FrequencySystem> make_bem_system(const BemSpec& spec);
 std::vector<std::vector<Complex>> evaluate_many(const FrequencySystem& system, std::span<const Complex> s);
 // "b200" or "cpu-oracle": which solver this binary links.
 const char* solver_name();
+// The linked library's own AFS driver for its BEM systems (GPU build: J0
+// batched, fits on the device); empty => the caller runs the reference run_afs.
+std::optional<AfsResult> run_afs_native(const FrequencySystem& system, const AfsConfig& cfg);
+
+// ORF draw of afs.cpp:28-46 (sorted partial Fisher–Yates, xorshift64 without the
+// zero-state guard), so explicit and drawn ORF sets are interchangeable.
+inline std::vector<int> draw_indices(int n, int k, std::uint64_t seed) {
+    std::vector<int> pool(n);
+    for (int i = 0; i < n; ++i) pool[i] = i;
+    std::uint64_t state = seed ^ 0x9e3779b97f4a7c15ULL;
+    std::vector<int> out;
+    for (int i = 0; i < k; ++i) {
+        state ^= state << 13;
+        state ^= state >> 7;
+        state ^= state << 17;
+        const int j = i + static_cast<int>(state % (pool.size() - i));
+        std::swap(pool[i], pool[j]);
+        out.push_back(pool[i]);
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+}
 
 // ---------------------------------------------------------------- generators
 // xorshift64 of proj/src/afs.cpp:31-37 (state = seed ^ 0x9e3779b97f4a7c15).

@@ -28,4 +28,9 @@ std::vector<std::vector<Complex>> evaluate_many(const FrequencySystem& system, s
 
 const char* solver_name() { return "b200"; }
 
+std::optional<AfsResult> run_afs_native(const FrequencySystem& system, const AfsConfig& cfg) {
+    if (const auto* bem = dynamic_cast<const b200::BemSystem*>(&system)) return b200::run_afs_bem(*bem, cfg);
+    return std::nullopt;
+}
+
 }  // namespace fdsweep::cli

@@ -225,13 +225,12 @@ int cmd_sweep_afs(const Args& a) {
     }
     const FsmGrid grid(cfg.period, ns);
 
+    // explicit ORF set (afs.cpp:234-238 draws the same one from the seed)
+    const int K = sys->descriptor().channel_count;
+    if (cfg.orf_indices.empty()) cfg.orf_indices = cli::draw_indices(K, std::min(5, K), cfg.seed);
     Outputs o{a.out};
-    AfsResult r;
-    try {
-        r = run_afs(*sys, cfg);
-    } catch (const ConvergenceError&) {
-        throw;
-    }
+    std::optional<AfsResult> native = cli::run_afs_native(*sys, cfg);
+    const AfsResult r = native ? std::move(*native) : run_afs(*sys, cfg);
     const auto& labels = sys->descriptor().channel_labels;
     const TimeSeries ts = rational_invert(r.model_high, grid.time_grid());
     o.put("spectrum.csv", spectrum_csv(r.samples, labels));

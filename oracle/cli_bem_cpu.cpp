@@ -68,4 +68,6 @@ std::vector<std::vector<Complex>> evaluate_many(const FrequencySystem& system, s
 
 const char* solver_name() { return "cpu-oracle"; }
 
+std::optional<AfsResult> run_afs_native(const FrequencySystem&, const AfsConfig&) { return std::nullopt; }
+
 }  // namespace fdsweep::cli

@@ -2,7 +2,8 @@
 (integration/_build/fdsweep_b200, B200) against the same main linked with the
 CPU oracle (oracle/_ref/fdsweep_oracle_cli, OpenMP assembly + OpenBLAS zgetrf
 on every host core), on the config-2 FSM sweep (1280-triangle sphere, 129
-contour frequencies, 16 collocation points) and a config-1 AFS sweep.
+contour frequencies, 16 collocation points) and an AFS sweep on the config-2 mesh (random traction, 16 points, J0 = 12,
+J_c = 6, thresholds off so both builds take the same 18 samples).
 Writes profiles/r01_cli_timing.json."""
 import json, os, subprocess, sys, tempfile, time
 from pathlib import Path
@@ -37,9 +38,9 @@ def main():
         rg = json.loads((d / "g" / "report.json").read_text())
         out["sweep_fsm_cfg2"] = {"n_c": rg["n_c"], "gpu_wall_s": g, "gpu_system_s": rg["system_s"], "gpu_solve_s": rg["solve_s"], "cpu_wall_s": c, "speedup": c / g,
                                  "gpu_solves_per_s": rg["n_c"] / g, "cpu_solves_per_s": rg["n_c"] / c}
-        (d / "cfg1.json").write_text(json.dumps({"type": "bem", "mesh": {"kind": "icosphere", "level": 2},
+        (d / "cfg1.json").write_text(json.dumps({"type": "bem", "mesh": {"kind": "icosphere", "level": 3},
                                                  "load": {"kind": "random", "seed": 0},
-                                                 "collocation_points": [3, 40, 77, 150, 222, 301]}))
+                                                 "collocation_points": list(range(0, 1280, 80))}))
         (d / "afs.json").write_text(json.dumps({"omega_max": 3.141592653589793 * 256 / 20.0, "eta": 0.25,
                                                 "period": 20.0, "initial_count": 12, "validation_steps": 6,
                                                 "e1_threshold": "inf", "e2_threshold": "inf", "samples": 256}))
@@ -48,7 +49,7 @@ def main():
         c = run(CPU, args + ["--out", str(d / "ca")], env)
         ra = json.loads((d / "ga" / "report.json").read_text())
         rc = json.loads((d / "ca" / "report.json").read_text())
-        out["sweep_afs_cfg1"] = {"n_c": ra["n_c"], "gpu_wall_s": g, "cpu_wall_s": c, "speedup": c / g,
+        out["sweep_afs_cfg2_mesh"] = {"n_c": ra["n_c"], "gpu_wall_s": g, "cpu_wall_s": c, "speedup": c / g,
                                  "identical_frequencies": ra["frequencies"] == rc["frequencies"]}
     (ROOT / "profiles" / "r01_cli_timing.json").write_text(json.dumps(out, indent=1))
     print(json.dumps(out))
