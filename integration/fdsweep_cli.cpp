@@ -21,6 +21,8 @@
 //               "order": M (req), "n_relocations": 3
 //   invert:    {"model": path (req), "period": T, "samples": N_s} or "t": [...]
 //   compare:   {"fsm": dir (req), "afs": dir (req)}
+// sweep-afs also takes --resume <archive.json> (reuse its samples) and
+// --checkpoint (rewrite <out>/archive.json after every new sample).
 // Exit codes: 0 ok; 2 usage; 3 ValidationError; 4 NumericError; 5 IoError;
 // 6 ConvergenceError or an AFS run that did not converge; 7 other errors.
 #include <algorithm>
@@ -28,6 +30,7 @@
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
+#include <functional>
 #include <map>
 #include <sstream>
 #include <string>
@@ -49,7 +52,8 @@ using namespace fdsweep;
 namespace {
 
 struct Args {
-    std::string command, system, config, out;
+    std::string command, system, config, out, resume;
+    bool checkpoint = false;
     std::optional<std::uint64_t> seed;
     std::optional<std::vector<int>> orf, test;
 };
@@ -229,8 +233,34 @@ int cmd_sweep_afs(const Args& a) {
     const int K = sys->descriptor().channel_count;
     if (cfg.orf_indices.empty()) cfg.orf_indices = cli::draw_indices(K, std::min(5, K), cfg.seed);
     Outputs o{a.out};
-    std::optional<AfsResult> native = cli::run_afs_native(*sys, cfg);
-    const AfsResult r = native ? std::move(*native) : run_afs(*sys, cfg);
+    // --resume: samples of an earlier (interrupted) run are reused, never re-solved
+    // (afs.cpp:281-302); --checkpoint: the archive is rewritten after every new
+    // sample, so an interrupted run can be resumed.
+    std::vector<FrequencySample> resume;
+    if (!a.resume.empty()) resume = load_archive(a.resume).samples;
+    std::vector<FrequencySample> done = resume;
+    std::function<void(const FrequencySample&)> on_sample;
+    if (a.checkpoint)
+        on_sample = [&](const FrequencySample& smp) {
+            done.push_back(smp);
+            SweepArchive ar;
+            ar.config = cfg;
+            ar.samples = done;
+            save_archive(ar, o.dir / "archive.json");
+        };
+    std::optional<AfsResult> native;
+    if (resume.empty() && !a.checkpoint) native = cli::run_afs_native(*sys, cfg);
+    AfsResult r;
+    if (native) {
+        r = std::move(*native);
+    } else {
+        try {
+            r = run_afs(*sys, cfg, resume, on_sample);
+        } catch (const ConvergenceError&) {  // budget exhausted: the checkpoint archive is the partial result
+            if (a.checkpoint) std::fprintf(stderr, "fdsweep_b200: partial archive in %s\n", (o.dir / "archive.json").c_str());
+            throw;
+        }
+    }
     const auto& labels = sys->descriptor().channel_labels;
     const TimeSeries ts = rational_invert(r.model_high, grid.time_grid());
     o.put("spectrum.csv", spectrum_csv(r.samples, labels));
@@ -346,7 +376,7 @@ int cmd_compare(const Args& a) {
 void usage() {
     std::fprintf(stderr,
                  "usage: fdsweep_b200 {sweep-fsm|sweep-afs|fit|invert|compare} [--system s.json] --config c.json "
-                 "--out dir [--seed n] [--orf i,j,..] [--test i,j,..]\n");
+                 "--out dir [--seed n] [--orf i,j,..] [--test i,j,..] [--resume archive.json] [--checkpoint]\n");
 }
 
 }  // namespace
@@ -371,6 +401,8 @@ int main(int argc, char** argv) {
             else if (f == "--seed") a.seed = std::stoull(val());
             else if (f == "--orf") a.orf = parse_list(val());
             else if (f == "--test") a.test = parse_list(val());
+            else if (f == "--resume") a.resume = val();
+            else if (f == "--checkpoint") a.checkpoint = true;
             else {
                 usage();
                 return 2;

@@ -234,3 +234,38 @@ def test_gpu_cli_fit_poles_match_oracle(tmp_path, modal):
     pc = np.array([complex(*p) for p in json.loads((c / "model.json").read_text())["poles"]])
     for p in pc:
         assert np.min(np.abs(pg - p)) / abs(p) < 1e-6
+
+
+def _resume_roundtrip(cli, tmp_path, sysj, cfg_full, cfg_short):
+    full, part, res = tmp_path / "full", tmp_path / "part", tmp_path / "res"
+    r = run(cli, "sweep-afs", "--system", sysj, "--config", cfg_full, "--out", full, timeout=1800)
+    assert r.returncode == 0, r.stderr
+    r = run(cli, "sweep-afs", "--system", sysj, "--config", cfg_short, "--out", part, "--checkpoint", timeout=1800)
+    assert r.returncode == 6, (r.returncode, r.stderr)  # ConvergenceError: iteration budget exhausted
+    arch = json.loads((part / "archive.json").read_text())
+    r = run(cli, "sweep-afs", "--system", sysj, "--config", cfg_full, "--out", res, "--resume",
+            part / "archive.json", timeout=1800)
+    assert r.returncode == 0, r.stderr
+    jf, jr = json.loads((full / "report.json").read_text()), json.loads((res / "report.json").read_text())
+    assert jr["frequencies"] == jf["frequencies"] and jr["n_c"] == jf["n_c"]
+    assert jr["solver_calls"] == jf["n_c"] - len(arch["samples"])  # resumed samples are never re-solved
+    return jf
+
+
+def test_sweep_afs_resume_equivalence(tmp_path, modal):
+    """SPEC.md io invariant: interrupted + archived + resumed == uninterrupted."""
+    full = dict(AFS_MODAL)
+    short = dict(AFS_MODAL, max_iterations=3)
+    _resume_roundtrip(CPU_CLI, tmp_path, modal, write(tmp_path / "f.json", full), write(tmp_path / "s.json", short))
+
+
+@pytest.mark.gpu
+def test_gpu_cli_bem_resume_equivalence(tmp_path):
+    sysj = write(tmp_path / "bem.json", {"type": "bem", "mesh": {"kind": "icosphere", "level": 2},
+                                         "load": {"kind": "random", "seed": 0},
+                                         "collocation_points": [3, 40, 77, 150, 222, 301]})
+    base = {"omega_max": math.pi * 256 / 20.0, "eta": 0.25, "period": 20.0, "initial_count": 10,
+            "validation_steps": 4, "e1_threshold": "inf", "e2_threshold": "inf", "samples": 256}
+    jf = _resume_roundtrip(GPU_CLI, tmp_path, sysj, write(tmp_path / "f.json", base),
+                           write(tmp_path / "s.json", dict(base, max_iterations=2)))
+    assert jf["n_c"] == 14
