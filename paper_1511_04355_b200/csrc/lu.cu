@@ -730,8 +730,9 @@ lu_l11_inverse_kernel(const double* A, size_t mstride, size_t plane, int n, int 
 }
 
 constexpr int SAS = 68;  // padded smem stride (≡ 4 mod 16 doubles)
+constexpr int kApplyThreads = 256;
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kApplyThreads)
 lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv) {
     extern __shared__ __align__(16) double ssm[];
     double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
@@ -801,27 +802,29 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
     }
     // panel rows permuted in place through registers
     {
-        double pr[32], pi[32];
+        constexpr int kPer = 64 * 64 / kApplyThreads;
+        double pr[kPer], pi[kPer];
 #pragma unroll
-        for (int p = 0; p < 32; ++p) {
-            const int q = tid + 128 * p, nn = q / 64, kk = q % 64;
+        for (int p = 0; p < kPer; ++p) {
+            const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
             vget(nn, map.psrc[kk], pr[p], pi[p]);
         }
         __syncthreads();
 #pragma unroll
-        for (int p = 0; p < 32; ++p) {
-            const int q = tid + 128 * p, nn = q / 64, kk = q % 64;
+        for (int p = 0; p < kPer; ++p) {
+            const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
             Xr[nn * SAS + kk] = pr[p];
             Xi[nn * SAS + kk] = pi[p];
         }
     }
     __syncthreads();
+    // 8 warps: 2 (rows of 32) x 4 (columns of 16)
     const int wm = warp & 1, wn = warp >> 1;
-    double acr[4][4][2] = {}, aci[4][4][2] = {};
+    double acr[4][2][2] = {}, aci[4][2][2] = {};
 #pragma unroll 4
     for (int k4 = 0; k4 < 64; k4 += 4) {
         const int kr = k4 + (lane & 3);
-        double ar[4], ai[4], an[4], br[4], bi[4];
+        double ar[4], ai[4], an[4], br[2], bi[2];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
             const int m = wm * 32 + mi * 8 + (lane >> 2);
@@ -830,22 +833,22 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
             an[mi] = -ai[mi];
         }
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            const int nn = wn * 32 + ni * 8 + (lane >> 2);
+        for (int ni = 0; ni < 2; ++ni) {
+            const int nn = wn * 16 + ni * 8 + (lane >> 2);
             br[ni] = Xr[nn * SAS + kr];
             bi[ni] = Xi[nn * SAS + kr];
         }
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
+            for (int ni = 0; ni < 2; ++ni) {
                 dmma(acr[mi][ni][0], acr[mi][ni][1], ar[mi], br[ni]);
                 dmma(aci[mi][ni][0], aci[mi][ni][1], ar[mi], bi[ni]);
             }
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
+            for (int ni = 0; ni < 2; ++ni) {
                 dmma(acr[mi][ni][0], acr[mi][ni][1], an[mi], bi[ni]);
                 dmma(aci[mi][ni][0], aci[mi][ni][1], ai[mi], br[ni]);
             }
@@ -854,10 +857,10 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
     for (int mi = 0; mi < 4; ++mi) {
         const int row = k + wm * 32 + mi * 8 + (lane >> 2);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int cl = wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+                const int cl = wn * 16 + ni * 8 + 2 * (lane & 3) + e;
                 if (cl < ncols) {
                     const size_t gi = static_cast<size_t>(col0 + cl) * ld + row;
                     Are[gi] = acr[mi][ni][e];
@@ -1239,7 +1242,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
         }
         FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, kInvThreads, ismem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
                    pb.ipiv, linv);
-        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, 64), pb.batch), 128, asmem, st, pb.A, pb.mstride,
+        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, 64), pb.batch), kApplyThreads, asmem, st, pb.A, pb.mstride,
                    pb.plane, pb.n, pb.ld, k, linv);
     } else {
         dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
