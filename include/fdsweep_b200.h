@@ -94,6 +94,15 @@ int fds_bem_assemble_host(fds_bem* bem, fds_c64 s, fds_c64* A, fds_c64* b);
 int fds_bem_last_timing(const fds_bem* bem, double* assembly_ms, double* lu_ms, double* solve_ms,
                         int* launches);
 
+/* Solver of subsequent evaluate calls: kind 0 = batched LU with partial
+ * pivoting (default); kind 1 = restarted GMRES per frequency on the assembled
+ * dense A (right block-Jacobi on the 3x3 element blocks), stopping at
+ * ||b - A u|| <= tol ||b|| (FDS_ECONVERGENCE if max_iter is reached first).
+ * For large N one O(N^2) product per iteration beats the O(N^3) factorization. */
+int fds_bem_set_solver(fds_bem* bem, int kind, double tol, int restart, int max_iter);
+/* Largest GMRES iteration count and true relative residual of the last evaluate. */
+int fds_bem_last_gmres(const fds_bem* bem, int* iterations, double* rel_residual);
+
 /* Dense complex LU + solve on the device for caller-provided host matrices
  * (column-major, B matrices of order n): x[b] = A[b]^{-1} rhs[b]. */
 int fds_zgesv_batch(int n, int B, const fds_c64* A, const fds_c64* rhs, fds_c64* x);

@@ -9,6 +9,7 @@
 
 #include "bem.cuh"
 #include "capi_util.h"
+#include "gmres.cuh"
 #include "lu.cuh"
 
 namespace fdsb {
@@ -83,6 +84,12 @@ struct fds_bem {
     cplx* svec = nullptr;
     cplx* out = nullptr;
     LuWorkspace ws;
+    // solver: 0 = batched LU (default), 1 = restarted GMRES per frequency
+    int solver = 0;
+    GmresParams gp;
+    GmresWorkspace gws;
+    int gm_iters = 0;
+    double gm_resid = 0.0;
     cudaEvent_t ev[4] = {};
     double t_asm = 0, t_lu = 0, t_solve = 0;
     int launches = 0;
@@ -134,9 +141,22 @@ struct fds_bem {
         pb.batch = B;
         pb.ipiv = ipiv;
         pb.info = info;
-        lu_factor(pb, ws, st);
-        FDS_CUDA(cudaEventRecord(ev[2], st));
-        lu_solve(pb, rhs, ld, st);
+        if (solver == 1) {
+            FDS_CUDA(cudaMemsetAsync(info, 0, B * sizeof(int), st));
+            gm_iters = 0;
+            gm_resid = 0.0;
+            for (int b = 0; b < B; ++b) {
+                const double* Ab = A + static_cast<size_t>(b) * mstride;
+                const GmresStats gs = gmres_solve(Ab, Ab + plane, n, ld, rhs + static_cast<size_t>(b) * ld, gp, gws, st);
+                gm_iters = std::max(gm_iters, gs.iterations);
+                gm_resid = std::max(gm_resid, gs.rel_residual);
+            }
+            FDS_CUDA(cudaEventRecord(ev[2], st));
+        } else {
+            lu_factor(pb, ws, st);
+            FDS_CUDA(cudaEventRecord(ev[2], st));
+            lu_solve(pb, rhs, ld, st);
+        }
         FDS_LAUNCH(gather_channels_kernel, ceil_div(K * B, 256), 256, 0, st, rhs, static_cast<size_t>(ld),
                    chan, K, B, out);
         FDS_CUDA(cudaEventRecord(ev[3], st));
@@ -342,6 +362,30 @@ int fds_bem_last_timing(const fds_bem* h, double* a, double* l, double* s, int* 
     if (s) *s = h->t_solve;
     if (launches) *launches = h->launches;
     return FDS_OK;
+}
+
+int fds_bem_set_solver(fds_bem* h, int kind, double tol, int restart, int max_iter) {
+    return fds_guard([&] {
+        if (!h) throw ValidationError("fds_bem_set_solver: null handle");
+        if (kind != 0 && kind != 1) throw ValidationError("fds_bem_set_solver: kind must be 0 (LU) or 1 (GMRES)");
+        if (kind == 1 && (!(tol > 0.0) || restart < 1 || max_iter < 1))
+            throw ValidationError("fds_bem_set_solver: GMRES needs tol > 0, restart >= 1, max_iter >= 1");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->solver = kind;
+        if (kind == 1) {
+            h->gp.tol = tol;
+            h->gp.restart = restart;
+            h->gp.max_iter = max_iter;
+        }
+    });
+}
+
+int fds_bem_last_gmres(const fds_bem* h, int* iterations, double* rel_residual) {
+    return fds_guard([&] {
+        if (!h) throw ValidationError("fds_bem_last_gmres: null handle");
+        if (iterations) *iterations = h->gm_iters;
+        if (rel_residual) *rel_residual = h->gm_resid;
+    });
 }
 
 // ------------------------------------------------------------------ batched zgesv
