@@ -2,11 +2,12 @@
 //
 //   gm_pinv_kernel       3x3 complex diagonal-block inverses (one per element):
 //                        the block-Jacobi preconditioner M^{-1}.
-//   gm_matvec_kernel     y = A x, planar column-major A: each CTA owns 256 rows
-//                        x a 1024-column chunk (x chunk staged in smem, 8-column
-//                        unroll so every thread keeps 16 coalesced loads in
-//                        flight); partial sums reduced over chunks in a fixed
-//                        order (gm_chunk_reduce_kernel). HBM-bound: 16 n² bytes.
+//   gm_matvec_kernel     y = A x, planar column-major A: each CTA owns 512 rows
+//                        (two per thread, 16-byte loads) x a 1024-column chunk
+//                        (x chunk staged in smem, 8-column unroll so every thread
+//                        keeps 16 coalesced 16-byte loads in flight); partial
+//                        sums reduced over chunks in a fixed order
+//                        (gm_chunk_reduce_kernel). HBM-bound: 16 n² bytes.
 //   gm_dots_kernel       h_i = <V_i, w> for all Krylov vectors at once (fixed
 //                        block partition + tree, so reductions are reproducible).
 //   gm_axpy_kernel       w -= V h / x += V y style updates, thread per row.
@@ -24,7 +25,7 @@ namespace fdsb {
 
 namespace {
 
-constexpr int kMvRows = 256, kMvCols = 1024, kDotThreads = 256, kDotRows = 2048;
+constexpr int kMvThreads = 256, kMvRows = 2 * kMvThreads, kMvCols = 1024, kDotThreads = 256, kDotRows = 2048;
 
 __global__ void gm_pinv_kernel(const double* __restrict__ Are, const double* __restrict__ Aim, int ne, int ld,
                                cplx* __restrict__ pinv) {
@@ -74,40 +75,49 @@ __global__ void gm_precond_kernel(const cplx* __restrict__ pinv, const cplx* __r
     for (int i = 0; i < 3; ++i) z[3 * e + i] = P[3 * i] * x0 + P[3 * i + 1] * x1 + P[3 * i + 2] * x2;
 }
 
-__global__ void __launch_bounds__(kMvRows)
+// Each thread owns two adjacent rows (16-byte loads), so a warp streams 512
+// contiguous bytes of a column per plane and a CTA 4 KB.
+__global__ void __launch_bounds__(kMvThreads)
 gm_matvec_kernel(const double* __restrict__ Are, const double* __restrict__ Aim, int n, int ld,
                  const cplx* __restrict__ x, cplx* __restrict__ partial) {
     __shared__ cplx xs[kMvCols];
     const int c0 = blockIdx.y * kMvCols, cn = min(kMvCols, n - c0);
-    for (int q = threadIdx.x; q < cn; q += kMvRows) xs[q] = x[c0 + q];
+    for (int q = threadIdx.x; q < cn; q += kMvThreads) xs[q] = x[c0 + q];
     __syncthreads();
-    const int r = blockIdx.x * kMvRows + threadIdx.x;
+    const int r = blockIdx.x * kMvRows + 2 * threadIdx.x;  // rows r, r+1 (ld is even, A is 16 B aligned)
     if (r >= n) return;
     const double* pr = Are + static_cast<size_t>(c0) * ld + r;
     const double* pi = Aim + static_cast<size_t>(c0) * ld + r;
-    double sr = 0.0, si = 0.0;
+    double s0r = 0.0, s0i = 0.0, s1r = 0.0, s1i = 0.0;
     int c = 0;
     for (; c + 8 <= cn; c += 8) {
-        double ar[8], ai[8];
+        double2 ar[8], ai[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            ar[u] = __ldcs(pr + static_cast<size_t>(c + u) * ld);
-            ai[u] = __ldcs(pi + static_cast<size_t>(c + u) * ld);
+            ar[u] = __ldcs(reinterpret_cast<const double2*>(pr + static_cast<size_t>(c + u) * ld));
+            ai[u] = __ldcs(reinterpret_cast<const double2*>(pi + static_cast<size_t>(c + u) * ld));
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const cplx v = xs[c + u];
-            sr += ar[u] * v.re - ai[u] * v.im;
-            si += ar[u] * v.im + ai[u] * v.re;
+            s0r += ar[u].x * v.re - ai[u].x * v.im;
+            s0i += ar[u].x * v.im + ai[u].x * v.re;
+            s1r += ar[u].y * v.re - ai[u].y * v.im;
+            s1i += ar[u].y * v.im + ai[u].y * v.re;
         }
     }
     for (; c < cn; ++c) {
-        const double ar = pr[static_cast<size_t>(c) * ld], ai = pi[static_cast<size_t>(c) * ld];
+        const double2 ar = *reinterpret_cast<const double2*>(pr + static_cast<size_t>(c) * ld);
+        const double2 ai = *reinterpret_cast<const double2*>(pi + static_cast<size_t>(c) * ld);
         const cplx v = xs[c];
-        sr += ar * v.re - ai * v.im;
-        si += ar * v.im + ai * v.re;
+        s0r += ar.x * v.re - ai.x * v.im;
+        s0i += ar.x * v.im + ai.x * v.re;
+        s1r += ar.y * v.re - ai.y * v.im;
+        s1i += ar.y * v.im + ai.y * v.re;
     }
-    partial[static_cast<size_t>(blockIdx.y) * n + r] = mk(sr, si);
+    cplx* out = partial + static_cast<size_t>(blockIdx.y) * n;
+    out[r] = mk(s0r, s0i);
+    if (r + 1 < n) out[r + 1] = mk(s1r, s1i);
 }
 
 // y = sum over chunks of partial (fixed order); optionally y = b - y.
@@ -176,7 +186,7 @@ struct Ops {
     // y = A x  (or y = b - A x)
     void matvec(const cplx* x, cplx* y, const cplx* b = nullptr) const {
         dim3 g(ceil_div(n, kMvRows), nchunk());
-        FDS_LAUNCH(gm_matvec_kernel, g, kMvRows, 0, st, Are, Aim, n, ld, x, partial());
+        FDS_LAUNCH(gm_matvec_kernel, g, kMvThreads, 0, st, Are, Aim, n, ld, x, partial());
         FDS_LAUNCH(gm_chunk_reduce_kernel, ceil_div(n, 256), 256, 0, st, partial(), nchunk(), n, b, y);
     }
     void precond(const cplx* x, cplx* z) const {
