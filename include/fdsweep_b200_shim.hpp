@@ -80,6 +80,10 @@ class BemSystem : public FrequencySystem {
         return out;
     }
     fds_bem* handle() const { return h_.get(); }
+    // Solver of later evaluations: LU (default) or GMRES (fds_bem_set_solver).
+    void set_solver(bool gmres, double tol = 1e-12, int restart = 60, int max_iter = 1000) {
+        check(fds_bem_set_solver(h_.get(), gmres ? 1 : 0, tol, restart, max_iter));
+    }
     // B independent solves in one batched assembly + LU (e.g. the FSM contour).
     std::vector<std::vector<Complex>> evaluate_batch(std::span<const Complex> s) const {
         std::vector<Complex> flat(s.size() * desc_.channel_count);

@@ -36,6 +36,10 @@ struct BemSpec {
     std::vector<double> traction;  // [ne][3], times the Heaviside factor 1/s
     std::vector<int> channels;     // output DOFs u[3e+i]; empty => all
     int max_batch = 0;             // 0 => library default
+    // "solver": {"kind": "lu" | "gmres", "tol": 1e-12, "restart": 60, "max_iter": 1000}
+    std::string solver = "lu";
+    double tol = 1e-12;
+    int restart = 60, max_iter = 1000;
 };
 
 // FrequencySystem over a BemSpec, plus a many-frequency evaluation that the

@@ -15,7 +15,9 @@ std::unique_ptr<FrequencySystem> make_bem_system(const BemSpec& spec) {
     m.density = spec.density;
     m.traction = spec.traction;
     m.channels = spec.channels;
-    return std::make_unique<b200::BemSystem>(m);
+    auto sys = std::make_unique<b200::BemSystem>(m);
+    if (spec.solver == "gmres") sys->set_solver(true, spec.tol, spec.restart, spec.max_iter);
+    return sys;
 }
 
 std::vector<std::vector<Complex>> evaluate_many(const FrequencySystem& system, std::span<const Complex> s) {

@@ -115,6 +115,14 @@ cli::BemSpec bem_spec(const json& j) {
         for (int e : j.at("collocation_points").get<std::vector<int>>())
             for (int d = 0; d < 3; ++d) b.channels.push_back(3 * e + d);
     b.max_batch = j.value("max_batch", 0);
+    if (j.contains("solver")) {
+        const json& sv = j.at("solver");
+        b.solver = sv.value("kind", "lu");
+        if (b.solver != "lu" && b.solver != "gmres") throw ValidationError("bem: solver kind must be lu or gmres");
+        b.tol = sv.value("tol", b.tol);
+        b.restart = sv.value("restart", b.restart);
+        b.max_iter = sv.value("max_iter", b.max_iter);
+    }
     return b;
 }
 

@@ -269,3 +269,21 @@ def test_gpu_cli_bem_resume_equivalence(tmp_path):
     jf = _resume_roundtrip(GPU_CLI, tmp_path, sysj, write(tmp_path / "f.json", base),
                            write(tmp_path / "s.json", dict(base, max_iterations=2)))
     assert jf["n_c"] == 14
+
+
+@pytest.mark.gpu
+def test_gpu_cli_bem_gmres_solver_matches_lu(tmp_path):
+    base = {"type": "bem", "mesh": {"kind": "icosphere", "level": 2}, "load": {"kind": "pressure"},
+            "collocation_points": list(range(16))}
+    cfg = write(tmp_path / "c.json", {"period": 20.0, "samples": 32, "eta": 0.25})
+    a, b = tmp_path / "lu", tmp_path / "gm"
+    assert run(GPU_CLI, "sweep-fsm", "--system", write(tmp_path / "s1.json", base), "--config", cfg,
+               "--out", a).returncode == 0
+    r = run(GPU_CLI, "sweep-fsm", "--system",
+            write(tmp_path / "s2.json", dict(base, solver={"kind": "gmres", "tol": 1e-13})), "--config", cfg,
+            "--out", b)
+    assert r.returncode == 0, r.stderr
+    sa, sb = read_spectrum(a / "spectrum.csv"), read_spectrum(b / "spectrum.csv")
+    x = np.array([sa[k] for k in sorted(sa)])
+    y = np.array([sb[k] for k in sorted(sb)])
+    assert np.linalg.norm(x - y) / np.linalg.norm(x) < 1e-10
