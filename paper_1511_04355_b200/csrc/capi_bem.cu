@@ -145,9 +145,7 @@ struct fds_bem {
             FDS_CUDA(cudaMemsetAsync(info, 0, B * sizeof(int), st));
             gm_iters = 0;
             gm_resid = 0.0;
-            for (int b = 0; b < B; ++b) {
-                const double* Ab = A + static_cast<size_t>(b) * mstride;
-                const GmresStats gs = gmres_solve(Ab, Ab + plane, n, ld, rhs + static_cast<size_t>(b) * ld, gp, gws, st);
+            for (const GmresStats& gs : gmres_solve_batch(A, mstride, plane, n, ld, B, rhs, ld, gp, gws, st)) {
                 gm_iters = std::max(gm_iters, gs.iterations);
                 gm_resid = std::max(gm_resid, gs.rel_residual);
             }

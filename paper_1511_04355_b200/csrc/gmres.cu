@@ -1,4 +1,6 @@
-// Restarted, right-preconditioned GMRES on a dense device-resident system.
+// Restarted, right-preconditioned GMRES on dense device-resident systems, run
+// for a batch of independent systems in lockstep (one launch per operation for
+// every still-active system, one host round trip per Arnoldi step).
 //
 //   gm_pinv_kernel       3x3 complex diagonal-block inverses (one per element):
 //                        the block-Jacobi preconditioner M^{-1}.
@@ -12,9 +14,11 @@
 //                        block partition + tree, so reductions are reproducible).
 //   gm_axpy_kernel       w -= V h / x += V y style updates, thread per row.
 //
-// Classical Gram–Schmidt applied twice (CGS2) keeps the basis orthogonal to
-// rounding; the small Hessenberg least-squares problem (Givens rotations) runs
-// on the host.
+// Classical Gram–Schmidt applied twice (CGS2) keeps each basis orthogonal to
+// rounding; the small Hessenberg least-squares problems (Givens rotations) run
+// on the host. A system leaves the Arnoldi loop when its own residual estimate
+// reaches tol, so converged systems stop costing matrix-vector products.
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <vector>
@@ -27,10 +31,20 @@ namespace {
 
 constexpr int kMvThreads = 256, kMvRows = 2 * kMvThreads, kMvCols = 1024, kDotThreads = 256, kDotRows = 2048;
 
-__global__ void gm_pinv_kernel(const double* __restrict__ Are, const double* __restrict__ Aim, int ne, int ld,
+// per-system vector: system b at base + b * stride (+ off)
+struct SysVec {
+    cplx* base;
+    size_t stride;
+    __host__ __device__ cplx* at(int b, size_t off = 0) const { return base + b * stride + off; }
+};
+
+__global__ void gm_pinv_kernel(const double* __restrict__ A, size_t mstride, size_t plane, int ne, int ld,
                                cplx* __restrict__ pinv) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.y;
     if (e >= ne) return;
+    const double* Are = A + b * mstride;
+    const double* Aim = Are + plane;
     cplx a[3][3], x[3][3];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) {
@@ -62,25 +76,33 @@ __global__ void gm_pinv_kernel(const double* __restrict__ Are, const double* __r
             }
         }
     }
+    cplx* P = pinv + (static_cast<size_t>(b) * ne + e) * 9;
     for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) pinv[9 * static_cast<size_t>(e) + 3 * i + j] = x[i][j];
+        for (int j = 0; j < 3; ++j) P[3 * i + j] = x[i][j];
 }
 
-__global__ void gm_precond_kernel(const cplx* __restrict__ pinv, const cplx* __restrict__ x, int ne,
-                                  cplx* __restrict__ z) {
+__global__ void gm_precond_kernel(const cplx* __restrict__ pinv, int ne, const int* __restrict__ act, SysVec x,
+                                  size_t xoff, SysVec z) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= ne) return;
-    const cplx* P = pinv + 9 * static_cast<size_t>(e);
-    const cplx x0 = x[3 * e], x1 = x[3 * e + 1], x2 = x[3 * e + 2];
-    for (int i = 0; i < 3; ++i) z[3 * e + i] = P[3 * i] * x0 + P[3 * i + 1] * x1 + P[3 * i + 2] * x2;
+    const int b = act[blockIdx.y];
+    const cplx* P = pinv + (static_cast<size_t>(b) * ne + e) * 9;
+    const cplx* xb = x.at(b, xoff);
+    cplx* zb = z.at(b);
+    const cplx x0 = xb[3 * e], x1 = xb[3 * e + 1], x2 = xb[3 * e + 2];
+    for (int i = 0; i < 3; ++i) zb[3 * e + i] = P[3 * i] * x0 + P[3 * i + 1] * x1 + P[3 * i + 2] * x2;
 }
 
 // Each thread owns two adjacent rows (16-byte loads), so a warp streams 512
 // contiguous bytes of a column per plane and a CTA 4 KB.
-__global__ void __launch_bounds__(kMvThreads)
-gm_matvec_kernel(const double* __restrict__ Are, const double* __restrict__ Aim, int n, int ld,
-                 const cplx* __restrict__ x, cplx* __restrict__ partial) {
+__global__ void __launch_bounds__(kMvThreads, 4)
+gm_matvec_kernel(const double* __restrict__ A, size_t mstride, size_t plane, int n, int ld,
+                 const int* __restrict__ act, SysVec xv, cplx* __restrict__ partial, int nchunk) {
     __shared__ cplx xs[kMvCols];
+    const int a = blockIdx.z, b = act[a];
+    const double* Are = A + b * mstride;
+    const double* Aim = Are + plane;
+    const cplx* x = xv.at(b);
     const int c0 = blockIdx.y * kMvCols, cn = min(kMvCols, n - c0);
     for (int q = threadIdx.x; q < cn; q += kMvThreads) xs[q] = x[c0 + q];
     __syncthreads();
@@ -115,210 +137,326 @@ gm_matvec_kernel(const double* __restrict__ Are, const double* __restrict__ Aim,
         s1r += ar.y * v.re - ai.y * v.im;
         s1i += ar.y * v.im + ai.y * v.re;
     }
-    cplx* out = partial + static_cast<size_t>(blockIdx.y) * n;
+    cplx* out = partial + (static_cast<size_t>(a) * nchunk + blockIdx.y) * n;
     out[r] = mk(s0r, s0i);
     if (r + 1 < n) out[r + 1] = mk(s1r, s1i);
 }
 
-// y = sum over chunks of partial (fixed order); optionally y = b - y.
+// y_b = sum over chunks (fixed order); with rhs: y_b = rhs_b - sum.
 __global__ void gm_chunk_reduce_kernel(const cplx* __restrict__ partial, int nchunk, int n,
-                                       const cplx* __restrict__ b, cplx* __restrict__ y) {
+                                       const int* __restrict__ act, SysVec rhs, bool with_rhs, SysVec y) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    const int a = blockIdx.y, b = act[a];
+    const cplx* p = partial + static_cast<size_t>(a) * nchunk * n;
     cplx s = mk(0.0, 0.0);
-    for (int q = 0; q < nchunk; ++q) s = s + partial[static_cast<size_t>(q) * n + r];
-    y[r] = b ? b[r] - s : s;
+    for (int q = 0; q < nchunk; ++q) s = s + p[static_cast<size_t>(q) * n + r];
+    y.at(b)[r] = with_rhs ? rhs.at(b)[r] - s : s;
 }
 
-// partial[blk][i] = sum over the block's rows of conj(V_i[r]) w[r], i < cnt.
+// partial[a][blk][i] = sum over the block's rows of conj(V_i[r]) w[r], i < cnt.
 __global__ void __launch_bounds__(kDotThreads)
-gm_dots_kernel(const cplx* __restrict__ V, int n, int cnt, const cplx* __restrict__ w, cplx* __restrict__ partial) {
+gm_dots_kernel(SysVec V, int n, int cnt, const int* __restrict__ act, SysVec w, cplx* __restrict__ partial) {
     __shared__ cplx red[kDotThreads];
+    const int a = blockIdx.y, b = act[a];
+    const cplx* wb = w.at(b);
     const int r0 = blockIdx.x * kDotRows;
     const int r1 = min(n, r0 + kDotRows);
+    cplx* out = partial + (static_cast<size_t>(a) * gridDim.x + blockIdx.x) * cnt;
     for (int i = 0; i < cnt; ++i) {
-        const cplx* vi = V + static_cast<size_t>(i) * n;
+        const cplx* vi = V.at(b, static_cast<size_t>(i) * n);
         cplx s = mk(0.0, 0.0);
-        for (int r = r0 + threadIdx.x; r < r1; r += kDotThreads) s = s + conjg(vi[r]) * w[r];
+        for (int r = r0 + threadIdx.x; r < r1; r += kDotThreads) s = s + conjg(vi[r]) * wb[r];
         red[threadIdx.x] = s;
         __syncthreads();
         for (int h = kDotThreads / 2; h > 0; h >>= 1) {
             if (threadIdx.x < h) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + h];
             __syncthreads();
         }
-        if (threadIdx.x == 0) partial[static_cast<size_t>(blockIdx.x) * cnt + i] = red[0];
+        if (threadIdx.x == 0) out[i] = red[0];
         __syncthreads();
     }
 }
 
 __global__ void gm_dots_reduce_kernel(const cplx* __restrict__ partial, int nblk, int cnt, cplx* __restrict__ h) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int a = blockIdx.y;
     if (i >= cnt) return;
+    const cplx* p = partial + static_cast<size_t>(a) * nblk * cnt;
     cplx s = mk(0.0, 0.0);
-    for (int q = 0; q < nblk; ++q) s = s + partial[static_cast<size_t>(q) * cnt + i];
-    h[i] = s;
+    for (int q = 0; q < nblk; ++q) s = s + p[static_cast<size_t>(q) * cnt + i];
+    h[static_cast<size_t>(a) * cnt + i] = s;
 }
 
-// y[r] = alpha * y[r] + sign * sum_{i<cnt} V_i[r] c_i   (c in device memory)
-__global__ void gm_axpy_kernel(const cplx* __restrict__ V, int n, int cnt, const cplx* __restrict__ c, double sign,
-                               double alpha, cplx* __restrict__ y) {
+// y_b = alpha * y_b + sign * sum_{i<cnt} V_b,i c[a][i]
+__global__ void gm_axpy_kernel(SysVec V, int n, int cnt, const int* __restrict__ act, const cplx* __restrict__ c,
+                               double sign, double alpha, SysVec y) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    const int a = blockIdx.y, b = act[a];
+    const cplx* ca = c + static_cast<size_t>(a) * cnt;
     cplx s = mk(0.0, 0.0);
-    for (int i = 0; i < cnt; ++i) s = s + V[static_cast<size_t>(i) * n + r] * c[i];
-    y[r] = y[r] * alpha + s * sign;
+    for (int i = 0; i < cnt; ++i) s = s + V.at(b, static_cast<size_t>(i) * n)[r] * ca[i];
+    cplx* yb = y.at(b);
+    yb[r] = yb[r] * alpha + s * sign;
 }
 
-__global__ void gm_scale_kernel(const cplx* __restrict__ x, int n, double s, cplx* __restrict__ y) {
+// y_b (+off) = x_b * s[a]
+__global__ void gm_scale_kernel(SysVec x, int n, const int* __restrict__ act, const double* __restrict__ s, SysVec y,
+                                size_t yoff) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) y[r] = x[r] * s;
+    if (r >= n) return;
+    const int a = blockIdx.y, b = act[a];
+    y.at(b, yoff)[r] = x.at(b)[r] * s[a];
 }
 
 using Cx = std::complex<double>;
 
 struct Ops {
-    const double *Are, *Aim;
-    int n, ld;
+    const double* A;
+    size_t mstride, plane;
+    int n, ld, B, m;
     GmresWorkspace& ws;
     cudaStream_t st;
+    int nact = 0;
+    int* act_dev() const { return ws.act; }
     cplx* partial() const { return reinterpret_cast<cplx*>(ws.partial); }
+    cplx* hbuf() const { return reinterpret_cast<cplx*>(ws.h_dev); }
     int nchunk() const { return ceil_div(n, kMvCols); }
-    // y = A x  (or y = b - A x)
-    void matvec(const cplx* x, cplx* y, const cplx* b = nullptr) const {
-        dim3 g(ceil_div(n, kMvRows), nchunk());
-        FDS_LAUNCH(gm_matvec_kernel, g, kMvThreads, 0, st, Are, Aim, n, ld, x, partial());
-        FDS_LAUNCH(gm_chunk_reduce_kernel, ceil_div(n, 256), 256, 0, st, partial(), nchunk(), n, b, y);
+    // Staging rule: a pinned slot is rewritten only after a stream synchronisation
+    // that follows its previous copy (every Arnoldi step synchronises in dots()).
+    void set_active(const std::vector<int>& act) {
+        nact = static_cast<int>(act.size());
+        if (!nact) return;
+        std::copy(act.begin(), act.end(), ws.pin_act);
+        FDS_CUDA(cudaMemcpyAsync(ws.act, ws.pin_act, nact * sizeof(int), cudaMemcpyHostToDevice, st));
     }
-    void precond(const cplx* x, cplx* z) const {
-        FDS_LAUNCH(gm_precond_kernel, ceil_div(n / 3, 128), 128, 0, st, reinterpret_cast<const cplx*>(ws.pinv), x,
-                   n / 3, z);
+    SysVec V() const { return {reinterpret_cast<cplx*>(ws.V), static_cast<size_t>(m + 1) * n}; }
+    SysVec vec(double* p) const { return {reinterpret_cast<cplx*>(p), static_cast<size_t>(n)}; }
+    // y = A x, or y = rhs - A x
+    void matvec(SysVec x, SysVec y, const SysVec* rhs = nullptr) const {
+        dim3 g(ceil_div(n, kMvRows), nchunk(), nact);
+        FDS_LAUNCH(gm_matvec_kernel, g, kMvThreads, 0, st, A, mstride, plane, n, ld, act_dev(), x, partial(),
+                   nchunk());
+        dim3 gr(ceil_div(n, 256), nact);
+        FDS_LAUNCH(gm_chunk_reduce_kernel, gr, 256, 0, st, partial(), nchunk(), n, act_dev(), rhs ? *rhs : y,
+                   rhs != nullptr, y);
     }
-    // h[0..cnt) = V^H w, copied to the host
-    void dots(const cplx* V, int cnt, const cplx* w, std::vector<Cx>& h) const {
+    void precond(SysVec x, size_t xoff, SysVec z) const {
+        dim3 g(ceil_div(n / 3, 128), nact);
+        FDS_LAUNCH(gm_precond_kernel, g, 128, 0, st, reinterpret_cast<const cplx*>(ws.pinv), n / 3, act_dev(), x,
+                   xoff, z);
+    }
+    // h[a][0..cnt) = V_b^H w_b, to the host
+    void dots(SysVec Vv, int cnt, SysVec w, std::vector<Cx>& h) const {
         const int nblk = ceil_div(n, kDotRows);
-        cplx* hd = reinterpret_cast<cplx*>(ws.h_dev);
-        FDS_LAUNCH(gm_dots_kernel, nblk, kDotThreads, 0, st, V, n, cnt, w, partial());
-        FDS_LAUNCH(gm_dots_reduce_kernel, ceil_div(cnt, 64), 64, 0, st, partial(), nblk, cnt, hd);
-        h.resize(cnt);
-        FDS_CUDA(cudaMemcpyAsync(h.data(), hd, cnt * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+        FDS_LAUNCH(gm_dots_kernel, dim3(nblk, nact), kDotThreads, 0, st, Vv, n, cnt, act_dev(), w, partial());
+        FDS_LAUNCH(gm_dots_reduce_kernel, dim3(ceil_div(cnt, 64), nact), 64, 0, st, partial(), nblk, cnt, hbuf());
+        h.resize(static_cast<size_t>(nact) * cnt);
+        FDS_CUDA(cudaMemcpyAsync(h.data(), hbuf(), h.size() * sizeof(cplx), cudaMemcpyDeviceToHost, st));
         FDS_CUDA(cudaStreamSynchronize(st));
     }
-    void axpy(const cplx* V, int cnt, const std::vector<Cx>& c, double sign, double alpha, cplx* y) const {
-        cplx* hd = reinterpret_cast<cplx*>(ws.h_dev);
-        FDS_CUDA(cudaMemcpyAsync(hd, c.data(), cnt * sizeof(cplx), cudaMemcpyHostToDevice, st));
-        FDS_LAUNCH(gm_axpy_kernel, ceil_div(n, 256), 256, 0, st, V, n, cnt, hd, sign, alpha, y);
+    // y_b = alpha y_b + sign * V_b c[a]   (c: host, [nact][cnt]; staged in pinned slot `slot`)
+    void axpy(SysVec Vv, int cnt, const std::vector<Cx>& c, double sign, double alpha, SysVec y, int slot = 0) const {
+        std::copy(c.begin(), c.end(), reinterpret_cast<Cx*>(ws.pin_coef[slot]));
+        cplx* dst = hbuf() + static_cast<size_t>(slot) * B * (m + 2);
+        FDS_CUDA(cudaMemcpyAsync(dst, ws.pin_coef[slot], c.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
+        FDS_LAUNCH(gm_axpy_kernel, dim3(ceil_div(n, 256), nact), 256, 0, st, Vv, n, cnt, act_dev(), dst, sign, alpha,
+                   y);
     }
-    double norm(const cplx* w) const {
+    void norms(SysVec w, std::vector<double>& out) const {
         std::vector<Cx> h;
         dots(w, 1, w, h);
-        return std::sqrt(std::max(h[0].real(), 0.0));
+        out.resize(nact);
+        for (int a = 0; a < nact; ++a) out[a] = std::sqrt(std::max(h[a].real(), 0.0));
+    }
+    void scale(SysVec x, const std::vector<double>& s, SysVec y, size_t yoff) const {
+        std::copy(s.begin(), s.begin() + nact, ws.pin_scal);
+        FDS_CUDA(cudaMemcpyAsync(ws.scal, ws.pin_scal, nact * sizeof(double), cudaMemcpyHostToDevice, st));
+        FDS_LAUNCH(gm_scale_kernel, dim3(ceil_div(n, 256), nact), 256, 0, st, x, n, act_dev(), ws.scal, y, yoff);
+    }
+};
+
+// per-system Arnoldi / Givens state of one cycle
+struct Cycle {
+    std::vector<Cx> H, cs, sn, g;
+    int j = 0;  // columns built
+    void reset(int m, double beta) {
+        H.assign(static_cast<size_t>(m + 1) * m, Cx(0.0, 0.0));
+        cs.assign(m, Cx(0.0, 0.0));
+        sn.assign(m, Cx(0.0, 0.0));
+        g.assign(m + 1, Cx(0.0, 0.0));
+        g[0] = beta;
+        j = 0;
     }
 };
 
 }  // namespace
 
-void GmresWorkspace::ensure(int n, int m) {
-    if (static_cast<size_t>(n) <= n_cap && m <= m_cap) return;
+void GmresWorkspace::ensure(int n, int m, int B) {
+    if (static_cast<size_t>(n) <= n_cap && m <= m_cap && B <= b_cap) return;
     release();
-    const size_t nc = static_cast<size_t>(n);
+    const size_t nc = static_cast<size_t>(n), bb = static_cast<size_t>(B);
     const size_t nchunk = (nc + kMvCols - 1) / kMvCols;
-    FDS_CUDA(cudaMalloc(&V, 2 * nc * (m + 1) * sizeof(double)));
-    FDS_CUDA(cudaMalloc(&w, 2 * nc * sizeof(double)));
-    FDS_CUDA(cudaMalloc(&z, 2 * nc * sizeof(double)));
-    FDS_CUDA(cudaMalloc(&pinv, 2 * 3 * nc * sizeof(double)));
     const size_t nblk = (nc + kDotRows - 1) / kDotRows;
-    FDS_CUDA(cudaMalloc(&partial, 2 * std::max(nchunk * nc, nblk * (m + 2)) * sizeof(double)));
-    FDS_CUDA(cudaMalloc(&h_dev, 2 * (m + 2) * sizeof(double)));
-    FDS_CUDA(cudaMalloc(&bsave, 2 * nc * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&V, 2 * nc * (m + 1) * bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&w, 2 * nc * bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&z, 2 * nc * bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&bsave, 2 * nc * bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&pinv, 2 * 3 * nc * bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&partial, 2 * bb * std::max(nchunk * nc, nblk * (m + 2)) * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&h_dev, 2 * 2 * bb * (m + 2) * sizeof(double)));  // dots results / two coefficient slots
+    FDS_CUDA(cudaMallocHost(&pin_act, bb * sizeof(int)));
+    FDS_CUDA(cudaMallocHost(&pin_coef[0], 2 * bb * (m + 2) * sizeof(double)));
+    FDS_CUDA(cudaMallocHost(&pin_coef[1], 2 * bb * (m + 2) * sizeof(double)));
+    FDS_CUDA(cudaMallocHost(&pin_scal, bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&scal, bb * sizeof(double)));
+    FDS_CUDA(cudaMalloc(&act, bb * sizeof(int)));
     n_cap = nc;
     m_cap = m;
+    b_cap = B;
 }
 
 void GmresWorkspace::release() {
-    for (double* p : {V, w, z, pinv, partial, h_dev, bsave})
+    for (double* p : {V, w, z, pinv, partial, h_dev, bsave, scal})
         if (p) cudaFree(p);
-    V = w = z = pinv = partial = h_dev = bsave = nullptr;
+    if (act) cudaFree(act);
+    for (void* q : {static_cast<void*>(pin_act), static_cast<void*>(pin_coef[0]), static_cast<void*>(pin_coef[1]),
+                    static_cast<void*>(pin_scal)})
+        if (q) cudaFreeHost(q);
+    V = w = z = pinv = partial = h_dev = bsave = scal = nullptr;
+    act = nullptr;
+    pin_act = nullptr;
+    pin_coef[0] = pin_coef[1] = pin_scal = nullptr;
     n_cap = 0;
     m_cap = 0;
+    b_cap = 0;
 }
 
-GmresStats gmres_solve(const double* Are, const double* Aim, int n, int ld, cplx* b, const GmresParams& p,
-                       GmresWorkspace& ws, cudaStream_t st) {
+std::vector<GmresStats> gmres_solve_batch(const double* A, size_t mstride, size_t plane, int n, int ld, int B,
+                                          cplx* rhs, size_t rstride, const GmresParams& p, GmresWorkspace& ws,
+                                          cudaStream_t st) {
     if (n % 3 != 0) throw ValidationError("gmres: n must be a multiple of 3 (element-major DOFs)");
+    std::vector<GmresStats> stats(B);
+    if (B == 0) return stats;
     const int m = std::max(1, p.restart);
-    ws.ensure(n, m);
-    Ops op{Are, Aim, n, ld, ws, st};
-    cplx* V = reinterpret_cast<cplx*>(ws.V);
-    cplx* w = reinterpret_cast<cplx*>(ws.w);
-    cplx* z = reinterpret_cast<cplx*>(ws.z);
-    cplx* bsave = reinterpret_cast<cplx*>(ws.bsave);
-    auto col = [&](int i) { return V + static_cast<size_t>(i) * n; };
-    FDS_LAUNCH(gm_pinv_kernel, ceil_div(n / 3, 128), 128, 0, st, Are, Aim, n / 3, ld, reinterpret_cast<cplx*>(ws.pinv));
-    // keep the right-hand side; x accumulates in b's buffer from x = 0, and r = b - A x = b
-    FDS_CUDA(cudaMemcpyAsync(bsave, b, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    FDS_CUDA(cudaMemcpyAsync(w, b, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    FDS_CUDA(cudaMemsetAsync(b, 0, n * sizeof(cplx), st));
-    const double bnorm = op.norm(w);
-    GmresStats stats;
-    if (bnorm == 0.0) return stats;  // x = 0
-    double beta = bnorm;
-    std::vector<Cx> H(static_cast<size_t>(m + 1) * m), cs(m), sn(m), g(m + 1), h, h2;
+    ws.ensure(n, m, B);
+    Ops op{A, mstride, plane, n, ld, B, m, ws, st};
+    const SysVec V = op.V(), w = op.vec(ws.w), z = op.vec(ws.z), bs = op.vec(ws.bsave);
+    const SysVec x{rhs, rstride};
+    FDS_LAUNCH(gm_pinv_kernel, dim3(ceil_div(n / 3, 128), B), 128, 0, st, A, mstride, plane, n / 3, ld,
+               reinterpret_cast<cplx*>(ws.pinv));
+    // save b, r = b (x = 0), x := 0
+    for (int b = 0; b < B; ++b) {
+        FDS_CUDA(cudaMemcpyAsync(bs.at(b), x.at(b), n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        FDS_CUDA(cudaMemcpyAsync(w.at(b), x.at(b), n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        FDS_CUDA(cudaMemsetAsync(x.at(b), 0, n * sizeof(cplx), st));
+    }
+    std::vector<int> all(B);
+    for (int b = 0; b < B; ++b) all[b] = b;
+    op.set_active(all);
+    std::vector<double> bnorm, beta;
+    op.norms(w, bnorm);
+    beta = bnorm;
+    std::vector<Cycle> cyc(B);
+    std::vector<int> live;  // systems still being solved (b = 0 gives x = 0 at once)
+    for (int b = 0; b < B; ++b)
+        if (bnorm[b] > 0.0) live.push_back(b);
+    std::vector<Cx> h, h2, coef;
+    std::vector<double> hn, sc;
     while (true) {
-        if (beta / bnorm <= p.tol || stats.iterations >= p.max_iter) break;
-        FDS_LAUNCH(gm_scale_kernel, ceil_div(n, 256), 256, 0, st, w, n, 1.0 / beta, col(0));
-        std::fill(g.begin(), g.end(), Cx(0.0, 0.0));
-        g[0] = beta;
-        int j = 0;
-        for (; j < m && stats.iterations < p.max_iter; ++j) {
-            op.precond(col(j), z);
+        std::vector<int> act;  // systems that still need a cycle
+        for (int b : live) {
+            stats[b].rel_residual = beta[b] / bnorm[b];
+            if (stats[b].rel_residual > p.tol && stats[b].iterations < p.max_iter) act.push_back(b);
+        }
+        live = act;
+        if (live.empty()) break;
+        // new cycle: V_b0 = r_b / beta_b
+        op.set_active(live);
+        sc.resize(live.size());
+        for (size_t a = 0; a < live.size(); ++a) {
+            sc[a] = 1.0 / beta[live[a]];
+            cyc[live[a]].reset(m, beta[live[a]]);
+        }
+        op.scale(w, sc, V, 0);
+        std::vector<int> arn = live;  // systems still extending their basis in this cycle
+        for (int j = 0; j < m && !arn.empty(); ++j) {
+            if (j > 0) op.set_active(arn);  // j = 0: the device list already holds `live`
+            const int na = static_cast<int>(arn.size());
+            op.precond(V, static_cast<size_t>(j) * n, z);
             op.matvec(z, w);
             op.dots(V, j + 1, w, h);  // CGS, twice
             op.axpy(V, j + 1, h, -1.0, 1.0, w);
             op.dots(V, j + 1, w, h2);
             op.axpy(V, j + 1, h2, -1.0, 1.0, w);
-            for (int i = 0; i <= j; ++i) H[static_cast<size_t>(i) * m + j] = h[i] + h2[i];
-            const double hn = op.norm(w);
-            H[static_cast<size_t>(j + 1) * m + j] = hn;
-            // previous rotations, then a new one zeroing H[j+1][j]
-            for (int i = 0; i < j; ++i) {
-                const Cx a = H[static_cast<size_t>(i) * m + j], bb = H[static_cast<size_t>(i + 1) * m + j];
-                H[static_cast<size_t>(i) * m + j] = std::conj(cs[i]) * a + std::conj(sn[i]) * bb;
-                H[static_cast<size_t>(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+            op.norms(w, hn);
+            sc.assign(na, 0.0);
+            std::vector<int> next;
+            for (int a = 0; a < na; ++a) {
+                const int b = arn[a];
+                Cycle& c = cyc[b];
+                auto Hc = [&](int i, int col) -> Cx& { return c.H[static_cast<size_t>(i) * m + col]; };
+                for (int i = 0; i <= j; ++i)
+                    Hc(i, j) = h[static_cast<size_t>(a) * (j + 1) + i] + h2[static_cast<size_t>(a) * (j + 1) + i];
+                Hc(j + 1, j) = hn[a];
+                for (int i = 0; i < j; ++i) {  // previous rotations
+                    const Cx u = Hc(i, j), v = Hc(i + 1, j);
+                    Hc(i, j) = std::conj(c.cs[i]) * u + std::conj(c.sn[i]) * v;
+                    Hc(i + 1, j) = -c.sn[i] * u + c.cs[i] * v;
+                }
+                const Cx u = Hc(j, j), v = Hc(j + 1, j);
+                const double den = std::sqrt(std::norm(u) + std::norm(v));
+                if (den == 0.0) throw NumericError("gmres: breakdown (zero Krylov column)");
+                c.cs[j] = u / den;
+                c.sn[j] = v / den;
+                Hc(j, j) = den;
+                Hc(j + 1, j) = 0.0;
+                c.g[j + 1] = -c.sn[j] * c.g[j];
+                c.g[j] = std::conj(c.cs[j]) * c.g[j];
+                c.j = j + 1;
+                ++stats[b].iterations;
+                sc[a] = hn[a] > 0.0 ? 1.0 / hn[a] : 0.0;
+                const bool done = std::abs(c.g[j + 1]) / bnorm[b] <= p.tol || hn[a] == 0.0 ||
+                                  stats[b].iterations >= p.max_iter;
+                if (!done) next.push_back(b);
             }
-            const Cx a = H[static_cast<size_t>(j) * m + j], bb = H[static_cast<size_t>(j + 1) * m + j];
-            const double den = std::sqrt(std::norm(a) + std::norm(bb));
-            if (den == 0.0) throw NumericError("gmres: breakdown (zero Krylov column)");
-            cs[j] = a / den;
-            sn[j] = bb / den;
-            H[static_cast<size_t>(j) * m + j] = den;
-            H[static_cast<size_t>(j + 1) * m + j] = 0.0;
-            g[j + 1] = -sn[j] * g[j];
-            g[j] = std::conj(cs[j]) * g[j];
-            ++stats.iterations;
-            if (hn > 0.0) FDS_LAUNCH(gm_scale_kernel, ceil_div(n, 256), 256, 0, st, w, n, 1.0 / hn, col(j + 1));
-            if (std::abs(g[j + 1]) / bnorm <= p.tol || hn == 0.0) {
-                ++j;
-                break;
+            op.scale(w, sc, V, static_cast<size_t>(j + 1) * n);
+            arn = next;
+        }
+        // y_b = H_b^{-1} g_b; x_b += M^{-1} V_b y_b; true residual
+        op.set_active(live);
+        int jmax = 0;
+        for (int b : live) jmax = std::max(jmax, cyc[b].j);
+        coef.assign(live.size() * static_cast<size_t>(jmax), Cx(0.0, 0.0));
+        for (size_t a = 0; a < live.size(); ++a) {
+            Cycle& c = cyc[live[a]];
+            for (int i = c.j - 1; i >= 0; --i) {
+                Cx s = c.g[i];
+                for (int q = i + 1; q < c.j; ++q) s -= c.H[static_cast<size_t>(i) * m + q] * coef[a * jmax + q];
+                coef[a * jmax + i] = s / c.H[static_cast<size_t>(i) * m + i];
             }
         }
-        // y = H^{-1} g (upper triangular j x j); x += M^{-1} V y
-        std::vector<Cx> y(j);
-        for (int i = j - 1; i >= 0; --i) {
-            Cx s = g[i];
-            for (int q = i + 1; q < j; ++q) s -= H[static_cast<size_t>(i) * m + q] * y[q];
-            y[i] = s / H[static_cast<size_t>(i) * m + i];
-        }
-        op.axpy(V, j, y, 1.0, 0.0, w);  // w = V y
-        op.precond(w, z);
-        op.axpy(z, 1, std::vector<Cx>{Cx(1.0, 0.0)}, 1.0, 1.0, b);  // x += M^{-1} V y
-        op.matvec(b, w, bsave);                                     // true residual r = b - A x
-        beta = op.norm(w);
+        op.axpy(V, jmax, coef, 1.0, 0.0, w, 0);  // w = V y
+        op.precond(w, 0, z);
+        coef.assign(live.size(), Cx(1.0, 0.0));
+        op.axpy(z, 1, coef, 1.0, 1.0, x, 1);  // x += M^{-1} V y (second staging slot: no sync in between)
+        op.matvec(x, w, &bs);             // r = b - A x
+        op.norms(w, hn);
+        for (size_t a = 0; a < live.size(); ++a) beta[live[a]] = hn[a];
     }
-    stats.rel_residual = beta / bnorm;
-    if (!(stats.rel_residual <= p.tol))
-        throw ConvergenceError("gmres: relative residual " + std::to_string(stats.rel_residual) + " after " +
-                               std::to_string(stats.iterations) + " iterations");
+    for (int b = 0; b < B; ++b)
+        if (!(stats[b].rel_residual <= p.tol))
+            throw ConvergenceError("gmres: relative residual " + std::to_string(stats[b].rel_residual) + " after " +
+                                   std::to_string(stats[b].iterations) + " iterations (system " + std::to_string(b) +
+                                   ")");
     return stats;
+}
+
+GmresStats gmres_solve(const double* Are, const double* Aim, int n, int ld, cplx* b, const GmresParams& p,
+                       GmresWorkspace& ws, cudaStream_t st) {
+    const size_t plane = static_cast<size_t>(Aim - Are);
+    return gmres_solve_batch(Are, 2 * plane, plane, n, ld, 1, b, static_cast<size_t>(n), p, ws, st)[0];
 }
 
 }  // namespace fdsb
