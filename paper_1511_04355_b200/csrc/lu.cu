@@ -20,6 +20,7 @@
 //                        double-buffered smem, bank-conflict-free padded layouts.
 // Row swaps are LAPACK-style inside a panel and LINPACK-style across panels
 // (earlier L columns are not permuted); lu_solve applies them in that order.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -207,6 +208,162 @@ lu_panel_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batc
             }
         __syncthreads();
     }
+}
+
+// Cluster variant for batches of moderate N: the P CTAs of one matrix form a
+// thread-block cluster, so the per-column pivot exchange runs through
+// distributed shared memory — every CTA publishes its candidate (|a|, row, row
+// values) in its own smem, one hardware cluster barrier, then each CTA reads
+// the P keys and the winning row straight from the peers' smem (mapa /
+// ld.shared::cluster) instead of a global-memory slot + atomic-counter barrier.
+// Candidate slots are double-buffered by column parity, so a single barrier per
+// column suffices (a slot is rewritten two columns later, after every CTA has
+// passed the intervening barrier).
+template <int NB>
+__global__ void __launch_bounds__(kPanelThreads)
+lu_panel_cluster_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int batch, int k, int w, int R,
+                        int G, int* ipiv, int* info) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ double sm[];
+    double* tre = sm;             // [NB][R]
+    double* tim = tre + NB * R;   // [NB][R]
+    double* urow = tim + NB * R;  // [2NB] pivot row (new row c)
+    double* drow = urow + 2 * NB; // [2NB] old row c (moves to the pivot row)
+    // published per parity: [0] |a|, [1] row, [2 .. 2+2NB) candidate row, [2+2NB .. 2+4NB) old row c
+    __shared__ double pub[2][2 + 4 * NB];
+    __shared__ double red_v[kPanelThreads / 32];
+    __shared__ int red_i[kPanelThreads / 32];
+    __shared__ int s_piv;
+    __shared__ double s_best;
+
+    const int P = static_cast<int>(cluster.num_blocks());
+    const int p = static_cast<int>(cluster.block_rank());
+    const int g = blockIdx.x / P;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned step = 0;
+    for (int b = g; b < batch; b += G) {
+        double* Are = A + static_cast<size_t>(b) * mstride;
+        double* Aim = Are + plane;
+        const int r0 = k + p * R;
+        const int r1 = min(r0 + R, n);
+        const int nr = max(0, r1 - r0);
+        const int myrow = r0 + tid;
+        const bool own = tid < nr;
+        if (own)
+            for (int j = 0; j < w; ++j) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + myrow;
+                tre[j * R + tid] = Are[gi];
+                tim[j * R + tid] = Aim[gi];
+            }
+        for (int j = 0; j < w; ++j) {
+            const int c = k + j;
+            const int par = step & 1;
+            double best = -1.0;
+            int bi = INT_MAX;
+            if (own && myrow >= c) {
+                best = fabs(tre[j * R + tid]) + fabs(tim[j * R + tid]);
+                bi = myrow;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+            }
+            if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+            __syncthreads();
+            if (wid == 0) {
+                double v = lane < kPanelThreads / 32 ? red_v[lane] : -1.0;
+                int ri = lane < kPanelThreads / 32 ? red_i[lane] : INT_MAX;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+                    const int oi = __shfl_xor_sync(0xffffffffu, ri, off);
+                    if (ov > v || (ov == v && oi < ri)) { v = ov; ri = oi; }
+                }
+                if (lane == 0) {
+                    pub[par][0] = v;
+                    pub[par][1] = static_cast<double>(ri);
+                }
+                if (ri != INT_MAX)
+                    for (int jj = lane; jj < 2 * NB; jj += 32) {
+                        const int col = jj % NB;
+                        pub[par][2 + jj] = col < w ? (jj < NB ? tre[col * R + ri - r0] : tim[col * R + ri - r0]) : 0.0;
+                    }
+            } else if (wid == 1 && c >= r0 && c < r1) {
+                for (int jj = lane; jj < 2 * NB; jj += 32) {
+                    const int col = jj % NB;
+                    pub[par][2 + 2 * NB + jj] = col < w ? (jj < NB ? tre[col * R + c - r0] : tim[col * R + c - r0]) : 0.0;
+                }
+            }
+            ++step;
+            cluster.sync();
+            // winner among the P candidates (peers' smem), pivot row + old row c
+            if (wid == 0) {
+                double bv = -1.0;
+                int bidx = INT_MAX, bw = 0;
+                for (int q = lane; q < P; q += 32) {
+                    const double* rp = cluster.map_shared_rank(&pub[par][0], q);
+                    const double kv = rp[0];
+                    const int ri = static_cast<int>(rp[1]);
+                    if (kv > bv || (kv == bv && ri < bidx)) { bv = kv; bidx = ri; bw = q; }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+                    const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+                    if (ov > bv || (ov == bv && oi < bidx)) { bv = ov; bidx = oi; bw = ow; }
+                }
+                const int owner = (c - k) / R;  // CTA holding row c
+                const double* wp = cluster.map_shared_rank(&pub[par][2], bw);
+                const double* op = cluster.map_shared_rank(&pub[par][2 + 2 * NB], owner);
+                for (int jj = lane; jj < 2 * NB; jj += 32) {
+                    urow[jj] = wp[jj];
+                    drow[jj] = op[jj];
+                }
+                if (lane == 0) {
+                    s_piv = bidx;
+                    s_best = bv;
+                    if (p == 0) {
+                        ipiv[static_cast<size_t>(b) * n + c] = bidx;
+                        if (!(bv > 0.0) && info[b] == 0) info[b] = c + 1;
+                    }
+                }
+            }
+            __syncthreads();
+            const int piv = s_piv;
+            if (own) {
+                if (myrow == c && piv != c) {
+                    for (int jj = 0; jj < w; ++jj) { tre[jj * R + tid] = urow[jj]; tim[jj * R + tid] = urow[NB + jj]; }
+                } else if (myrow == piv && piv != c) {
+                    for (int jj = 0; jj < w; ++jj) { tre[jj * R + tid] = drow[jj]; tim[jj * R + tid] = drow[NB + jj]; }
+                }
+                if (myrow > c) {
+                    const cplx u = mk(urow[j], urow[NB + j]);
+                    if (u.re != 0.0 || u.im != 0.0) {
+                        const cplx l = mk(tre[j * R + tid], tim[j * R + tid]) * crecip(u);
+                        tre[j * R + tid] = l.re;
+                        tim[j * R + tid] = l.im;
+                        for (int jj = j + 1; jj < w; ++jj) {
+                            const double ur = urow[jj], ui = urow[NB + jj];
+                            tre[jj * R + tid] -= l.re * ur - l.im * ui;
+                            tim[jj * R + tid] -= l.re * ui + l.im * ur;
+                        }
+                    }
+                }
+            }
+        }
+        if (own)
+            for (int j = 0; j < w; ++j) {
+                const size_t gi = static_cast<size_t>(k + j) * ld + myrow;
+                Are[gi] = tre[j * R + tid];
+                Aim[gi] = tim[j * R + tid];
+            }
+        __syncthreads();
+    }
+    cluster.sync();  // peers may still read this CTA's published slots
 }
 
 // ------------------------------------------------------------------ swaps + TRSM
@@ -1168,6 +1325,49 @@ int panel_rows_max() {
     return std::min(by_smem, kPanelThreads);  // one thread per row
 }
 
+bool use_cluster_panel() {
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_PANEL_CLUSTER");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+// One cluster of P CTAs per matrix (P <= 16, non-portable size), as many
+// clusters as fit at once; each loops over matrices g, g+G, ...
+template <int NB>
+void panel_step_cluster(const LuProblem& pb, int k, int w, int P, int R, size_t smem, cudaStream_t st) {
+    auto kern = lu_panel_cluster_kernel<NB>;
+    static size_t attr_smem = 0;
+    if (smem > attr_smem) {
+        FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_smem = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kPanelThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(P);
+    int clusters = 0;
+    FDS_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
+    const int G = std::max(1, std::min(pb.batch, clusters));
+    cfg.gridDim = dim3(G * P);
+    cudaEvent_t pe;
+    profiler().begin(st, kProfLuPanel, 0.0, pe);
+    FDS_CUDA(cudaLaunchKernelEx(&cfg, kern, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, pb.batch, k, w, R, G, pb.ipiv,
+                                pb.info));
+    profiler().end(st, pe, kProfLuPanel, 8.0 * (pb.n - k) * w * w / 2.0 * pb.batch);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 template <int NB>
 void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t st, bool coop = true) {
     const int sms = device_info().sms;
@@ -1182,6 +1382,10 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
         FDS_CUDA(cudaFuncSetAttribute(lu_panel_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
         attr_smem = smem;
+    }
+    if (NB == kSub && P <= 16 && use_cluster_panel()) {
+        panel_step_cluster<NB>(pb, k, w, P, R, smem, st);
+        return;
     }
     int per_sm = 1;
     FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_kernel<NB>, kPanelThreads, smem));
