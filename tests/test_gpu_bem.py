@@ -121,3 +121,25 @@ def test_random_traction_parity():
     orc, gpu = O.Bem(V, F, tr), BemSystem(V, F, tr)
     s = complex(0.25, 6.0)
     assert rel_l2(gpu.evaluate(s), orc.solve(s)) < 1e-9
+
+
+def test_cluster_and_global_panels_identical(tmp_path):
+    """The DSMEM cluster panel (default for N <= 4096 batches) and the global
+    slot + atomic-barrier panel (FDSWEEP_PANEL_CLUSTER=0) choose the same pivots
+    and do the same arithmetic: bit-identical solutions."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1511_04355_b200 import zgesv_batch;"
+        "r = np.random.default_rng(5); n, B = 700, 6;"
+        "A = r.normal(size=(B, n, n)) + 1j * r.normal(size=(B, n, n));"
+        "b = r.normal(size=(B, n)) + 1j * r.normal(size=(B, n));"
+        f"np.save('{tmp_path}/x' + sys.argv[1] + '.npy', zgesv_batch(A, b))"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for tag, env in (("c", {}), ("g", {"FDSWEEP_PANEL_CLUSTER": "0"})):
+        subprocess.run([sys.executable, "-c", code, tag], cwd=root, env=dict(os.environ, **env), check=True)
+    assert np.array_equal(np.load(tmp_path / "xc.npy"), np.load(tmp_path / "xg.npy"))
