@@ -465,7 +465,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 2)
-lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int c0) {
+lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int c0, int c1) {
     extern __shared__ __align__(16) double gsm[];
     const int b = blockIdx.z;
     double* Are = A + static_cast<size_t>(b) * mstride;
@@ -485,7 +485,7 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
             const int rem = q % (GBK * (GBM / 2));
             const int kk = rem / (GBM / 2), ch = rem % (GBM / 2);
             const double* src = (pl ? Aim : Are) + static_cast<size_t>(k + kk0 + kk) * ld + m0 + 2 * ch;
-            const int bytes = (kk0 + kk < w) ? 16 : 0;
+            const int bytes = (kk0 + kk < w && m0 + 2 * ch < ld) ? 16 : 0;  // rows past ld: sub-panel windows
             cp_async16(As(st, pl) + kk * GAS + 2 * ch, bytes ? src : Are, bytes);
         }
         // B tile: U12[k+kk0 .. +16)[n0..n0+64): per (plane, column) 16 contiguous doubles = 8 chunks
@@ -495,7 +495,7 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
             const int nn = rem / (GBK / 2), ch = rem % (GBK / 2);
             const int kk = kk0 + 2 * ch;
             const double* src = (pl ? Aim : Are) + static_cast<size_t>(n0 + nn) * ld + k + kk;
-            const int bytes = kk + 2 <= w ? 16 : (kk < w ? 8 : 0);
+            const int bytes = n0 + nn >= c1 ? 0 : (kk + 2 <= w ? 16 : (kk < w ? 8 : 0));  // window [c0, c1)
             cp_async16(Bs(st, pl) + nn * GBS + 2 * ch, bytes ? src : Are, bytes);
         }
     };
@@ -515,8 +515,9 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
             for (int e = 0; e < 2; ++e) {
                 const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
                 const size_t gi = static_cast<size_t>(col) * ld + row;
-                acr[mi][ni][e] = Are[gi];
-                aci[mi][ni][e] = Aim[gi];
+                const bool in = col < c1;  // column window [c0, c1) (sub-panel updates stop at the panel edge)
+                acr[mi][ni][e] = in ? Are[gi] : 0.0;
+                aci[mi][ni][e] = in ? Aim[gi] : 0.0;
             }
     }
     for (int kc = 0; kc < nk; ++kc) {
@@ -574,7 +575,7 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
-                if (row < n && col < n) {
+                if (row < n && col < c1) {
                     const size_t gi = static_cast<size_t>(col) * ld + row;
                     Are[gi] = acr[mi][ni][e];
                     Aim[gi] = aci[mi][ni][e];
@@ -1075,42 +1076,6 @@ lu_sub_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, 
     for (int i = 0; i < kSub; ++i) { Are[cb + ks + i] = xr[i]; Aim[cb + ks + i] = xi[i]; }
 }
 
-__global__ void __launch_bounds__(128)
-lu_sub_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, int w, int ks) {
-    // rows r >= ks+16, columns [ks+16, k+w): A -= L21s (r, ks..ks+15) * U (ks..ks+15, col)
-    __shared__ double ur[kSub][64 - kSub], ui[kSub][64 - kSub];
-    const int b = blockIdx.y;
-    double* Are = A + static_cast<size_t>(b) * mstride;
-    double* Aim = Are + plane;
-    const int c0 = ks + kSub, nc = k + w - c0;
-    for (int q = threadIdx.x; q < kSub * nc; q += blockDim.x) {
-        const int t = q % kSub, c = q / kSub;
-        const size_t gi = static_cast<size_t>(c0 + c) * ld + ks + t;
-        ur[t][c] = Are[gi];
-        ui[t][c] = Aim[gi];
-    }
-    __syncthreads();
-    const int r = ks + kSub + blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    double lr[kSub], li[kSub];
-#pragma unroll
-    for (int t = 0; t < kSub; ++t) {
-        const size_t gi = static_cast<size_t>(ks + t) * ld + r;
-        lr[t] = Are[gi];
-        li[t] = Aim[gi];
-    }
-    for (int c = 0; c < nc; ++c) {
-        const size_t gi = static_cast<size_t>(c0 + c) * ld + r;
-        double ar = Are[gi], ai = Aim[gi];
-#pragma unroll
-        for (int t = 0; t < kSub; ++t) {
-            ar -= lr[t] * ur[t][c] - li[t] * ui[t][c];
-            ai -= lr[t] * ui[t][c] + li[t] * ur[t][c];
-        }
-        Are[gi] = ar;
-        Aim[gi] = ai;
-    }
-}
 
 // ------------------------------------------------------------------ solves
 // Blocked substitution, one 64-wide block column per step (the factor's panel
@@ -1532,7 +1497,7 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                    pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
     } else {
         FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
-                   pb.plane, pb.n, pb.ld, k, w, c0);
+                   pb.plane, pb.n, pb.ld, k, w, c0, c1);
     }
     // algorithmic flops of A22 -= L21 U12 (complex): 8 * rest^2 * w per matrix
     profiler().end(st, ge, kProfLuGemm, 8.0 * rest * (c1 - c0) * w * pb.batch);
@@ -1596,8 +1561,9 @@ void subpanel_block(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStre
         FDS_LAUNCH(lu_sub_swap_trsm_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks,
                    pb.ipiv);
         if (ks + kSub < k + 64) {
-            dim3 g(ceil_div(pb.n - ks - kSub, 128), pb.batch);
-            FDS_LAUNCH(lu_sub_gemm_kernel, g, 128, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks);
+            // rank-16 update of the panel's remaining columns on the DMMA GEMM
+            // (K = 16, column window [ks+16, k+64))
+            gemm_step(pb, ks, kSub, st, ks + kSub, k + 64);
         }
     }
     profiler().enabled = keep;
