@@ -95,13 +95,16 @@ int fds_bem_last_timing(const fds_bem* bem, double* assembly_ms, double* lu_ms, 
                         int* launches);
 
 /* Solver of subsequent evaluate calls: kind 0 = batched LU with partial
- * pivoting (default); kind 1 = restarted GMRES per frequency on the assembled
- * dense A (right block-Jacobi on the 3x3 element blocks), stopping at
- * ||b - A u|| <= tol ||b|| (FDS_ECONVERGENCE if max_iter is reached first).
- * For large N one O(N^2) product per iteration beats the O(N^3) factorization. */
+ * pivoting (default); kind 1 = restarted GMRES on the assembled dense A (all
+ * frequencies of a batch in lockstep, right block-Jacobi on the 3x3 element
+ * blocks), stopping at ||b - A u|| <= tol ||b||. A frequency whose GMRES misses
+ * tol within max_iter (e.g. near an interior resonance) is solved by LU
+ * instead. For large N one O(N^2) product per iteration beats the O(N^3)
+ * factorization. */
 int fds_bem_set_solver(fds_bem* bem, int kind, double tol, int restart, int max_iter);
-/* Largest GMRES iteration count and true relative residual of the last evaluate. */
-int fds_bem_last_gmres(const fds_bem* bem, int* iterations, double* rel_residual);
+/* Of the last evaluate: largest GMRES iteration count, largest true relative
+ * residual of the GMRES-solved frequencies, number of LU fallbacks. */
+int fds_bem_last_gmres(const fds_bem* bem, int* iterations, double* rel_residual, int* lu_fallbacks);
 
 /* Dense complex LU + solve on the device for caller-provided host matrices
  * (column-major, B matrices of order n): x[b] = A[b]^{-1} rhs[b]. */

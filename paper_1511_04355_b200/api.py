@@ -220,15 +220,16 @@ class BemSystem:
         return dict(assembly_ms=a.value, lu_ms=l_.value, solve_ms=s.value, launches=n.value)
 
     def set_solver(self, kind: str = "lu", tol: float = 1e-12, restart: int = 60, max_iter: int = 1000):
-        """'lu' (batched LU, default) or 'gmres' (restarted GMRES per frequency,
-        right block-Jacobi, stop at ||b - A u|| <= tol ||b||)."""
+        """'lu' (batched LU, default) or 'gmres' (restarted GMRES, all frequencies
+        in lockstep, right block-Jacobi, stop at ||b - A u|| <= tol ||b||; a
+        frequency that misses tol within max_iter is solved by LU instead)."""
         k = {"lu": 0, "gmres": 1}[kind]
         _check(lib().fds_bem_set_solver(self._h, k, ctypes.c_double(tol), int(restart), int(max_iter)))
 
     def last_gmres(self):
-        it, res = ctypes.c_int(), ctypes.c_double()
-        _check(lib().fds_bem_last_gmres(self._h, ctypes.byref(it), ctypes.byref(res)))
-        return dict(iterations=it.value, rel_residual=res.value)
+        it, res, fb = ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+        _check(lib().fds_bem_last_gmres(self._h, ctypes.byref(it), ctypes.byref(res), ctypes.byref(fb)))
+        return dict(iterations=it.value, rel_residual=res.value, lu_fallbacks=fb.value)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -90,6 +90,7 @@ struct fds_bem {
     GmresWorkspace gws;
     int gm_iters = 0;
     double gm_resid = 0.0;
+    int gm_fallbacks = 0;
     cudaEvent_t ev[4] = {};
     double t_asm = 0, t_lu = 0, t_solve = 0;
     int launches = 0;
@@ -145,9 +146,26 @@ struct fds_bem {
             FDS_CUDA(cudaMemsetAsync(info, 0, B * sizeof(int), st));
             gm_iters = 0;
             gm_resid = 0.0;
-            for (const GmresStats& gs : gmres_solve_batch(A, mstride, plane, n, ld, B, rhs, ld, gp, gws, st)) {
-                gm_iters = std::max(gm_iters, gs.iterations);
-                gm_resid = std::max(gm_resid, gs.rel_residual);
+            gm_fallbacks = 0;
+            const std::vector<GmresStats> gst = gmres_solve_batch(A, mstride, plane, n, ld, B, rhs, ld, gp, gws, st);
+            for (int b = 0; b < B; ++b) {
+                gm_iters = std::max(gm_iters, gst[b].iterations);
+                if (gst[b].converged) {
+                    gm_resid = std::max(gm_resid, gst[b].rel_residual);
+                    continue;
+                }
+                // GMRES stagnated (e.g. near an interior resonance of the cavity): this
+                // frequency is solved by the LU path instead, from its saved right-hand side
+                ++gm_fallbacks;
+                FDS_CUDA(cudaMemcpyAsync(rhs + static_cast<size_t>(b) * ld, gws.bsave + 2 * static_cast<size_t>(b) * n,
+                                         n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+                LuProblem one = pb;
+                one.A = A + static_cast<size_t>(b) * mstride;
+                one.batch = 1;
+                one.ipiv = ipiv + static_cast<size_t>(b) * n;
+                one.info = info + b;
+                lu_factor(one, ws, st);
+                lu_solve(one, rhs + static_cast<size_t>(b) * ld, ld, st);
             }
             FDS_CUDA(cudaEventRecord(ev[2], st));
         } else {
@@ -378,11 +396,12 @@ int fds_bem_set_solver(fds_bem* h, int kind, double tol, int restart, int max_it
     });
 }
 
-int fds_bem_last_gmres(const fds_bem* h, int* iterations, double* rel_residual) {
+int fds_bem_last_gmres(const fds_bem* h, int* iterations, double* rel_residual, int* lu_fallbacks) {
     return fds_guard([&] {
         if (!h) throw ValidationError("fds_bem_last_gmres: null handle");
         if (iterations) *iterations = h->gm_iters;
         if (rel_residual) *rel_residual = h->gm_resid;
+        if (lu_fallbacks) *lu_fallbacks = h->gm_fallbacks;
     });
 }
 

@@ -285,6 +285,7 @@ int fds_run_afs_bem(fds_bem* bem, const fds_afs_config* cfg, int cap, fds_c64* s
                                                   static_cast<int>(s.size()), reinterpret_cast<fds_c64*>(out.data()));
             if (rc == FDS_ENUMERIC) throw NumericError(fds_last_error());
             if (rc == FDS_EVALIDATION) throw ValidationError(fds_last_error());
+            if (rc == FDS_ECONVERGENCE) throw ConvergenceError(fds_last_error());
             if (rc != FDS_OK) throw CudaError(fds_last_error());
         };
         const AfsOut r = run_afs_impl(eval, K, cfg_of(cfg));

@@ -364,12 +364,19 @@ std::vector<GmresStats> gmres_solve_batch(const double* A, size_t mstride, size_
         if (bnorm[b] > 0.0) live.push_back(b);
     std::vector<Cx> h, h2, coef;
     std::vector<double> hn, sc;
+    std::vector<double> prev(B, 1.0);  // relative residual at the start of the previous cycle
+    bool first = true;
     while (true) {
         std::vector<int> act;  // systems that still need a cycle
         for (int b : live) {
             stats[b].rel_residual = beta[b] / bnorm[b];
-            if (stats[b].rel_residual > p.tol && stats[b].iterations < p.max_iter) act.push_back(b);
+            // a full restart cycle that did not halve the residual is stagnation
+            // (e.g. near an interior resonance): give up early, the caller falls back
+            const bool stalled = !first && stats[b].rel_residual > 0.5 * prev[b];
+            prev[b] = stats[b].rel_residual;
+            if (stats[b].rel_residual > p.tol && stats[b].iterations < p.max_iter && !stalled) act.push_back(b);
         }
+        first = false;
         live = act;
         if (live.empty()) break;
         // new cycle: V_b0 = r_b / beta_b
@@ -445,18 +452,18 @@ std::vector<GmresStats> gmres_solve_batch(const double* A, size_t mstride, size_
         op.norms(w, hn);
         for (size_t a = 0; a < live.size(); ++a) beta[live[a]] = hn[a];
     }
-    for (int b = 0; b < B; ++b)
-        if (!(stats[b].rel_residual <= p.tol))
-            throw ConvergenceError("gmres: relative residual " + std::to_string(stats[b].rel_residual) + " after " +
-                                   std::to_string(stats[b].iterations) + " iterations (system " + std::to_string(b) +
-                                   ")");
+    for (int b = 0; b < B; ++b) stats[b].converged = stats[b].rel_residual <= p.tol;
     return stats;
 }
 
 GmresStats gmres_solve(const double* Are, const double* Aim, int n, int ld, cplx* b, const GmresParams& p,
                        GmresWorkspace& ws, cudaStream_t st) {
     const size_t plane = static_cast<size_t>(Aim - Are);
-    return gmres_solve_batch(Are, 2 * plane, plane, n, ld, 1, b, static_cast<size_t>(n), p, ws, st)[0];
+    const GmresStats r = gmres_solve_batch(Are, 2 * plane, plane, n, ld, 1, b, static_cast<size_t>(n), p, ws, st)[0];
+    if (!r.converged)
+        throw ConvergenceError("gmres: relative residual " + std::to_string(r.rel_residual) + " after " +
+                               std::to_string(r.iterations) + " iterations");
+    return r;
 }
 
 }  // namespace fdsb

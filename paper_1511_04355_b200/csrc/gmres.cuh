@@ -18,6 +18,7 @@ struct GmresParams {
 struct GmresStats {
     int iterations = 0;
     double rel_residual = 0.0;  // true residual of the returned x
+    bool converged = false;
 };
 
 struct GmresWorkspace {
@@ -48,7 +49,8 @@ struct GmresWorkspace {
 // diagonal blocks (one per element, DOF-major u[3e+i]); n % 3 == 0. The systems
 // iterate in lockstep, each leaving the Arnoldi loop at its own tolerance.
 // Deterministic: every reduction has a fixed order, so equal inputs give
-// bit-identical x. Throws ConvergenceError if a system misses tol within max_iter.
+// bit-identical x. A system that misses tol within max_iter is reported with
+// converged = false (its original right-hand side stays in ws.bsave).
 std::vector<GmresStats> gmres_solve_batch(const double* A, size_t mstride, size_t plane, int n, int ld, int B,
                                           cplx* rhs, size_t rstride, const GmresParams& p, GmresWorkspace& ws,
                                           cudaStream_t st);

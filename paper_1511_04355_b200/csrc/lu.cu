@@ -515,7 +515,9 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
             for (int e = 0; e < 2; ++e) {
                 const int col = n0 + wn * (GBN / GWN) + ni * 8 + 2 * (lane & 3) + e;
                 const size_t gi = static_cast<size_t>(col) * ld + row;
-                const bool in = col < c1;  // column window [c0, c1) (sub-panel updates stop at the panel edge)
+                // column window [c0, c1) (sub-panel updates stop at the panel edge); rows of a
+                // sub-panel window's last tile can pass n (and ld): never read past the matrix
+                const bool in = col < c1 && row < n;
                 acr[mi][ni][e] = in ? Are[gi] : 0.0;
                 aci[mi][ni][e] = in ? Aim[gi] : 0.0;
             }

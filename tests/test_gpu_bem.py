@@ -143,3 +143,22 @@ def test_cluster_and_global_panels_identical(tmp_path):
     for tag, env in (("c", {}), ("g", {"FDSWEEP_PANEL_CLUSTER": "0"})):
         subprocess.run([sys.executable, "-c", code, tag], cwd=root, env=dict(os.environ, **env), check=True)
     assert np.array_equal(np.load(tmp_path / "xc.npy"), np.load(tmp_path / "xg.npy"))
+
+
+def test_handle_reuse_after_close():
+    """Regression: a second handle allocated where a closed one lived (sub-panel
+    GEMM windows once read past the matrix end there)."""
+    from paper_1511_04355_b200 import BemSystem, mesh
+
+    V, F = mesh.icosphere(3)
+    tr = mesh.random_traction(F.shape[0], seed=0)
+    s = 0.25 + 1j * np.linspace(0.0, 40.0, 12)
+    h1 = BemSystem(V, F, tr, channels=list(range(48)))
+    u1 = h1.evaluate_batch(s)
+    h1.evaluate(s[3])
+    h1.close()
+    h2 = BemSystem(V, F, tr)
+    u2 = h2.evaluate_batch(s)
+    np.testing.assert_array_equal(u2[:, :48], u1)
+    h2.evaluate(s[3])
+    h2.close()
