@@ -155,7 +155,16 @@ AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
     std::vector<double> e1_grid(cfg.time_points);
     for (int i = 0; i < cfg.time_points; ++i) e1_grid[i] = cfg.period * i / (cfg.time_points - 1);
 
-    std::optional<std::vector<double>> prev;
+    // E1 series of the test channels stay in HBM (current and previous fit),
+    // only the per-channel ratios cross to the host
+    auto& vcx = VfContext::get();
+    double* ser[2] = {nullptr, nullptr};
+    struct Free {
+        double** p;
+        ~Free() { for (int i = 0; i < 2; ++i) if (p[i]) cudaFree(p[i]); }
+    } free_ser{ser};
+    bool have_prev = false;
+    int cur_slot = 0;
     int streak = 0;
     std::vector<Cx> ph;
     std::vector<Cx> rh_all;
@@ -179,10 +188,16 @@ AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
         std::vector<Cx> r_test(static_cast<size_t>(KT) * MH);
         for (int q = 0; q < KT; ++q)
             std::copy_n(r_h.begin() + static_cast<size_t>(test_pos[q]) * MH, MH, r_test.begin() + static_cast<size_t>(q) * MH);
-        std::vector<double> series(static_cast<size_t>(KT) * e1_grid.size());
-        rat_invert_host(p_h, r_test, KT, e1_grid, series.data());
-        const double e1 = prev ? afs_error_e1(e1_grid, series, *prev, KT) : std::numeric_limits<double>::infinity();
-        prev = std::move(series);
+        if (!ser[0]) {
+            const size_t bytes = static_cast<size_t>(KT) * e1_grid.size() * sizeof(double);
+            FDS_CUDA(cudaMalloc(&ser[0], bytes));
+            FDS_CUDA(cudaMalloc(&ser[1], bytes));
+        }
+        rat_invert_to_device(p_h, r_test, KT, e1_grid, ser[cur_slot], vcx.st);
+        const double e1 = have_prev ? afs_error_e1_device(e1_grid, ser[cur_slot], ser[cur_slot ^ 1], KT, vcx.st)
+                                    : std::numeric_limits<double>::infinity();
+        have_prev = true;
+        cur_slot ^= 1;
         r.history.push_back({J, MH, ML, false, Cx(0, 0), e1, e2});
         ph = p_h;
         rh_all = r_h;

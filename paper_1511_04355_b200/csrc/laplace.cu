@@ -665,8 +665,8 @@ void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int
     profiler().end(st, pe, kProfRatInv, 2.0 * (2.0 * nt) * T * static_cast<double>(K));
 }
 
-void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K, const std::vector<double>& t,
-                     double* out) {
+void rat_invert_to_device(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K,
+                          const std::vector<double>& t, double* out_dev, cudaStream_t st) {
     // laplace.cpp:127-164 validation
     if (t.empty()) throw ValidationError("rational_invert: empty time grid");
     for (size_t i = 1; i < t.size(); ++i)
@@ -696,11 +696,68 @@ void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km
         for (int m = 0; m < M; ++m) rmk[static_cast<size_t>(m) * K + k] = res_km[static_cast<size_t>(k) * M + m];
     auto& cx = VfContext::get();
     cplx* dres = vdev<cplx>(cx.resid, rmk.size() + 1);
+    FDS_CUDA(cudaMemcpyAsync(dres, rmk.data(), rmk.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    rat_invert_device(poles, dres, K, t, out_dev, paired, st);
+    // rmk is a host temporary read by the async copy above
+    FDS_CUDA(cudaStreamSynchronize(st));
+}
+
+void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K, const std::vector<double>& t,
+                     double* out) {
+    auto& cx = VfContext::get();
+    const size_t T = t.size();
+    if (K == 0 || T == 0) {
+        rat_invert_to_device(poles, res_km, K, t, nullptr, cx.st);  // validation only
+        return;
+    }
     double* dout = vdev<double>(cx.out, static_cast<size_t>(K) * T);
-    FDS_CUDA(cudaMemcpyAsync(dres, rmk.data(), rmk.size() * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
-    rat_invert_device(poles, dres, K, t, dout, paired, cx.st);
+    rat_invert_to_device(poles, res_km, K, t, dout, cx.st);
     FDS_CUDA(cudaMemcpyAsync(out, dout, static_cast<size_t>(K) * T * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
     FDS_CUDA(cudaStreamSynchronize(cx.st));
+}
+
+// error_e1 (afs.cpp:189-216) on device-resident series: one thread per channel
+// runs the trapezoid sums in the reference's order with round-to-nearest
+// intrinsics (no FMA contraction), so each ratio is bit-identical to the host's.
+__global__ void afs_e1_kernel(const double* __restrict__ cur, const double* __restrict__ prev,
+                              const double* __restrict__ t, int K, int T, double* __restrict__ ratio) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const double* a = cur + static_cast<size_t>(k) * T;
+    const double* b = prev + static_cast<size_t>(k) * T;
+    double num = 0.0, den = 0.0;
+    double d0 = __dsub_rn(a[0], b[0]);
+    double dd_prev = __dmul_rn(d0, d0), cc_prev = __dmul_rn(a[0], a[0]);
+    for (int i = 1; i < T; ++i) {
+        const double w = __dmul_rn(0.5, __dsub_rn(t[i], t[i - 1]));
+        const double d = __dsub_rn(a[i], b[i]);
+        const double dd = __dmul_rn(d, d), cc = __dmul_rn(a[i], a[i]);
+        num = __dadd_rn(num, __dmul_rn(w, __dadd_rn(dd, dd_prev)));
+        den = __dadd_rn(den, __dmul_rn(w, __dadd_rn(cc, cc_prev)));
+        dd_prev = dd;
+        cc_prev = cc;
+    }
+    ratio[k] = den == 0.0 ? -1.0 : __ddiv_rn(num, den);  // -1 flags zero energy
+}
+
+double afs_error_e1_device(const std::vector<double>& t, const double* cur_dev, const double* prev_dev, int K,
+                           cudaStream_t st) {
+    if (K == 0) throw ValidationError("error_e1: no channels");
+    auto& cx = VfContext::get();
+    const int T = static_cast<int>(t.size());
+    double* dt = vdev<double>(cx.misc2, static_cast<size_t>(T) + K + 1);
+    double* dr = dt + T;
+    FDS_CUDA(cudaMemcpyAsync(dt, t.data(), T * sizeof(double), cudaMemcpyHostToDevice, st));
+    FDS_LAUNCH(afs_e1_kernel, ceil_div(K, 128), 128, 0, st, cur_dev, prev_dev, dt, K, T, dr);
+    std::vector<double> r(K);
+    FDS_CUDA(cudaMemcpyAsync(r.data(), dr, K * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FDS_CUDA(cudaStreamSynchronize(st));
+    double worst = 0.0;
+    for (int k = 0; k < K; ++k) {
+        if (r[k] < 0.0) throw NumericError("error_e1: test channel " + std::to_string(k) + " has zero energy");
+        worst = std::max(worst, r[k]);
+    }
+    return worst;
 }
 
 // N_s = 512 uses the Stockham kernel unless FDSWEEP_FSM=shuffle selects the

@@ -69,6 +69,12 @@ Cx vf_select_new_frequency(const std::vector<Cx>& ph, const std::vector<Cx>& rh,
 // rational_invert (laplace.cpp:127-164): host model -> host out[k][t].
 void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K,
                      const std::vector<double>& t, double* out);
+// host model -> series left in HBM (out_dev, [k][t]).
+void rat_invert_to_device(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K,
+                          const std::vector<double>& t, double* out_dev, cudaStream_t st);
+// error_e1 (afs.cpp:189-216) of two device-resident series [k][t]; bit-identical to the host sums.
+double afs_error_e1_device(const std::vector<double>& t, const double* cur_dev, const double* prev_dev, int K,
+                           cudaStream_t st);
 // device variant: residues on device [m][k]; paired = residues exactly conjugate per pair.
 void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int K, const std::vector<double>& t,
                        double* out_dev, bool paired, cudaStream_t st);
