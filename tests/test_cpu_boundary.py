@@ -40,9 +40,11 @@ def test_library_built_for_sm100a():
     assert "sm_100a" in out.stdout
 
 
-def test_library_has_dmma_sass():
+def test_library_has_dmma_tma_and_cluster_sass():
     out = subprocess.run(["cuobjdump", "-sass", str(P.library_path())], capture_output=True, text=True).stdout
-    assert "DMMA" in out  # LU trailing GEMM and rational inversion on the FP64 tensor pipe
+    assert "DMMA" in out  # LU trailing GEMM, TRSM, residues, rational inversion on the FP64 tensor pipe
+    assert "UTMALDG" in out  # TMA-fed trailing GEMM (cp.async.bulk.tensor)
+    assert "UCGABAR_ARV" in out and "UCGABAR_WAIT" in out  # cluster barrier of the DSMEM pivot exchange
 
 
 def test_no_gpu_fails_loudly():
