@@ -463,7 +463,7 @@ int fds_lu_factor_device(int n, int B, double* A_planar, int* ipiv, int* info, d
         pb.batch = B;
         pb.ipiv = ipiv;
         pb.info = info;
-        static LuWorkspace ws;
+        static thread_local LuWorkspace ws;
         cudaEvent_t e0, e1;
         FDS_CUDA(cudaEventCreate(&e0));
         FDS_CUDA(cudaEventCreate(&e1));

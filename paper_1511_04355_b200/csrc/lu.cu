@@ -1253,6 +1253,15 @@ void LuWorkspace::ensure(int groups, int P, int nb) {
     }
 }
 
+void LuWorkspace::ensure_side() {
+    if (side) return;
+    int lo = 0, hi = 0;
+    FDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FDS_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+    FDS_CUDA(cudaStreamCreateWithPriority(&side_lo, cudaStreamNonBlocking, lo));
+    for (auto& e : ev) FDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 double* LuWorkspace::linv(int batch) {
     if (batch > linv_cap) {
         if (linv_buf) cudaFree(linv_buf);
@@ -1277,6 +1286,15 @@ void LuWorkspace::release() {
     if (counters) cudaFree(counters);
     slots = nullptr;
     counters = nullptr;
+    if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+    }
+    if (side_lo) cudaStreamDestroy(side_lo);
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    side = side_lo = nullptr;
+    for (auto& e : ev) e = nullptr;
     slot_bytes = 0;
     counter_count = 0;
 }
@@ -1588,15 +1606,9 @@ bool use_pipeline(const LuProblem& pb) {
 // trailing GEMM occupies the tensor pipes on a low-priority stream, so the
 // latency-bound panel work hides behind the compute-bound GEMM.
 void lu_factor_pipelined(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
-    static cudaStream_t s_hi = nullptr, s_lo = nullptr;
-    static cudaEvent_t ev[8];
-    if (!s_hi) {
-        int lo = 0, hi = 0;
-        FDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        FDS_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, hi));
-        FDS_CUDA(cudaStreamCreateWithPriority(&s_lo, cudaStreamNonBlocking, lo));
-        for (auto& e : ev) FDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    ws.ensure_side();
+    cudaStream_t s_hi = ws.side, s_lo = ws.side_lo;
+    cudaEvent_t* ev = ws.ev;
     cudaEvent_t ev_start = ev[0], ev_hi_end = ev[1], ev_lo_end = ev[2];
     cudaEvent_t ev_trsm[2] = {ev[3], ev[4]}, ev_gemm[2] = {ev[5], ev[6]};
     const int b0 = pb.batch / 2;
@@ -1653,15 +1665,9 @@ bool use_lookahead(const LuProblem& pb) {
 // latency-bound column steps hide behind the tensor-pipe work. The next
 // step's swap+TRSM waits for both (same stream order as the serial schedule).
 void lu_factor_lookahead(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
-    static cudaStream_t s_hi = nullptr;
-    static cudaEvent_t ev_a = nullptr, ev_p = nullptr;
-    if (!s_hi) {
-        int lo = 0, hi = 0;
-        FDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        FDS_CUDA(cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, hi));
-        FDS_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
-        FDS_CUDA(cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming));
-    }
+    ws.ensure_side();
+    cudaStream_t s_hi = ws.side;
+    cudaEvent_t ev_a = ws.ev[0], ev_p = ws.ev[1];
     double* linv = ws.linv(pb.batch);
     subpanel_block(pb, ws, 0, 64, st, true);
     for (int k = 0; k < pb.n; k += 64) {

@@ -35,6 +35,11 @@ struct CaluWorkspace {
 
 struct LuWorkspace {
     CaluWorkspace calu;
+    // side stream + events of the look-ahead / pipelined schedules (per
+    // workspace, so concurrent handles never share them)
+    cudaStream_t side = nullptr, side_lo = nullptr;
+    cudaEvent_t ev[8] = {};
+    void ensure_side();
     double* linv_buf = nullptr;  // [batch][2][64][64] L11^{-1} per panel
     int linv_cap = 0;
     double* linv(int batch);
@@ -44,6 +49,10 @@ struct LuWorkspace {
     int counter_count = 0;
     void ensure(int groups, int P, int nb);
     void release();
+    LuWorkspace() = default;
+    LuWorkspace(const LuWorkspace&) = delete;
+    LuWorkspace& operator=(const LuWorkspace&) = delete;
+    ~LuWorkspace() { release(); }
 };
 
 inline int lu_ld(int n) { return (n + 63) / 64 * 64; }
