@@ -162,3 +162,35 @@ def test_handle_reuse_after_close():
     np.testing.assert_array_equal(u2[:, :48], u1)
     h2.evaluate(s[3])
     h2.close()
+
+
+def test_concurrent_handles_and_shared_handle():
+    """Reentrancy: two handles solving at the same time from two
+    threads, and two threads sharing one handle, give the sequential results."""
+    import threading
+
+    from paper_1511_04355_b200 import BemSystem, mesh
+
+    V, F = mesh.icosphere(2)
+    tr = mesh.random_traction(F.shape[0], seed=2)
+    s1 = 0.25 + 1j * np.linspace(0.0, 30.0, 9)
+    s2 = 0.3 + 1j * np.linspace(1.0, 20.0, 5)
+    ref = BemSystem(V, F, tr)
+    r1, r2 = ref.evaluate_batch(s1), ref.evaluate_batch(s2)
+    r3 = ref.evaluate(0.25 + 5j)
+    ha, hb = BemSystem(V, F, tr), BemSystem(V, F, tr)
+    out = {}
+
+    def work(key, h, s):
+        for _ in range(3):
+            out[key] = h.evaluate_batch(s)
+
+    ts = [threading.Thread(target=work, args=("a", ha, s1)), threading.Thread(target=work, args=("b", hb, s2)),
+          threading.Thread(target=lambda: out.__setitem__("c", ha.evaluate(0.25 + 5j)))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    np.testing.assert_array_equal(out["a"], r1)
+    np.testing.assert_array_equal(out["b"], r2)
+    np.testing.assert_array_equal(out["c"], r3)
