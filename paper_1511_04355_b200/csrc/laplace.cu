@@ -509,9 +509,13 @@ __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
+// QS > 0: the term count padded to 4 is known at compile time (fully unrolled
+// DMMA k-loop); QS = 0: runtime Q.
+template <int QS>
 __global__ void __launch_bounds__(256)
-rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, const double* __restrict__ term_w,
+rat_invert_kernel(int K, int T, int Qrt, int nt, const int* __restrict__ term_m, const double* __restrict__ term_w,
                   const cplx* __restrict__ res /*[m][K]*/, const double* __restrict__ E, double* __restrict__ out) {
+    const int Q = QS > 0 ? QS : Qrt;
     extern __shared__ __align__(16) double rsm[];
     double* As = rsm;                 // [Q][RS]  (q, channel)
     double* Bs0 = rsm + Q * RS;       // [Q][RS]  (q, time) x 2 buffers
@@ -557,7 +561,8 @@ rat_invert_kernel(int K, int T, int Q, int nt, const int* __restrict__ term_m, c
         }
         __syncthreads();
         double acc[4][2][2] = {};
-        for (int q0 = 0; q0 < Q; q0 += 4) {
+#pragma unroll
+        for (int q0 = 0; q0 < (QS > 0 ? QS : Qrt); q0 += 4) {
             const int q = q0 + (lane & 3);
             double fa[4], fb[2];
 #pragma unroll
@@ -651,16 +656,25 @@ void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int
     FDS_LAUNCH(rat_table_kernel, ceil_div(Q * T, 256), 256, 0, st, Q, nt, T, dtp, dt, dE);
     const size_t smem = 3 * static_cast<size_t>(Q) * RS * sizeof(double);
     if (smem > device_info().smem_optin - 1024) throw ValidationError("rational_invert: model order too large");
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        FDS_CUDA(cudaFuncSetAttribute(rat_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        attr = smem;
-    }
+    auto go = [&](auto kern) {
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            attr = smem;
+        }
+        return kern;
+    };
     dim3 g(ceil_div(K, RBM));
     cudaEvent_t pe;
     profiler().begin(st, kProfRatInv, 0.0, pe);
-    FDS_LAUNCH(rat_invert_kernel, g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev);
+    // common model orders get a compile-time k-loop
+    switch (Q) {
+        case 16: FDS_LAUNCH(go(rat_invert_kernel<16>), g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev); break;
+        case 32: FDS_LAUNCH(go(rat_invert_kernel<32>), g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev); break;
+        case 48: FDS_LAUNCH(go(rat_invert_kernel<48>), g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev); break;
+        case 64: FDS_LAUNCH(go(rat_invert_kernel<64>), g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev); break;
+        default: FDS_LAUNCH(go(rat_invert_kernel<0>), g, 256, smem, st, K, T, Q, nt, dtm, dtw, res_mk_dev, dE, out_dev); break;
+    }
     // algorithmic FP64 work: 2 * Q * T per channel (2*M*T for M/2 pairs)
     profiler().end(st, pe, kProfRatInv, 2.0 * (2.0 * nt) * T * static_cast<double>(K));
 }
