@@ -3,6 +3,7 @@
 // (proj/include/fdsweep/systems.hpp:34-42) with a CUDA path; there is no CPU
 // fallback — every entry point fails with FDS_ECUDA if the device path fails.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -125,6 +126,13 @@ struct fds_bem {
 
     // Solves B frequencies already in svec_host; result (B x K) left in `out` on device.
     void run(const fds_c64* s_host, int B) {
+        for (int b = 0; b < B; ++b) {
+            const fds_c64 z = s_host[b];
+            if (!std::isfinite(z.re) || !std::isfinite(z.im))
+                throw ValidationError("bem: contour frequency must be finite");
+            if (z.re == 0.0 && z.im == 0.0)
+                throw ValidationError("bem: s = 0 is the pole of the Heaviside load p(s) = 1/s");
+        }
         launches = 0;
         t_asm = t_lu = t_solve = 0;
         const int64_t l0 = g_launches.load();

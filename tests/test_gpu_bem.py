@@ -194,3 +194,16 @@ def test_concurrent_handles_and_shared_handle():
     np.testing.assert_array_equal(out["a"], r1)
     np.testing.assert_array_equal(out["b"], r2)
     np.testing.assert_array_equal(out["c"], r3)
+
+
+def test_invalid_frequencies_rejected():
+    from paper_1511_04355_b200 import BemSystem, ValidationError, mesh
+
+    V, F = mesh.icosphere(1)
+    h = BemSystem(V, F, mesh.pressure_traction(V, F))
+    for bad in (0.0, complex(float("nan"), 1.0), complex(0.25, float("inf"))):
+        with pytest.raises(ValidationError):
+            h.evaluate(bad)
+    with pytest.raises(ValidationError):
+        h.evaluate_batch(np.array([0.25 + 1j, 0.0]))
+    assert np.all(np.isfinite(h.evaluate(0.25 + 1j)))  # handle still usable
