@@ -183,6 +183,12 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU leg
+# FP64 flops per far-field kernel evaluation: 32 x (2 DFMA + DMUL + DADD) warp
+# instructions of bem_far_kernel (ncu sass__inst_executed_per_opcode on cfg2)
+# divided by its 7 N_e (N_e - 1) B evaluations (profiles/r01_assembly_ncu_full.json).
+ASM_FLOPS_PER_EVAL = 439.0
+
+
 def run_ours(args, world, rank, local, dist):
     import paper_1511_04355_b200 as P
     from paper_1511_04355_b200 import BemSystem
@@ -231,6 +237,8 @@ def run_ours(args, world, rank, local, dist):
     panel = dict(launches=c.value, ms=ms.value)
     P.api._check(L.fds_profile_read(2, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
     trsm = dict(launches=c.value, ms=ms.value)
+    P.api._check(L.fds_profile_read(3, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
+    far = dict(ms=ms.value, evaluations=wk.value)
     P.api._check(L.fds_profile_enable(0))
     peak, peak_src = measured_fp64_peak()
     achieved = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
@@ -254,6 +262,12 @@ def run_ours(args, world, rank, local, dist):
         "stages_ms": {"assembly": stage["assembly_ms"], "lu": stage["lu_ms"], "solve": stage["solve_ms"],
                       "lu_panel": panel["ms"], "lu_trsm": trsm["ms"], "lu_gemm": gemm["ms"]},
         "lu_tflops": lu_flops / (stage["lu_ms"] * 1e-3) / 1e12,
+        # assembly far field: kernel evaluations x a per-evaluation FP64 flop
+        # constant taken from the kernel's SASS op counts (DFMA = 2), profiles/r01_assembly_ncu_full.json
+        "assembly_far": {"ms": far["ms"], "kernel_evaluations": far["evaluations"],
+                         "flops_per_evaluation": ASM_FLOPS_PER_EVAL,
+                         "tflops": ASM_FLOPS_PER_EVAL * far["evaluations"] / max(far["ms"], 1e-9) / 1e9,
+                         "fp64_frac": ASM_FLOPS_PER_EVAL * far["evaluations"] / max(far["ms"], 1e-9) / 1e9 / peak},
         "wall_ms_per_step": wall * 1e3 / args.steps,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
