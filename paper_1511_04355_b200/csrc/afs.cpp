@@ -37,6 +37,27 @@ void validate(const AfsCfg& c) {  // afs.cpp:59-84
     if (c.n_relocations < 1) throw ValidationError("afs: n_relocations must be >= 1");
 }
 
+// growable device allocation owned by one run_afs call (contents not kept on growth)
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { if (p) cudaFree(p); }
+    template <class T>
+    T* get(size_t count) {
+        const size_t need = std::max<size_t>(count, 1) * sizeof(T);
+        if (need > bytes) {
+            if (p) FDS_CUDA(cudaFree(p));
+            p = nullptr;
+            FDS_CUDA(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return static_cast<T*>(p);
+    }
+};
+
 }  // namespace
 
 std::vector<int> draw_channels(int n, int k, uint64_t seed) {  // afs.cpp:28-46
@@ -155,52 +176,84 @@ AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
     std::vector<double> e1_grid(cfg.time_points);
     for (int i = 0; i < cfg.time_points; ++i) e1_grid[i] = cfg.period * i / (cfg.time_points - 1);
 
-    // E1 series of the test channels stay in HBM (current and previous fit),
-    // only the per-channel ratios cross to the host
+    // GPU-resident iteration: the fit-channel samples,
+    // both models' residues, the channel errors and the E1 series stay in HBM.
+    // Per iteration only the new sample row goes up; E2, the worst ORF channel,
+    // the per-channel E1 ratios and the selected grid index come back.
     auto& vcx = VfContext::get();
-    double* ser[2] = {nullptr, nullptr};
-    struct Free {
-        double** p;
-        ~Free() { for (int i = 0; i < 2; ++i) if (p[i]) cudaFree(p[i]); }
-    } free_ser{ser};
+    const cudaStream_t st = vcx.st;
+    DevMem samp[2], res_h, res_l, res_t, ce, pos, red, ser[2];
+    int samp_cur = 0, jcap = 0, j_dev = 0;
+    const bool test_all = static_cast<int>(test_pos.size()) == KF &&
+                          std::is_sorted(test_pos.begin(), test_pos.end()) && (KF == 0 || test_pos.back() == KF - 1);
+    const int KT = static_cast<int>(test_pos.size()), KO = static_cast<int>(orf_pos.size());
+    int* dtest = pos.get<int>(static_cast<size_t>(KT) + KO);
+    int* dorf = dtest + KT;
+    FDS_CUDA(cudaMemcpyAsync(dtest, test_pos.data(), KT * sizeof(int), cudaMemcpyHostToDevice, st));
+    FDS_CUDA(cudaMemcpyAsync(dorf, orf_pos.data(), KO * sizeof(int), cudaMemcpyHostToDevice, st));
+    double* dce = ce.get<double>(2 * static_cast<size_t>(KF));
+    AfsErrReduce* dred = red.get<AfsErrReduce>(1);
+    auto upload_samples = [&]() {  // append rows j_dev..J-1 of the fit channels
+        const int J = static_cast<int>(r.samples.size());
+        if (J > jcap) {
+            const int cap = std::max(2 * jcap, J + 8);
+            cplx* dst = samp[samp_cur ^ 1].get<cplx>(static_cast<size_t>(cap) * KF);
+            if (j_dev > 0)
+                FDS_CUDA(cudaMemcpyAsync(dst, samp[samp_cur].p, sizeof(cplx) * j_dev * static_cast<size_t>(KF),
+                                         cudaMemcpyDeviceToDevice, st));
+            samp_cur ^= 1;
+            jcap = cap;
+        }
+        std::vector<Cx> rows(static_cast<size_t>(J - j_dev) * KF);
+        for (int j = j_dev; j < J; ++j)
+            for (int q = 0; q < KF; ++q)
+                rows[static_cast<size_t>(j - j_dev) * KF + q] = r.values[static_cast<size_t>(j) * channels + fitc[q]];
+        FDS_CUDA(cudaMemcpyAsync(static_cast<cplx*>(samp[samp_cur].p) + static_cast<size_t>(j_dev) * KF, rows.data(),
+                                 rows.size() * sizeof(Cx), cudaMemcpyHostToDevice, st));
+        FDS_CUDA(cudaStreamSynchronize(st));  // rows is a host temporary
+        j_dev = J;
+    };
     bool have_prev = false;
     int cur_slot = 0;
     int streak = 0;
     std::vector<Cx> ph;
-    std::vector<Cx> rh_all;
     while (true) {  // afs.cpp:323-377
         if (static_cast<int>(r.history.size()) >= cfg.max_iterations)
             throw ConvergenceError("afs: no convergence within max_iterations");
         const int J = static_cast<int>(r.samples.size());
         const auto [MH, ML] = afs_fit_orders(J, cfg.alpha_high, cfg.alpha_low);
-        std::vector<Cx> restricted(static_cast<size_t>(J) * KF);
+        upload_samples();
+        const cplx* dsamp = static_cast<const cplx*>(samp[samp_cur].p);
+        std::vector<Cx> ov(static_cast<size_t>(J) * KO);  // ORF samples for the host relocation step
         for (int j = 0; j < J; ++j)
-            for (int q = 0; q < KF; ++q)
-                restricted[static_cast<size_t>(j) * KF + q] = r.values[static_cast<size_t>(j) * channels + fitc[q]];
-        std::vector<Cx> p_h, r_h, p_l, r_l;
-        vf_vector_fit(r.samples, restricted.data(), KF, orf_pos, MH, cfg.n_relocations, p_h, r_h, nullptr);
-        vf_vector_fit(r.samples, restricted.data(), KF, orf_pos, ML, cfg.n_relocations, p_l, r_l, nullptr);
-        const std::vector<double> errors = vf_channel_errors(p_h, r_h, p_l, r_l, KF, grid);
-        double e2 = -std::numeric_limits<double>::infinity();
+            for (int q = 0; q < KO; ++q) ov[static_cast<size_t>(j) * KO + q] = r.values[static_cast<size_t>(j) * channels + r.orf[q]];
+        cplx* drh = res_h.get<cplx>(static_cast<size_t>(MH) * KF);
+        cplx* drl = res_l.get<cplx>(static_cast<size_t>(ML) * KF);
+        const std::vector<Cx> p_h = vf_vector_fit_device(r.samples, ov.data(), dsamp, KF, orf_pos, MH, cfg.n_relocations, drh, st);
+        const std::vector<Cx> p_l = vf_vector_fit_device(r.samples, ov.data(), dsamp, KF, orf_pos, ML, cfg.n_relocations, drl, st);
+        vf_channel_errors_device(p_h, drh, p_l, drl, KF, grid, dtest, KT, dorf, KO, dce, dred, st);
+        AfsErrReduce er;
+        FDS_CUDA(cudaMemcpyAsync(&er, dred, sizeof(er), cudaMemcpyDeviceToHost, st));
+        FDS_CUDA(cudaStreamSynchronize(st));
+        if (er.zero_k >= 0)
+            throw NumericError("channel_errors: channel " + std::to_string(er.zero_k) +
+                               " has identically zero high-order fit");
         if (test_pos.empty()) throw ValidationError("error_e2: no test channels");
-        for (int p : test_pos) e2 = std::max(e2, errors[p]);
-        const int KT = static_cast<int>(test_pos.size());
-        std::vector<Cx> r_test(static_cast<size_t>(KT) * MH);
-        for (int q = 0; q < KT; ++q)
-            std::copy_n(r_h.begin() + static_cast<size_t>(test_pos[q]) * MH, MH, r_test.begin() + static_cast<size_t>(q) * MH);
-        if (!ser[0]) {
-            const size_t bytes = static_cast<size_t>(KT) * e1_grid.size() * sizeof(double);
-            FDS_CUDA(cudaMalloc(&ser[0], bytes));
-            FDS_CUDA(cudaMalloc(&ser[1], bytes));
+        const double e2 = er.e2;
+        const cplx* drt = drh;
+        if (!test_all) {
+            cplx* g = res_t.get<cplx>(static_cast<size_t>(MH) * KT);
+            vf_gather_channels(drh, KF, MH, dtest, KT, g, st);
+            drt = g;
         }
-        rat_invert_to_device(p_h, r_test, KT, e1_grid, ser[cur_slot], vcx.st);
-        const double e1 = have_prev ? afs_error_e1_device(e1_grid, ser[cur_slot], ser[cur_slot ^ 1], KT, vcx.st)
+        double* cur = ser[cur_slot].get<double>(static_cast<size_t>(KT) * e1_grid.size());
+        rat_invert_mk_device(p_h, drt, KT, e1_grid, cur, st);
+        const double e1 = have_prev ? afs_error_e1_device(e1_grid, cur, static_cast<double*>(ser[cur_slot ^ 1].p), KT, st)
                                     : std::numeric_limits<double>::infinity();
         have_prev = true;
         cur_slot ^= 1;
         r.history.push_back({J, MH, ML, false, Cx(0, 0), e1, e2});
         ph = p_h;
-        rh_all = r_h;
         if (e1 <= cfg.e1_threshold && e2 <= cfg.e2_threshold) {
             if (++streak > cfg.validation_steps) {
                 r.converged = true;
@@ -209,9 +262,11 @@ AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
         } else {
             streak = 0;
         }
-        // select_new_frequency recomputes channel_errors on the same models in the
-        // reference (afs.cpp:156); the values are identical, so they are reused.
-        const Cx s_new = vf_select_new_frequency(p_h, r_h, p_l, r_l, KF, grid, r.samples, orf_pos, radius, &errors);
+        // select_new_frequency (afs.cpp:147-187) reuses this iteration's channel
+        // errors (the reference recomputes identical values, afs.cpp:156)
+        const int sel = vf_select_device(p_h, drh + er.kmax, p_l, drl + er.kmax, static_cast<size_t>(KF), grid,
+                                         r.samples, radius, st);
+        const Cx s_new = grid[sel];
         r.history.back().has_s_new = true;
         r.history.back().s_new = s_new;
         evaluate({s_new});
@@ -221,10 +276,16 @@ AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
     const int J = static_cast<int>(r.samples.size());
     const int M = static_cast<int>(ph.size());
     auto& cx = VfContext::get();
-    cplx* dvals = static_cast<cplx*>(cx.values.get(sizeof(cplx) * J * static_cast<size_t>(channels)));
     cplx* dres = static_cast<cplx*>(cx.out.get(sizeof(cplx) * M * static_cast<size_t>(channels)));
-    FDS_CUDA(cudaMemcpyAsync(dvals, r.values.data(), sizeof(cplx) * J * static_cast<size_t>(channels),
-                             cudaMemcpyHostToDevice, cx.st));
+    const cplx* dvals = nullptr;
+    if (KF == channels && j_dev == J) {  // every channel is a fit channel: samples already in HBM
+        dvals = static_cast<const cplx*>(samp[samp_cur].p);
+    } else {
+        cplx* v = static_cast<cplx*>(cx.values.get(sizeof(cplx) * J * static_cast<size_t>(channels)));
+        FDS_CUDA(cudaMemcpyAsync(v, r.values.data(), sizeof(cplx) * J * static_cast<size_t>(channels),
+                                 cudaMemcpyHostToDevice, cx.st));
+        dvals = v;
+    }
     vf_residues_device(r.samples, dvals, channels, canonical_order(ph), dres, nullptr, cx.st);
     std::vector<Cx> rmk(static_cast<size_t>(M) * channels);
     FDS_CUDA(cudaMemcpyAsync(rmk.data(), dres, rmk.size() * sizeof(cplx), cudaMemcpyDeviceToHost, cx.st));

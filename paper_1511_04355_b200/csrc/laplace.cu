@@ -716,6 +716,31 @@ void rat_invert_to_device(const std::vector<Cx>& poles, const std::vector<Cx>& r
     FDS_CUDA(cudaStreamSynchronize(st));
 }
 
+void rat_invert_mk_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int K, const std::vector<double>& t,
+                          double* out_dev, cudaStream_t st) {
+    // laplace.cpp:127-164 validation, as rat_invert_to_device
+    if (t.empty()) throw ValidationError("rational_invert: empty time grid");
+    for (size_t i = 1; i < t.size(); ++i)
+        if (!(t[i] > t[i - 1])) throw ValidationError("rational_invert: times must be strictly increasing");
+    if (!conj_closed(poles)) throw ValidationError("rational_invert: model poles not conjugate-closed");
+    for (Cx p : poles)
+        if (p.real() * t.back() > 700.0) throw NumericError("rational_invert: exponential overflow on the grid");
+    const int M = static_cast<int>(poles.size());
+    if (K == 0) return;
+    // the residue kernels write exact conjugates for canonical pairs, so the
+    // pairing test reduces to the pole structure
+    bool paired = true;
+    for (int m = 0; m < M && paired;) {
+        if (poles[m].imag() != 0.0) {
+            paired = m + 1 < M && poles[m + 1] == std::conj(poles[m]);
+            m += 2;
+        } else {
+            m += 1;
+        }
+    }
+    rat_invert_device(poles, res_mk_dev, K, t, out_dev, paired, st);
+}
+
 void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K, const std::vector<double>& t,
                      double* out) {
     auto& cx = VfContext::get();

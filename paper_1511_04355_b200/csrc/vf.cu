@@ -438,14 +438,15 @@ __device__ __forceinline__ void model_at(int g, int G, int M, const cplx* r, con
 }
 
 __global__ void __launch_bounds__(256)
-vf_chanerr_kernel(int G, int MH, int ML, int K, const cplx* __restrict__ rh /*[k][MH]*/,
-                  const cplx* __restrict__ rl /*[k][ML]*/, const cplx* __restrict__ invh, const cplx* __restrict__ invl,
+vf_chanerr_kernel(int G, int MH, int ML, int K, const cplx* __restrict__ rh, const cplx* __restrict__ rl,
+                  size_t sk_h, size_t sm_h, size_t sk_l, size_t sm_l,  // residue (k, m) at r[k*sk + m*sm]
+                  const cplx* __restrict__ invh, const cplx* __restrict__ invl,
                   double* __restrict__ out /*[k][2]: max|fH-fL|, max|fH|*/) {
     extern __shared__ cplx rsm[];
     __shared__ double red[2][8];
     const int k = blockIdx.x;
-    for (int m = threadIdx.x; m < MH; m += blockDim.x) rsm[m] = rh[static_cast<size_t>(k) * MH + m];
-    for (int m = threadIdx.x; m < ML; m += blockDim.x) rsm[MH + m] = rl[static_cast<size_t>(k) * ML + m];
+    for (int m = threadIdx.x; m < MH; m += blockDim.x) rsm[m] = rh[k * sk_h + m * sm_h];
+    for (int m = threadIdx.x; m < ML; m += blockDim.x) rsm[MH + m] = rl[k * sk_l + m * sm_l];
     __syncthreads();
     double md = 0.0, mh = 0.0;
     for (int g = threadIdx.x; g < G; g += blockDim.x) {
@@ -474,16 +475,16 @@ vf_chanerr_kernel(int G, int MH, int ML, int K, const cplx* __restrict__ rh /*[k
 }
 
 __global__ void __launch_bounds__(1024)
-vf_select_kernel(int G, int MH, int ML, const cplx* __restrict__ rh, const cplx* __restrict__ rl,
-                 const cplx* __restrict__ invh, const cplx* __restrict__ invl, const cplx* __restrict__ grid,
+vf_select_kernel(int G, int MH, int ML, const cplx* __restrict__ rh, const cplx* __restrict__ rl, size_t sm_h,
+                 size_t sm_l, const cplx* __restrict__ invh, const cplx* __restrict__ invl, const cplx* __restrict__ grid,
                  int nex, const double* __restrict__ ex_im, double radius, int* __restrict__ out) {
     extern __shared__ double exs[];
     __shared__ cplx r[512];
     __shared__ double bv[32];
     __shared__ int bi[32];
     for (int i = threadIdx.x; i < nex; i += blockDim.x) exs[i] = ex_im[i];
-    for (int m = threadIdx.x; m < MH; m += blockDim.x) r[m] = rh[m];
-    for (int m = threadIdx.x; m < ML; m += blockDim.x) r[MH + m] = rl[m];
+    for (int m = threadIdx.x; m < MH; m += blockDim.x) r[m] = rh[m * sm_h];
+    for (int m = threadIdx.x; m < ML; m += blockDim.x) r[MH + m] = rl[m * sm_l];
     __syncthreads();
     double best = -1.0;
     int bidx = 0x7fffffff;
@@ -513,6 +514,61 @@ vf_select_kernel(int G, int MH, int ML, const cplx* __restrict__ rh, const cplx*
             if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) { bv[0] = bv[w]; bi[0] = bi[w]; }
         out[0] = bv[0] >= 0.0 ? bi[0] : -1;
     }
+}
+
+// channel errors -> E2 over the test positions, the worst ORF channel
+// (afs.cpp:151-160: first strict max in ORF order) and the first channel with
+// an identically zero high-order fit (afs.cpp:138-141). One CTA.
+__global__ void __launch_bounds__(1024)
+afs_reduce_errors_kernel(int K, const double* __restrict__ ce /*[k][2]*/, int KT, const int* __restrict__ test_pos,
+                         int KO, const int* __restrict__ orf_pos, AfsErrReduce* __restrict__ out) {
+    __shared__ double bv[32];
+    __shared__ int bi[32];
+    __shared__ int zero_k;
+    if (threadIdx.x == 0) zero_k = 0x7fffffff;
+    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += blockDim.x)
+        if (ce[2 * k + 1] == 0.0) atomicMin(&zero_k, k);
+    double e2 = -INFINITY;  // std::max(e2, e) keeps e2 on NaN, as fmax does
+    for (int q = threadIdx.x; q < KT; q += blockDim.x) {
+        const int k = test_pos[q];
+        e2 = fmax(e2, ce[2 * k] / ce[2 * k + 1]);
+    }
+    double best = -1.0;  // (error, list index): larger error, then smaller index
+    int bidx = 0x7fffffff;
+    for (int q = threadIdx.x; q < KO; q += blockDim.x) {
+        const int k = orf_pos[q];
+        const double e = ce[2 * k] / ce[2 * k + 1];
+        if (e > best) { best = e; bidx = q; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        e2 = fmax(e2, __shfl_xor_sync(0xffffffffu, e2, off));
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+        if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ double be2[32];
+    if (lane == 0) { bv[wid] = best; bi[wid] = bidx; be2[wid] = e2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) { bv[0] = bv[w]; bi[0] = bi[w]; }
+            be2[0] = fmax(be2[0], be2[w]);
+        }
+        out->e2 = be2[0];
+        out->kmax = orf_pos[bi[0] == 0x7fffffff ? 0 : bi[0]];
+        out->zero_k = zero_k == 0x7fffffff ? -1 : zero_k;
+    }
+}
+
+__global__ void vf_gather_channels_kernel(int K, int M, int KT, const cplx* __restrict__ src /*[m][K]*/,
+                                          const int* __restrict__ pos, cplx* __restrict__ dst /*[m][KT]*/) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<size_t>(M) * KT) return;
+    const int m = static_cast<int>(idx / KT), q = static_cast<int>(idx % KT);
+    dst[idx] = src[static_cast<size_t>(m) * K + pos[q]];
 }
 
 // ------------------------------------------------------------------ host drivers
@@ -722,10 +778,30 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
     }
 }
 
-void vf_vector_fit(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<int>& orf, int order,
-                   int n_reloc, std::vector<Cx>& poles, std::vector<Cx>& res_km, FitReportC* rep) {
-    // vecfit.cpp:410-488
-    const int J = static_cast<int>(s.size());
+namespace {
+
+// vecfit.cpp:410-462: validation, starting poles and the relocation loop on the
+// ORF channels (host values ov [j][KO]); returns the relocated poles.
+std::vector<Cx> fit_poles(const std::vector<Cx>& s, const Cx* ov, int KO, int order, int n_reloc, FitReportC& r) {
+    double band = 0.0;
+    for (Cx x : s) band = std::max(band, std::abs(x.imag()));
+    if (band == 0.0)
+        for (Cx x : s) band = std::max(band, std::abs(x));
+    if (band == 0.0) throw ValidationError("vector_fit: samples carry no frequency band");
+    std::vector<Cx> poles = start_poles(band, order);
+    RelocResult rr;
+    for (int it = 0; it < n_reloc; ++it) {
+        rr = vf_relocate(s, ov, KO, poles);
+        poles = rr.poles;
+        r.iterations = it + 1;
+        r.movement = rr.movement;
+        if (rr.movement < 1e-8) break;
+    }
+    r.reloc_rms = rr.rms;
+    return poles;
+}
+
+void check_fit_args(int J, int K, const std::vector<int>& orf, int order, int n_reloc) {
     if (J == 0) throw ValidationError("vector_fit: no samples");
     if (order < 1) throw ValidationError("vector_fit: order must be >= 1");
     if (order >= 2 * J) throw ValidationError("vector_fit: order too high for the sample count");
@@ -733,26 +809,32 @@ void vf_vector_fit(const std::vector<Cx>& s, const Cx* values, int K, const std:
     if (orf.empty()) throw ValidationError("vector_fit: ORF channel set is empty");
     for (int k : orf)
         if (k < 0 || k >= K) throw ValidationError("vector_fit: ORF channel index out of range");
+}
+
+}  // namespace
+
+std::vector<Cx> vf_vector_fit_device(const std::vector<Cx>& s, const Cx* values_orf, const cplx* values_dev, int K,
+                                     const std::vector<int>& orf, int order, int n_reloc, cplx* res_dev,
+                                     cudaStream_t st) {
+    const int J = static_cast<int>(s.size());
+    check_fit_args(J, K, orf, order, n_reloc);
+    FitReportC r;
+    const std::vector<Cx> canon = canonical_order(fit_poles(s, values_orf, static_cast<int>(orf.size()), order, n_reloc, r));
+    vf_residues_device(s, values_dev, K, canon, res_dev, nullptr, st);
+    return canon;
+}
+
+void vf_vector_fit(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<int>& orf, int order,
+                   int n_reloc, std::vector<Cx>& poles, std::vector<Cx>& res_km, FitReportC* rep) {
+    // vecfit.cpp:410-488
+    const int J = static_cast<int>(s.size());
+    check_fit_args(J, K, orf, order, n_reloc);
     const int KO = static_cast<int>(orf.size());
     std::vector<Cx> ov(static_cast<size_t>(J) * KO);
     for (int j = 0; j < J; ++j)
         for (int q = 0; q < KO; ++q) ov[static_cast<size_t>(j) * KO + q] = values[static_cast<size_t>(j) * K + orf[q]];
-    double band = 0.0;
-    for (Cx x : s) band = std::max(band, std::abs(x.imag()));
-    if (band == 0.0)
-        for (Cx x : s) band = std::max(band, std::abs(x));
-    if (band == 0.0) throw ValidationError("vector_fit: samples carry no frequency band");
-    poles = start_poles(band, order);
     FitReportC r;
-    RelocResult rr;
-    for (int it = 0; it < n_reloc; ++it) {
-        rr = vf_relocate(s, ov.data(), KO, poles);
-        poles = rr.poles;
-        r.iterations = it + 1;
-        r.movement = rr.movement;
-        if (rr.movement < 1e-8) break;
-    }
-    r.reloc_rms = rr.rms;
+    poles = fit_poles(s, ov.data(), KO, order, n_reloc, r);
     // residues for every channel on the device
     const std::vector<Cx> canon = canonical_order(poles);
     auto& cx = VfContext::get();
@@ -804,7 +886,8 @@ std::vector<double> vf_channel_errors(const std::vector<Cx>& ph, const std::vect
     cudaEvent_t pe;
     profiler().begin(cx.st, kProfChanErr, 0.0, pe);
     FDS_LAUNCH(vf_chanerr_kernel, K, 256, (MH + ML) * sizeof(cplx), cx.st, G, MH, ML, K, dr,
-               dr + static_cast<size_t>(K) * MH, dinv, dinv + static_cast<size_t>(G) * MH, dout);
+               dr + static_cast<size_t>(K) * MH, size_t(MH), size_t(1), size_t(ML), size_t(1), dinv,
+               dinv + static_cast<size_t>(G) * MH, dout);
     profiler().end(cx.st, pe, kProfChanErr, 8.0 * G * static_cast<double>(K) * (MH + ML));
     std::vector<double> h(2 * static_cast<size_t>(K));
     FDS_CUDA(cudaMemcpyAsync(h.data(), dout, h.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
@@ -816,6 +899,86 @@ std::vector<double> vf_channel_errors(const std::vector<Cx>& ph, const std::vect
         e[k] = h[2 * k] / h[2 * k + 1];
     }
     return e;
+}
+
+void vf_channel_errors_device(const std::vector<Cx>& ph, const cplx* rh_mk, const std::vector<Cx>& pl,
+                              const cplx* rl_mk, int K, const std::vector<Cx>& grid, const int* test_pos_dev, int KT,
+                              const int* orf_pos_dev, int KO, double* ce_dev, AfsErrReduce* red_dev,
+                              cudaStream_t st) {
+    // afs.cpp:118-145 with residues [m][k] in HBM; the per-channel ratios are
+    // reduced on the device (E2, worst ORF channel, first zero-energy channel).
+    if (grid.empty()) throw ValidationError("channel_errors: empty grid");
+    const int G = static_cast<int>(grid.size()), MH = static_cast<int>(ph.size()), ML = static_cast<int>(pl.size());
+    for (Cx g : grid) {
+        for (Cx p : ph) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
+        for (Cx p : pl) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
+    }
+    auto& cx = VfContext::get();
+    std::vector<Cx> tabs(grid);
+    tabs.insert(tabs.end(), ph.begin(), ph.end());
+    tabs.insert(tabs.end(), pl.begin(), pl.end());
+    cplx* dgrid = dev<cplx>(cx.misc2, G + MH + ML);
+    cplx* dph = dgrid + G;
+    cplx* dpl = dph + MH;
+    cplx* dinv = dev<cplx>(cx.tab, static_cast<size_t>(G) * (MH + ML));
+    FDS_CUDA(cudaMemcpyAsync(dgrid, tabs.data(), tabs.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * MH, 256), 256, 0, st, G, MH, dgrid, dph, dinv);
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * ML, 256), 256, 0, st, G, ML, dgrid, dpl,
+               dinv + static_cast<size_t>(G) * MH);
+    cudaEvent_t pe;
+    profiler().begin(st, kProfChanErr, 0.0, pe);
+    FDS_LAUNCH(vf_chanerr_kernel, K, 256, (MH + ML) * sizeof(cplx), st, G, MH, ML, K, rh_mk, rl_mk, size_t(1),
+               size_t(K), size_t(1), size_t(K), dinv, dinv + static_cast<size_t>(G) * MH, ce_dev);
+    profiler().end(st, pe, kProfChanErr, 8.0 * G * static_cast<double>(K) * (MH + ML));
+    FDS_LAUNCH(afs_reduce_errors_kernel, 1, 1024, 0, st, K, ce_dev, KT, test_pos_dev, KO, orf_pos_dev, red_dev);
+    // tabs is read by the async copy above
+    FDS_CUDA(cudaStreamSynchronize(st));
+}
+
+int vf_select_device(const std::vector<Cx>& ph, const cplx* rh_k, const std::vector<Cx>& pl, const cplx* rl_k,
+                     size_t mstride, const std::vector<Cx>& grid, const std::vector<Cx>& existing, double radius,
+                     cudaStream_t st) {
+    // afs.cpp:162-187 for the worst ORF channel whose residues sit at rh_k[m*mstride]
+    const int G = static_cast<int>(grid.size()), MH = static_cast<int>(ph.size()), ML = static_cast<int>(pl.size());
+    if (MH + ML > 512) throw ValidationError("select_new_frequency: model order too large");
+    auto& cx = VfContext::get();
+    std::vector<Cx> tabs(grid);
+    tabs.insert(tabs.end(), ph.begin(), ph.end());
+    tabs.insert(tabs.end(), pl.begin(), pl.end());
+    cplx* dgrid = dev<cplx>(cx.misc2, G + MH + ML);
+    cplx* dph = dgrid + G;
+    cplx* dpl = dph + MH;
+    cplx* dinv = dev<cplx>(cx.tab, static_cast<size_t>(G) * (MH + ML));
+    std::vector<double> exim(existing.size());
+    for (size_t i = 0; i < existing.size(); ++i) exim[i] = existing[i].imag();
+    double* dex = dev<double>(cx.misc, std::max<size_t>(exim.size(), 1) + 2);
+    int* dsel = reinterpret_cast<int*>(dex + std::max<size_t>(exim.size(), 1));
+    FDS_CUDA(cudaMemcpyAsync(dgrid, tabs.data(), tabs.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    if (!exim.empty())
+        FDS_CUDA(cudaMemcpyAsync(dex, exim.data(), exim.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * MH, 256), 256, 0, st, G, MH, dgrid, dph, dinv);
+    FDS_LAUNCH(vf_inv_table_kernel, ceil_div(G * ML, 256), 256, 0, st, G, ML, dgrid, dpl,
+               dinv + static_cast<size_t>(G) * MH);
+    const int nex = static_cast<int>(exim.size());
+    const size_t smem = std::max<size_t>(nex, 1) * sizeof(double);
+    if (smem > 48 * 1024) {
+        FDS_CUDA(cudaFuncSetAttribute(vf_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(std::min(smem, device_info().smem_optin - 16 * 1024))));
+    }
+    FDS_LAUNCH(vf_select_kernel, 1, 1024, smem, st, G, MH, ML, rh_k, rl_k, mstride, mstride, dinv,
+               dinv + static_cast<size_t>(G) * MH, dgrid, nex, dex, radius, dsel);
+    int sel = -1;
+    FDS_CUDA(cudaMemcpyAsync(&sel, dsel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FDS_CUDA(cudaStreamSynchronize(st));
+    if (sel < 0) throw NumericError("select_new_frequency: every grid point is excluded");
+    return sel;
+}
+
+void vf_gather_channels(const cplx* src_mk, int K, int M, const int* pos_dev, int KT, cplx* dst_mk, cudaStream_t st) {
+    const size_t n = static_cast<size_t>(M) * KT;
+    if (n == 0) return;
+    FDS_LAUNCH(vf_gather_channels_kernel, static_cast<int>((n + 255) / 256), 256, 0, st, K, M, KT, src_mk, pos_dev,
+               dst_mk);
 }
 
 Cx vf_select_new_frequency(const std::vector<Cx>& ph, const std::vector<Cx>& rh, const std::vector<Cx>& pl,
@@ -860,8 +1023,8 @@ Cx vf_select_new_frequency(const std::vector<Cx>& ph, const std::vector<Cx>& rh,
         FDS_CUDA(cudaFuncSetAttribute(vf_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(std::min(smem, device_info().smem_optin - 16 * 1024))));
     }
-    FDS_LAUNCH(vf_select_kernel, 1, 1024, smem, cx.st, G, MH, ML, dr, dr + MH, dinv, dinv + static_cast<size_t>(G) * MH,
-               dgrid, nex, dex, radius, dsel);
+    FDS_LAUNCH(vf_select_kernel, 1, 1024, smem, cx.st, G, MH, ML, dr, dr + MH, size_t(1), size_t(1), dinv,
+               dinv + static_cast<size_t>(G) * MH, dgrid, nex, dex, radius, dsel);
     int sel = -1;
     FDS_CUDA(cudaMemcpyAsync(&sel, dsel, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
     FDS_CUDA(cudaStreamSynchronize(cx.st));

@@ -66,6 +66,37 @@ Cx vf_select_new_frequency(const std::vector<Cx>& ph, const std::vector<Cx>& rh,
                            const std::vector<Cx>& existing, const std::vector<int>& orf_pos, double radius,
                            const std::vector<double>* errors);
 
+// ---- device-resident AFS iteration
+// vector_fit whose residue step reads samples [j][k] already in HBM and leaves
+// residues [m][k] in HBM; relocation runs on the ORF values (host, [j][|orf|]).
+// Returns the canonical poles.
+std::vector<Cx> vf_vector_fit_device(const std::vector<Cx>& s, const Cx* values_orf, const cplx* values_dev, int K,
+                                     const std::vector<int>& orf, int order, int n_reloc, cplx* res_dev,
+                                     cudaStream_t st);
+struct AfsErrReduce {
+    double e2;   // max over the test positions of e_k
+    int kmax;    // worst ORF channel position (first strict max in ORF order)
+    int zero_k;  // first channel with an identically zero high-order fit, or -1
+};
+// channel_errors of two device-resident models (residues [m][k]) into ce_dev
+// [k][2] = (max|fH-fL|, max|fH|), reduced into *red_dev; synchronises st.
+void vf_channel_errors_device(const std::vector<Cx>& ph, const cplx* rh_mk, const std::vector<Cx>& pl,
+                              const cplx* rl_mk, int K, const std::vector<Cx>& grid, const int* test_pos_dev, int KT,
+                              const int* orf_pos_dev, int KO, double* ce_dev, AfsErrReduce* red_dev,
+                              cudaStream_t st);
+// select_new_frequency's grid scan for one channel whose residues sit at
+// rh_k[m*mstride], rl_k[m*mstride] on the device; returns the grid index.
+int vf_select_device(const std::vector<Cx>& ph, const cplx* rh_k, const std::vector<Cx>& pl, const cplx* rl_k,
+                     size_t mstride, const std::vector<Cx>& grid, const std::vector<Cx>& existing, double radius,
+                     cudaStream_t st);
+// dst[m][q] = src[m][pos[q]] for q < KT (channel subset of a [m][K] residue block)
+void vf_gather_channels(const cplx* src_mk, int K, int M, const int* pos_dev, int KT, cplx* dst_mk, cudaStream_t st);
+// rational_invert of a device-resident model (residues [m][k], exact conjugate
+// pairs as the residue kernels write them) into out_dev [k][t], with
+// rational_invert's validation.
+void rat_invert_mk_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int K, const std::vector<double>& t,
+                          double* out_dev, cudaStream_t st);
+
 // rational_invert (laplace.cpp:127-164): host model -> host out[k][t].
 void rat_invert_host(const std::vector<Cx>& poles, const std::vector<Cx>& res_km, int K,
                      const std::vector<double>& t, double* out);

@@ -28,5 +28,23 @@ for name, chans in (("16_points", list(range(0, 1280, 80))), ("all_dofs", None))
         solve = time.perf_counter() - t1
         out[f"{name}_{solver}"] = {"channels": sysb.descriptor().channel_count, "n_c": len(s), "afs_wall_s": wall,
                                    "solves_wall_s": solve, "driver_overhead_s": wall - solve}
+    # driver-only cost: replay the recorded samples through a Python system (dict lookup)
+    r = P.run_afs(sysb, **cfg)
+    s = np.asarray(r["samples"]); vals = np.asarray(r["values"]).reshape(len(s), -1)
+    table = {complex(z): vals[i] for i, z in enumerate(s)}
+
+    class Replay:
+        def descriptor(self):
+            return P.api.SystemDescriptor(vals.shape[1], [])
+
+        def evaluate(self, z):
+            return table[complex(z)]
+
+    P.run_afs(Replay(), **cfg)
+    t0 = time.perf_counter()
+    rr = P.run_afs(Replay(), **cfg)
+    out[f"{name}_replay"] = {"channels": vals.shape[1], "n_c": len(rr["samples"]),
+                             "driver_wall_s": time.perf_counter() - t0,
+                             "same_samples": bool(np.array_equal(np.asarray(rr["samples"]), s))}
     sysb.close()
 print(json.dumps(out))
