@@ -173,13 +173,13 @@ struct fds_bem {
                 one.ipiv = ipiv + static_cast<size_t>(b) * n;
                 one.info = info + b;
                 lu_factor(one, ws, st);
-                lu_solve(one, rhs + static_cast<size_t>(b) * ld, ld, st);
+                lu_solve(one, rhs + static_cast<size_t>(b) * ld, ld, ws, st);
             }
             FDS_CUDA(cudaEventRecord(ev[2], st));
         } else {
             lu_factor(pb, ws, st);
             FDS_CUDA(cudaEventRecord(ev[2], st));
-            lu_solve(pb, rhs, ld, st);
+            lu_solve(pb, rhs, ld, ws, st);
         }
         FDS_LAUNCH(gather_channels_kernel, ceil_div(K * B, 256), 256, 0, st, rhs, static_cast<size_t>(ld),
                    chan, K, B, out);
@@ -447,7 +447,7 @@ int fds_zgesv_batch(int n, int B, const fds_c64* A, const fds_c64* rhs, fds_c64*
         pb.info = di.p;
         LuWorkspace ws;
         lu_factor(pb, ws, st);
-        lu_solve(pb, dr.p, ld, st);
+        lu_solve(pb, dr.p, ld, ws, st);
         FDS_CUDA(cudaStreamSynchronize(st));
         ws.release();
         std::vector<int> info(B);

@@ -1237,6 +1237,231 @@ lu_bwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld
     if (tid < w) x[k + tid] = yt;
 }
 
+// ------------------------------------------------------------------ dataflow solve
+// Forward / backward substitution as a dataflow over row blocks of the
+// factorization's panel width nb: one CTA per (block, matrix), handed out in
+// dependency order through a per-matrix ticket, so every block a CTA waits on
+// already holds an SM or is done (no co-residency assumption). A block streams
+// its L21 / U12 row blocks, multiplying each by an earlier solution block as
+// soon as that block's flag is published (release / acquire), then finishes
+// with one warp's substitution on its diagonal block staged in smem. The
+// blocks progress as a wavefront instead of 2·n/nb dependent panel + GEMV
+// launches, so a single system's solve runs at HBM speed.
+//
+// The factors keep each panel's row interchanges in the panel and the columns
+// to its right only (the partial-pivoting schedule of lu_factor), so the L21
+// rows that meet a given final row r sit at r's position at that panel's step:
+// block m traces its rows back through panels m..0 (σ_{-1,m}, the position of
+// r's right-hand-side entry) and forward again one panel per step. Panels with
+// no interchange (pflag = 0, the usual case on BEM matrices) are skipped.
+constexpr int kDfThreads = 256;  // 64 rows x 4 column groups
+
+// poll a published flag with relaxed loads (an acquire per poll would
+// invalidate L1 each time), then order the following loads with one fence
+__device__ __forceinline__ void wait_flag(const int* p) {
+    int v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+        if (v == 0) __nanosleep(32);
+    } while (v == 0);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int swap_forward(int q, const int* pv, int k, int w) {
+    for (int i = 0; i < w; ++i) {
+        const int a = k + i, b = __ldg(pv + a);
+        q = q == a ? b : (q == b ? a : q);
+    }
+    return q;
+}
+
+__device__ __forceinline__ int swap_backward(int q, const int* pv, int k, int w) {
+    for (int i = w - 1; i >= 0; --i) {
+        const int a = k + i, b = __ldg(pv + a);
+        q = q == a ? b : (q == b ? a : q);
+    }
+    return q;
+}
+
+__global__ void __launch_bounds__(64)
+lu_pivflag_kernel(int n, int nb, const int* ipiv, int* pflag) {
+    const int b = blockIdx.y, m = blockIdx.x, nblk = (n + nb - 1) / nb;
+    const int r = m * nb + threadIdx.x;
+    const bool moved = threadIdx.x < nb && r < n && ipiv[static_cast<size_t>(b) * n + r] != r;
+    const int any = __syncthreads_or(moved);
+    if (threadIdx.x == 0) pflag[static_cast<size_t>(b) * nblk + m] = any;
+}
+
+// diagonal block rows/cols < w of matrix (Are, Aim) at (k, k) into smem, column-major [64][64] re then im
+__device__ __forceinline__ void stage_diag(double* dsm, const double* Are, const double* Aim, int k, int w, int ld) {
+#pragma unroll 4
+    for (int e = threadIdx.x; e < 64 * 64; e += kDfThreads) {
+        const int c = e >> 6, r = e & 63;
+        double vr = 0.0, vi = 0.0;
+        if (c < w && r < w) {
+            const size_t gi = static_cast<size_t>(k + c) * ld + k + r;
+            vr = Are[gi];
+            vi = Aim[gi];
+        }
+        dsm[e] = vr;
+        dsm[4096 + e] = vi;
+    }
+}
+
+__global__ void __launch_bounds__(kDfThreads, 3)
+lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int nb, const int* ipiv,
+                 const int* pflag, const cplx* rhs, size_t rstride, cplx* ybuf, int* flags, int* tickets) {
+    extern __shared__ double dsm[];  // unit-lower diagonal block
+    __shared__ cplx part[4][64];
+    __shared__ int s_m;
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+    const int nblk = (n + nb - 1) / nb;
+    if (tid == 0) s_m = atomicAdd(tickets + b, 1);
+    __syncthreads();
+    const int m = s_m, k = m * nb, w = min(nb, n - k);
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    const int* pv = ipiv + static_cast<size_t>(b) * n;
+    const int* pf = pflag + static_cast<size_t>(b) * nblk;
+    int* fl = flags + static_cast<size_t>(b) * nblk;
+    cplx* yb = ybuf + static_cast<size_t>(b) * n;
+    stage_diag(dsm, Are, Aim, k, w, ld);
+    const int tr = tid & 63, g = tid >> 6, cpg = nb >> 2;
+    const bool live = tr < w;
+    int q = k + tr;
+    if (live)
+        for (int p = m; p >= 0; --p)
+            if (pf[p]) q = swap_backward(q, pv, p * nb, min(nb, n - p * nb));
+    double ar = 0.0, ai = 0.0;
+    if (live && g == 0) {
+        const cplx v = rhs[static_cast<size_t>(b) * rstride + q];
+        ar = v.re;
+        ai = v.im;
+    }
+    for (int j = 0; j < m; ++j) {
+        const int kj = j * nb;
+        if (live && pf[j]) q = swap_forward(q, pv, kj, nb);
+        double lr[16], li[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            lr[c] = li[c] = 0.0;
+            if (c < cpg && live) {
+                const size_t gi = static_cast<size_t>(kj + g * cpg + c) * ld + q;
+                lr[c] = __ldg(Are + gi);
+                li[c] = __ldg(Aim + gi);
+            }
+        }
+        if (lane == 0) wait_flag(fl + j);
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            if (c < cpg) {
+                const double2 y = __ldcg(reinterpret_cast<const double2*>(yb + kj + g * cpg + c));
+                ar -= lr[c] * y.x - li[c] * y.y;
+                ai -= lr[c] * y.y + li[c] * y.x;
+            }
+        }
+    }
+    part[g][tr] = mk(ar, ai);
+    __syncthreads();
+    if (tid < 32) {
+        cplx v0 = part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane];
+        cplx v1 = part[0][lane + 32] + part[1][lane + 32] + part[2][lane + 32] + part[3][lane + 32];
+#pragma unroll 1
+        for (int j = 0; j < w - 1; ++j) {  // rolled: one warp runs it once per block, keep it in the i-cache
+            const cplx src = j < 32 ? v0 : v1;
+            const cplx yj = mk(__shfl_sync(0xffffffffu, src.re, j & 31), __shfl_sync(0xffffffffu, src.im, j & 31));
+            if (lane > j) v0 = v0 - mk(dsm[j * 64 + lane], dsm[4096 + j * 64 + lane]) * yj;
+            if (lane + 32 > j) v1 = v1 - mk(dsm[j * 64 + lane + 32], dsm[4096 + j * 64 + lane + 32]) * yj;
+        }
+        if (lane < w) yb[k + lane] = v0;
+        if (lane + 32 < w) yb[k + lane + 32] = v1;
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_i(fl + m, 1);
+    }
+}
+
+__global__ void __launch_bounds__(kDfThreads, 3)
+lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int nb, const cplx* ybuf, cplx* rhs,
+                 size_t rstride, int* flags, int* tickets) {
+    extern __shared__ double dsm[];  // upper diagonal block
+    __shared__ cplx part[4][64];
+    __shared__ int s_m;
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+    const int nblk = (n + nb - 1) / nb;
+    if (tid == 0) s_m = nblk - 1 - atomicAdd(tickets + b, 1);
+    __syncthreads();
+    const int m = s_m, k = m * nb, w = min(nb, n - k);
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    int* fl = flags + static_cast<size_t>(b) * nblk;
+    cplx* x = rhs + static_cast<size_t>(b) * rstride;
+    stage_diag(dsm, Are, Aim, k, w, ld);
+    const int tr = tid & 63, g = tid >> 6, cpg = nb >> 2;
+    const bool live = tr < w;
+    double ar = 0.0, ai = 0.0;
+    for (int j = nblk - 1; j > m; --j) {
+        const int kj = j * nb, wj = min(nb, n - kj);
+        double ur[16], ui[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            ur[c] = ui[c] = 0.0;
+            const int col = g * cpg + c;
+            if (c < cpg && live && col < wj) {
+                const size_t gi = static_cast<size_t>(kj + col) * ld + k + tr;
+                ur[c] = __ldg(Are + gi);
+                ui[c] = __ldg(Aim + gi);
+            }
+        }
+        if (lane == 0) wait_flag(fl + j);
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const int col = g * cpg + c;
+            if (c < cpg && col < wj) {
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(x + kj + col));
+                ar += ur[c] * v.x - ui[c] * v.y;
+                ai += ur[c] * v.y + ui[c] * v.x;
+            }
+        }
+    }
+    part[g][tr] = mk(ar, ai);
+    __syncthreads();
+    if (tid < 32) {
+        const cplx* yb = ybuf + static_cast<size_t>(b) * n;
+        cplx v0 = mk(0.0, 0.0), v1 = mk(0.0, 0.0);
+        if (lane < w) v0 = yb[k + lane] - (part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]);
+        if (lane + 32 < w)
+            v1 = yb[k + lane + 32] -
+                 (part[0][lane + 32] + part[1][lane + 32] + part[2][lane + 32] + part[3][lane + 32]);
+        // reciprocals of the diagonal, all lanes at once (off the sequential chain)
+        const cplx r0 = crecip(mk(dsm[lane * 65], dsm[4096 + lane * 65]));
+        const cplx r1 = crecip(mk(dsm[(lane + 32) * 65], dsm[4096 + (lane + 32) * 65]));
+#pragma unroll 1
+        for (int j = w - 1; j >= 0; --j) {  // rolled: one warp runs it once per block, keep it in the i-cache
+            if (j < 32) {
+                if (lane == j) v0 = v0 * r0;
+            } else {
+                if (lane == j - 32) v1 = v1 * r1;
+            }
+            const cplx src = j < 32 ? v0 : v1;
+            const cplx xj = mk(__shfl_sync(0xffffffffu, src.re, j & 31), __shfl_sync(0xffffffffu, src.im, j & 31));
+            if (lane < j) v0 = v0 - mk(dsm[j * 64 + lane], dsm[4096 + j * 64 + lane]) * xj;
+            if (lane + 32 < j) v1 = v1 - mk(dsm[j * 64 + lane + 32], dsm[4096 + j * 64 + lane + 32]) * xj;
+        }
+        if (lane < w) x[k + lane] = v0;
+        if (lane + 32 < w) x[k + lane + 32] = v1;
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_i(fl + m, 1);
+    }
+}
+
 // ------------------------------------------------------------------ host
 void LuWorkspace::ensure(int groups, int P, int nb) {
     const size_t need = static_cast<size_t>(groups) * 2 * (P + 1) * (2 + 2 * nb) * sizeof(double) +
@@ -1272,6 +1497,11 @@ double* LuWorkspace::linv(int batch) {
 }
 
 void LuWorkspace::release() {
+    if (ybuf) cudaFree(ybuf);
+    if (sflags) cudaFree(sflags);
+    ybuf = nullptr;
+    sflags = nullptr;
+    ybuf_cap = sflag_cap = 0;
     if (linv_buf) cudaFree(linv_buf);
     linv_buf = nullptr;
     linv_cap = 0;
@@ -1722,7 +1952,69 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     }
 }
 
-void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st) {
+void LuWorkspace::ensure_solve(int batch, int n, int nblk) {
+    const size_t yneed = static_cast<size_t>(batch) * n;
+    if (yneed > ybuf_cap) {
+        if (ybuf) cudaFree(ybuf);
+        ybuf = nullptr;
+        FDS_CUDA(cudaMalloc(&ybuf, yneed * sizeof(cplx)));
+        ybuf_cap = yneed;
+    }
+    // pflag [batch][nblk], flags fwd / bwd [batch][nblk], tickets fwd / bwd [batch]
+    const size_t fneed = 3 * static_cast<size_t>(batch) * nblk + 2 * static_cast<size_t>(batch);
+    if (fneed > sflag_cap) {
+        if (sflags) cudaFree(sflags);
+        sflags = nullptr;
+        FDS_CUDA(cudaMalloc(&sflags, fneed * sizeof(int)));
+        sflag_cap = fneed;
+    }
+}
+
+namespace {
+
+bool dataflow_solve() {
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_SOLVE");
+        return !(e && std::string(e) == "blocked");
+    }();
+    return on;
+}
+
+void lu_solve_blocked(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st);
+
+}  // namespace
+
+void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, cudaStream_t st) {
+    if (!dataflow_solve()) {
+        lu_solve_blocked(pb, rhs, rstride, st);
+        return;
+    }
+    const int nb = lu_panel_width(pb.n);
+    const int nblk = ceil_div(pb.n, nb);
+    ws.ensure_solve(pb.batch, pb.n, nblk);
+    int* pflag = ws.sflags;
+    int* ffl = pflag + static_cast<size_t>(pb.batch) * nblk;
+    int* bfl = ffl + static_cast<size_t>(pb.batch) * nblk;
+    int* tk = bfl + static_cast<size_t>(pb.batch) * nblk;
+    FDS_CUDA(cudaMemsetAsync(ffl, 0, (2 * static_cast<size_t>(pb.batch) * nblk + 2 * pb.batch) * sizeof(int), st));
+    const size_t smem = 2 * 64 * 64 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        FDS_CUDA(cudaFuncSetAttribute(lu_fwd_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        FDS_CUDA(cudaFuncSetAttribute(lu_bwd_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = true;
+    }
+    const dim3 g(nblk, pb.batch);
+    FDS_LAUNCH(lu_pivflag_kernel, g, 64, 0, st, pb.n, nb, pb.ipiv, pflag);
+    FDS_LAUNCH(lu_fwd_df_kernel, g, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, pb.ipiv, pflag,
+               rhs, rstride, ws.ybuf, ffl, tk);
+    FDS_LAUNCH(lu_bwd_df_kernel, g, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, ws.ybuf, rhs,
+               rstride, bfl, tk + pb.batch);
+}
+
+namespace {
+
+void lu_solve_blocked(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st) {
     const int nb = lu_panel_width(pb.n);
     for (int k = 0; k < pb.n; k += nb) {
         const int w = std::min(nb, pb.n - k);
@@ -1747,5 +2039,7 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st) {
         }
     }
 }
+
+}  // namespace
 
 }  // namespace fdsb

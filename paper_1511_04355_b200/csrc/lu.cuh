@@ -43,6 +43,12 @@ struct LuWorkspace {
     double* linv_buf = nullptr;  // [batch][2][64][64] L11^{-1} per panel
     int linv_cap = 0;
     double* linv(int batch);
+    // dataflow solve: forward results [batch][n], per-panel pivot flags, block flags, tickets
+    cplx* ybuf = nullptr;
+    size_t ybuf_cap = 0;
+    int* sflags = nullptr;
+    size_t sflag_cap = 0;
+    void ensure_solve(int batch, int n, int nblk);
     double* slots = nullptr;
     unsigned* counters = nullptr;
     size_t slot_bytes = 0;
@@ -60,8 +66,9 @@ inline size_t lu_plane(int n) { return static_cast<size_t>(lu_ld(n)) * lu_ld(n);
 
 // Per-step timings are not taken here; the caller brackets with events.
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st);
-// rhs[b*rstride + i], complex interleaved, overwritten with the solution.
-void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream_t st);
+// rhs[b*rstride + i], complex interleaved, overwritten with the solution
+// (dataflow substitution; FDSWEEP_SOLVE=blocked selects the per-panel launches).
+void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, cudaStream_t st);
 int lu_panel_width(int n);
 void calu_panel_step(const LuProblem& pb, CaluWorkspace& ws, int k, int w, cudaStream_t st);
 

@@ -38,8 +38,19 @@ def full(rep, kernel_regex):
             "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
             "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio"]
     res = []
+    units = rows[1]
+    scale = {"Gbyte": 1.0, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9, "ms": 1.0, "msecond": 1.0, "us": 1e-3,
+             "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6}
     for r in rows[2:]:
-        d = {w: r[hdr.index(w)] for w in want if w in hdr}
+        d = {}
+        for w in want:
+            if w not in hdr:
+                continue
+            i = hdr.index(w)
+            v = r[i]
+            if units[i] in scale:  # normalise to GB / ms
+                v = repr(float(v.replace(",", "")) * scale[units[i]])
+            d[w] = v
         res.append(d)
     return res
 
@@ -49,8 +60,9 @@ if __name__ == "__main__":
     json.dump({"command": "python bench.py --steps 1 --warmup 1 --no-extra --no-cpu",
                "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)",
                "total_ms": round(tot, 3), "kernels": summ}, open(f"profiles/{tag}_launches_summary.json", "w"), indent=1)
-    f = full("gpurun_out/prof_gemm_r1.ncu-rep", "lu_gemm")
-    json.dump({"command": "ncu --set full --clock-control none -k regex:lu_gemm -s 30 -c 1 python bench.py --steps 1 --warmup 1 --no-extra --no-cpu",
+    f = full("gpurun_out/prof_gemm_r1.ncu-rep", "lu_gemm_tma")
+    json.dump({"command": "ncu --set full --clock-control none --import-source on -k regex:lu_gemm_tma -s 30 -c 1 python bench.py --steps 1 --warmup 1 --no-extra --no-cpu",
+               "units": "GB, ms",
                "kernels": f}, open(f"profiles/{tag}_lu_gemm_ncu_full.json", "w"), indent=1)
     g = f[0]
     traffic = (float(g["dram__bytes_read.sum"]) + float(g["dram__bytes_write.sum"])) * 1e9  # GB -> bytes
