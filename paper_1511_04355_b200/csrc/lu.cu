@@ -1240,7 +1240,7 @@ lu_bwd_panel_kernel(const double* A, size_t mstride, size_t plane, int n, int ld
 // ------------------------------------------------------------------ dataflow solve
 // Forward / backward substitution as a dataflow over row blocks of the
 // factorization's panel width nb: one CTA per (block, matrix), handed out in
-// dependency order through a per-matrix ticket, so every block a CTA waits on
+// dependency order through a ticket, so every block a CTA waits on
 // already holds an SM or is done (no co-residency assumption). A block streams
 // its L21 / U12 row blocks, multiplying each by an earlier solution block as
 // soon as that block's flag is published (release / acquire), then finishes
@@ -1265,6 +1265,32 @@ __device__ __forceinline__ void wait_flag(const int* p) {
         if (v == 0) __nanosleep(32);
     } while (v == 0);
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+__device__ __forceinline__ int ld_relaxed_i(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Blocks publish in dependency order (block j's flag implies every block it
+// depends on), so a warp that needs block j first looks at the last block it
+// will ever need (`last`) and otherwise waits for j and scans on: it returns
+// the furthest block known ready, fenced once, and polls again only past it.
+// step = +1 (forward chain) or -1 (backward chain).
+__device__ __forceinline__ int wait_ready(const int* fl, int j, int last, int step) {
+    int r = 0;
+    if ((threadIdx.x & 31) == 0) {
+        if (ld_relaxed_i(fl + last) != 0) {
+            r = last;
+        } else {
+            wait_flag(fl + j);
+            r = j;
+            while (r != last && ld_relaxed_i(fl + r + step) != 0) r += step;
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    return __shfl_sync(0xffffffffu, r, 0);
 }
 
 __device__ __forceinline__ void st_release_i(int* p, int v) {
@@ -1312,24 +1338,96 @@ __device__ __forceinline__ void stage_diag(double* dsm, const double* Are, const
     }
 }
 
+// In-place inverse of the staged diagonal block by all 256 threads, before
+// the block's own wait: the unit-lower part (LOWER; X L = I, columns right to
+// left) or the upper part (X U = I, columns left to right). The diagonal
+// block's solve then becomes one parallel 64x64 product at the end of the
+// dependency chain instead of 64 sequential substitution steps.
+template <bool LOWER>
+__device__ __forceinline__ void invert_diag(double* dsm, cplx (*red)[64], int w) {
+    const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
+    auto S = [&](int r, int c) { return mk(dsm[c * 64 + r], dsm[4096 + c * 64 + r]); };
+    if (LOWER) {
+        for (int j = w - 2; j >= 0; --j) {
+            cplx acc = mk(0.0, 0.0);
+            if (i > j && i < w) {
+                for (int k = j + 1 + g; k < i; k += 4) acc = acc + S(i, k) * S(k, j);
+                if (g == 0) acc = acc + S(i, j);
+            }
+            red[g][i] = acc;
+            __syncthreads();
+            if (g == 0 && i > j && i < w) {
+                const cplx x = red[0][i] + red[1][i] + red[2][i] + red[3][i];
+                dsm[j * 64 + i] = -x.re;
+                dsm[4096 + j * 64 + i] = -x.im;
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int j = 0; j < w; ++j) {
+            cplx acc = mk(0.0, 0.0);
+            if (i < j)
+                for (int k = i + g; k < j; k += 4) acc = acc + S(i, k) * S(k, j);
+            red[g][i] = acc;
+            const cplx d = crecip(S(j, j));
+            __syncthreads();
+            if (g == 0 && i <= j) {
+                const cplx x = i == j ? d : mk(0.0, 0.0) - (red[0][i] + red[1][i] + red[2][i] + red[3][i]) * d;
+                dsm[j * 64 + i] = x.re;
+                dsm[4096 + j * 64 + i] = x.im;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// v (smem, 64) -> X v with X the inverted diagonal block (unit lower: ones on
+// the diagonal, zeros above; upper: zeros below). Returns row tr's value in
+// threads g == 0.
+template <bool LOWER>
+__device__ __forceinline__ cplx apply_diag(const double* dsm, const cplx* v, cplx (*red)[64], int w) {
+    const int tr = threadIdx.x & 63, g = threadIdx.x >> 6;
+    double ar = 0.0, ai = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) {
+        const int c = g * 16 + cc;
+        const bool on = LOWER ? c < tr : c >= tr;
+        if (on && c < w) {
+            const double xr = dsm[c * 64 + tr], xi = dsm[4096 + c * 64 + tr];
+            ar += xr * v[c].re - xi * v[c].im;
+            ai += xr * v[c].im + xi * v[c].re;
+        }
+    }
+    red[g][tr] = mk(ar, ai);
+    __syncthreads();
+    cplx y = red[0][tr] + red[1][tr] + red[2][tr] + red[3][tr];
+    if (LOWER) y = y + v[tr];
+    return y;
+}
+
 __global__ void __launch_bounds__(kDfThreads, 3)
 lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int nb, const int* ipiv,
                  const int* pflag, const cplx* rhs, size_t rstride, cplx* ybuf, int* flags, int* tickets) {
     extern __shared__ double dsm[];  // unit-lower diagonal block
     __shared__ cplx part[4][64];
     __shared__ int s_m;
-    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
-    const int nblk = (n + nb - 1) / nb;
-    if (tid == 0) s_m = atomicAdd(tickets + b, 1);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nblk = (n + nb - 1) / nb, batch = gridDim.x / nblk;
+    if (tid == 0) s_m = atomicAdd(tickets, 1);
     __syncthreads();
-    const int m = s_m, k = m * nb, w = min(nb, n - k);
+    // tickets interleave the matrices (block-major), so every matrix's chain
+    // advances in the same wave
+    const int b = s_m % batch, m = s_m / batch, k = m * nb, w = min(nb, n - k);
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     const int* pv = ipiv + static_cast<size_t>(b) * n;
     const int* pf = pflag + static_cast<size_t>(b) * nblk;
     int* fl = flags + static_cast<size_t>(b) * nblk;
     cplx* yb = ybuf + static_cast<size_t>(b) * n;
+    __shared__ cplx vsm[64];
     stage_diag(dsm, Are, Aim, k, w, ld);
+    __syncthreads();
+    invert_diag<true>(dsm, part, w);
     const int tr = tid & 63, g = tid >> 6, cpg = nb >> 2;
     const bool live = tr < w;
     int q = k + tr;
@@ -1342,6 +1440,7 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
         ar = v.re;
         ai = v.im;
     }
+    int ready = -1;  // furthest block known published (warp-uniform)
     for (int j = 0; j < m; ++j) {
         const int kj = j * nb;
         if (live && pf[j]) q = swap_forward(q, pv, kj, nb);
@@ -1355,7 +1454,7 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
                 li[c] = __ldg(Aim + gi);
             }
         }
-        if (lane == 0) wait_flag(fl + j);
+        if (j > ready) ready = wait_ready(fl, j, m - 1, 1);
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
@@ -1368,22 +1467,13 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     }
     part[g][tr] = mk(ar, ai);
     __syncthreads();
-    if (tid < 32) {
-        cplx v0 = part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane];
-        cplx v1 = part[0][lane + 32] + part[1][lane + 32] + part[2][lane + 32] + part[3][lane + 32];
-#pragma unroll 1
-        for (int j = 0; j < w - 1; ++j) {  // rolled: one warp runs it once per block, keep it in the i-cache
-            const cplx src = j < 32 ? v0 : v1;
-            const cplx yj = mk(__shfl_sync(0xffffffffu, src.re, j & 31), __shfl_sync(0xffffffffu, src.im, j & 31));
-            if (lane > j) v0 = v0 - mk(dsm[j * 64 + lane], dsm[4096 + j * 64 + lane]) * yj;
-            if (lane + 32 > j) v1 = v1 - mk(dsm[j * 64 + lane + 32], dsm[4096 + j * 64 + lane + 32]) * yj;
-        }
-        if (lane < w) yb[k + lane] = v0;
-        if (lane + 32 < w) yb[k + lane + 32] = v1;
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_i(fl + m, 1);
-    }
+    if (tid < 64) vsm[tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+    __syncthreads();
+    const cplx y = apply_diag<true>(dsm, vsm, part, w);
+    if (g == 0 && live) yb[k + tr] = y;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_i(fl + m, 1);
 }
 
 __global__ void __launch_bounds__(kDfThreads, 3)
@@ -1392,19 +1482,23 @@ lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     extern __shared__ double dsm[];  // upper diagonal block
     __shared__ cplx part[4][64];
     __shared__ int s_m;
-    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
-    const int nblk = (n + nb - 1) / nb;
-    if (tid == 0) s_m = nblk - 1 - atomicAdd(tickets + b, 1);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nblk = (n + nb - 1) / nb, batch = gridDim.x / nblk;
+    if (tid == 0) s_m = atomicAdd(tickets, 1);
     __syncthreads();
-    const int m = s_m, k = m * nb, w = min(nb, n - k);
+    const int b = s_m % batch, m = nblk - 1 - s_m / batch, k = m * nb, w = min(nb, n - k);
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     int* fl = flags + static_cast<size_t>(b) * nblk;
     cplx* x = rhs + static_cast<size_t>(b) * rstride;
+    __shared__ cplx vsm[64];
     stage_diag(dsm, Are, Aim, k, w, ld);
+    __syncthreads();
+    invert_diag<false>(dsm, part, w);
     const int tr = tid & 63, g = tid >> 6, cpg = nb >> 2;
     const bool live = tr < w;
     double ar = 0.0, ai = 0.0;
+    int ready = nblk;  // furthest block known published (warp-uniform)
     for (int j = nblk - 1; j > m; --j) {
         const int kj = j * nb, wj = min(nb, n - kj);
         double ur[16], ui[16];
@@ -1418,7 +1512,7 @@ lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
                 ui[c] = __ldg(Aim + gi);
             }
         }
-        if (lane == 0) wait_flag(fl + j);
+        if (j < ready) ready = wait_ready(fl, j, m + 1, -1);
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
@@ -1432,34 +1526,16 @@ lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     }
     part[g][tr] = mk(ar, ai);
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 64) {
         const cplx* yb = ybuf + static_cast<size_t>(b) * n;
-        cplx v0 = mk(0.0, 0.0), v1 = mk(0.0, 0.0);
-        if (lane < w) v0 = yb[k + lane] - (part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]);
-        if (lane + 32 < w)
-            v1 = yb[k + lane + 32] -
-                 (part[0][lane + 32] + part[1][lane + 32] + part[2][lane + 32] + part[3][lane + 32]);
-        // reciprocals of the diagonal, all lanes at once (off the sequential chain)
-        const cplx r0 = crecip(mk(dsm[lane * 65], dsm[4096 + lane * 65]));
-        const cplx r1 = crecip(mk(dsm[(lane + 32) * 65], dsm[4096 + (lane + 32) * 65]));
-#pragma unroll 1
-        for (int j = w - 1; j >= 0; --j) {  // rolled: one warp runs it once per block, keep it in the i-cache
-            if (j < 32) {
-                if (lane == j) v0 = v0 * r0;
-            } else {
-                if (lane == j - 32) v1 = v1 * r1;
-            }
-            const cplx src = j < 32 ? v0 : v1;
-            const cplx xj = mk(__shfl_sync(0xffffffffu, src.re, j & 31), __shfl_sync(0xffffffffu, src.im, j & 31));
-            if (lane < j) v0 = v0 - mk(dsm[j * 64 + lane], dsm[4096 + j * 64 + lane]) * xj;
-            if (lane + 32 < j) v1 = v1 - mk(dsm[j * 64 + lane + 32], dsm[4096 + j * 64 + lane + 32]) * xj;
-        }
-        if (lane < w) x[k + lane] = v0;
-        if (lane + 32 < w) x[k + lane + 32] = v1;
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_i(fl + m, 1);
+        vsm[tid] = tid < w ? yb[k + tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : mk(0.0, 0.0);
     }
+    __syncthreads();
+    const cplx xm = apply_diag<false>(dsm, vsm, part, w);
+    if (g == 0 && live) x[k + tr] = xm;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_i(fl + m, 1);
 }
 
 // ------------------------------------------------------------------ host
@@ -1960,8 +2036,8 @@ void LuWorkspace::ensure_solve(int batch, int n, int nblk) {
         FDS_CUDA(cudaMalloc(&ybuf, yneed * sizeof(cplx)));
         ybuf_cap = yneed;
     }
-    // pflag [batch][nblk], flags fwd / bwd [batch][nblk], tickets fwd / bwd [batch]
-    const size_t fneed = 3 * static_cast<size_t>(batch) * nblk + 2 * static_cast<size_t>(batch);
+    // pflag [batch][nblk], flags fwd / bwd [batch][nblk], tickets fwd / bwd
+    const size_t fneed = 3 * static_cast<size_t>(batch) * nblk + 2;
     if (fneed > sflag_cap) {
         if (sflags) cudaFree(sflags);
         sflags = nullptr;
@@ -1996,7 +2072,7 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
     int* ffl = pflag + static_cast<size_t>(pb.batch) * nblk;
     int* bfl = ffl + static_cast<size_t>(pb.batch) * nblk;
     int* tk = bfl + static_cast<size_t>(pb.batch) * nblk;
-    FDS_CUDA(cudaMemsetAsync(ffl, 0, (2 * static_cast<size_t>(pb.batch) * nblk + 2 * pb.batch) * sizeof(int), st));
+    FDS_CUDA(cudaMemsetAsync(ffl, 0, (2 * static_cast<size_t>(pb.batch) * nblk + 2) * sizeof(int), st));
     const size_t smem = 2 * 64 * 64 * sizeof(double);
     static bool attr = false;
     if (!attr) {
@@ -2004,12 +2080,12 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
         FDS_CUDA(cudaFuncSetAttribute(lu_bwd_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
     }
-    const dim3 g(nblk, pb.batch);
-    FDS_LAUNCH(lu_pivflag_kernel, g, 64, 0, st, pb.n, nb, pb.ipiv, pflag);
-    FDS_LAUNCH(lu_fwd_df_kernel, g, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, pb.ipiv, pflag,
+    FDS_LAUNCH(lu_pivflag_kernel, dim3(nblk, pb.batch), 64, 0, st, pb.n, nb, pb.ipiv, pflag);
+    const int ctas = nblk * pb.batch;
+    FDS_LAUNCH(lu_fwd_df_kernel, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, pb.ipiv, pflag,
                rhs, rstride, ws.ybuf, ffl, tk);
-    FDS_LAUNCH(lu_bwd_df_kernel, g, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, ws.ybuf, rhs,
-               rstride, bfl, tk + pb.batch);
+    FDS_LAUNCH(lu_bwd_df_kernel, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, ws.ybuf, rhs,
+               rstride, bfl, tk + 1);
 }
 
 namespace {
