@@ -1405,13 +1405,15 @@ __device__ __forceinline__ cplx apply_diag(const double* dsm, const cplx* v, cpl
     return y;
 }
 
-__global__ void __launch_bounds__(kDfThreads, 3)
-lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int nb, const int* ipiv,
+template <int NB>
+__global__ void __launch_bounds__(kDfThreads, 2)
+lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, const int* ipiv,
                  const int* pflag, const cplx* rhs, size_t rstride, cplx* ybuf, int* flags, int* tickets) {
     extern __shared__ double dsm[];  // unit-lower diagonal block
     __shared__ cplx part[4][64];
     __shared__ int s_m;
     const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int nb = NB, cpg = NB / 4;
     const int nblk = (n + nb - 1) / nb, batch = gridDim.x / nblk;
     if (tid == 0) s_m = atomicAdd(tickets, 1);
     __syncthreads();
@@ -1428,7 +1430,7 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     stage_diag(dsm, Are, Aim, k, w, ld);
     __syncthreads();
     invert_diag<true>(dsm, part, w);
-    const int tr = tid & 63, g = tid >> 6, cpg = nb >> 2;
+    const int tr = tid & 63, g = tid >> 6;
     const bool live = tr < w;
     int q = k + tr;
     if (live)
@@ -1444,25 +1446,23 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     for (int j = 0; j < m; ++j) {
         const int kj = j * nb;
         if (live && pf[j]) q = swap_forward(q, pv, kj, nb);
-        double lr[16], li[16];
+        double lr[cpg], li[cpg];
+        {
+            const double* pr = Are + static_cast<size_t>(kj + g * cpg) * ld + q;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            lr[c] = li[c] = 0.0;
-            if (c < cpg && live) {
-                const size_t gi = static_cast<size_t>(kj + g * cpg + c) * ld + q;
-                lr[c] = __ldg(Are + gi);
-                li[c] = __ldg(Aim + gi);
+            for (int c = 0; c < cpg; ++c) {
+                lr[c] = live ? __ldg(pr) : 0.0;
+                li[c] = live ? __ldg(pr + plane) : 0.0;
+                pr += ld;
             }
         }
         if (j > ready) ready = wait_ready(fl, j, m - 1, 1);
         __syncwarp();
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            if (c < cpg) {
-                const double2 y = __ldcg(reinterpret_cast<const double2*>(yb + kj + g * cpg + c));
-                ar -= lr[c] * y.x - li[c] * y.y;
-                ai -= lr[c] * y.y + li[c] * y.x;
-            }
+        for (int c = 0; c < cpg; ++c) {
+            const double2 y = __ldcg(reinterpret_cast<const double2*>(yb + kj + g * cpg + c));
+            ar -= lr[c] * y.x - li[c] * y.y;
+            ai -= lr[c] * y.y + li[c] * y.x;
         }
     }
     part[g][tr] = mk(ar, ai);
@@ -1476,13 +1476,15 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     if (tid == 0) st_release_i(fl + m, 1);
 }
 
-__global__ void __launch_bounds__(kDfThreads, 3)
-lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int nb, const cplx* ybuf, cplx* rhs,
+template <int NB>
+__global__ void __launch_bounds__(kDfThreads, 2)
+lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, const cplx* ybuf, cplx* rhs,
                  size_t rstride, int* flags, int* tickets) {
     extern __shared__ double dsm[];  // upper diagonal block
     __shared__ cplx part[4][64];
     __shared__ int s_m;
     const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int nb = NB, cpg = NB / 4;
     const int nblk = (n + nb - 1) / nb, batch = gridDim.x / nblk;
     if (tid == 0) s_m = atomicAdd(tickets, 1);
     __syncthreads();
@@ -1495,29 +1497,29 @@ lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     stage_diag(dsm, Are, Aim, k, w, ld);
     __syncthreads();
     invert_diag<false>(dsm, part, w);
-    const int tr = tid & 63, g = tid >> 6, cpg = nb >> 2;
+    const int tr = tid & 63, g = tid >> 6;
     const bool live = tr < w;
     double ar = 0.0, ai = 0.0;
     int ready = nblk;  // furthest block known published (warp-uniform)
     for (int j = nblk - 1; j > m; --j) {
         const int kj = j * nb, wj = min(nb, n - kj);
-        double ur[16], ui[16];
+        double ur[cpg], ui[cpg];
+        {
+            const double* pr = Are + static_cast<size_t>(kj + g * cpg) * ld + k + tr;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            ur[c] = ui[c] = 0.0;
-            const int col = g * cpg + c;
-            if (c < cpg && live && col < wj) {
-                const size_t gi = static_cast<size_t>(kj + col) * ld + k + tr;
-                ur[c] = __ldg(Are + gi);
-                ui[c] = __ldg(Aim + gi);
+            for (int c = 0; c < cpg; ++c) {
+                const bool on = live && g * cpg + c < wj;
+                ur[c] = on ? __ldg(pr) : 0.0;
+                ui[c] = on ? __ldg(pr + plane) : 0.0;
+                pr += ld;
             }
         }
         if (j < ready) ready = wait_ready(fl, j, m + 1, -1);
         __syncwarp();
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < cpg; ++c) {
             const int col = g * cpg + c;
-            if (c < cpg && col < wj) {
+            if (col < wj) {
                 const double2 v = __ldcg(reinterpret_cast<const double2*>(x + kj + col));
                 ar += ur[c] * v.x - ui[c] * v.y;
                 ai += ur[c] * v.y + ui[c] * v.x;
@@ -2074,18 +2076,22 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
     int* tk = bfl + static_cast<size_t>(pb.batch) * nblk;
     FDS_CUDA(cudaMemsetAsync(ffl, 0, (2 * static_cast<size_t>(pb.batch) * nblk + 2) * sizeof(int), st));
     const size_t smem = 2 * 64 * 64 * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        FDS_CUDA(cudaFuncSetAttribute(lu_fwd_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        FDS_CUDA(cudaFuncSetAttribute(lu_bwd_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
     FDS_LAUNCH(lu_pivflag_kernel, dim3(nblk, pb.batch), 64, 0, st, pb.n, nb, pb.ipiv, pflag);
     const int ctas = nblk * pb.batch;
-    FDS_LAUNCH(lu_fwd_df_kernel, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, pb.ipiv, pflag,
-               rhs, rstride, ws.ybuf, ffl, tk);
-    FDS_LAUNCH(lu_bwd_df_kernel, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, nb, ws.ybuf, rhs,
-               rstride, bfl, tk + 1);
+    auto go = [&](auto fwd, auto bwd) {
+        static bool attr = false;
+        if (!attr) {
+            FDS_CUDA(cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            FDS_CUDA(cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            attr = true;
+        }
+        FDS_LAUNCH(fwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, pb.ipiv, pflag, rhs, rstride,
+                   ws.ybuf, ffl, tk);
+        FDS_LAUNCH(bwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ws.ybuf, rhs, rstride, bfl,
+                   tk + 1);
+    };
+    if (nb == 64) go(lu_fwd_df_kernel<64>, lu_bwd_df_kernel<64>);
+    else go(lu_fwd_df_kernel<32>, lu_bwd_df_kernel<32>);
 }
 
 namespace {
