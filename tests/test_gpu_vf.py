@@ -246,6 +246,32 @@ def test_afs_modal_identical_sequence():
     assert worst_match(r["poles"], o["poles"]) < 1e-6
 
 
+@pytest.mark.parametrize("orf,test", [([2, 0, 1], [5, 3, 4]), ([1, 0, 2], [2, 5, 1]), ([2, 1, 0], [4, 0]),
+                                      ([1, 3], [3, 1, 0]), ([0, 2, 1], None), ([4, 1], [5, 0, 2])])
+def test_afs_channel_subsets_identical_sequence(orf, test):
+    """Unsorted / overlapping ORF and test sets (and the default all-channel
+    test set) through the device-resident iteration: the worst-ORF argmax, the
+    E2 max over test positions and the E1 series of a gathered channel subset
+    keep the reference's sequence. ([4, 1] is rank-deficient for the reference's
+    relocation: the product must raise the same error class.)"""
+    fx = ModalFixture(6)
+    kw = dict(omega_max=1.5 * fx.band, eta=0.35, period=20.0, initial_count=16, grid_points=1024,
+              time_points=256, e1_threshold=1e-2, e2_threshold=5e-2)
+    sel = dict(orf_indices=orf) if test is None else dict(orf_indices=orf, test_indices=test)
+    try:
+        o = O.run_afs(O.System.from_json(fx.system_json()), orf=orf, test=test if test is not None else [], **kw)
+    except O.OracleError as e:  # the reference fails on this set: the product must fail the same way
+        with pytest.raises(P.Error) as eg:
+            P.run_afs(_ModalSys(fx), **sel, **kw)
+        assert type(eg.value).__name__ == e.kind
+        return
+    r = P.run_afs(_ModalSys(fx), **sel, **kw)
+    assert r["n_c"] == o["n_c"] and r["converged"] == o["converged"]
+    np.testing.assert_array_equal(r["samples"], o["samples"])
+    np.testing.assert_array_equal(r["history"][:, :3], o["history"][:, :3])
+    np.testing.assert_allclose(r["history"][:, 7], o["history"][:, 7], rtol=1e-9)
+
+
 def test_afs_infinite_thresholds():
     fx = ModalFixture(4)
     r = P.run_afs(_ModalSys(fx), omega_max=1.5 * fx.band, eta=0.35, period=20.0, orf_indices=[0, 1],
