@@ -132,6 +132,22 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+def version() -> str:
+    return lib().fds_version().decode()
+
+
+def profile_enable(on: bool = True):
+    """Per-kernel-class device timings (CUDA events) and algorithmic work, as bench.py reads them."""
+    _check(lib().fds_profile_enable(1 if on else 0))
+
+
+def profile_read(kind: int):
+    """(launch count, total ms, total algorithmic work) of one profiler class (csrc/common.cuh kProf*)."""
+    c, ms, wk = ctypes.c_int(0), ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(lib().fds_profile_read(kind, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
+    return c.value, ms.value, wk.value
+
+
 def kernel_launches() -> int:
     return int(lib().fds_kernel_launches())
 

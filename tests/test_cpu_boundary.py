@@ -109,3 +109,9 @@ dist.destroy_process_group()
     outs = [p.communicate(timeout=120)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs)
     assert "OK 2" in outs[0]
+
+
+def test_version_string_names_the_target():
+    import paper_1511_04355_b200 as P
+
+    assert "sm_100a" in P.api.version()
