@@ -740,7 +740,7 @@ lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 // U12 = L11^{-1} P A12: per panel and matrix, lu_l11_inverse_kernel forms the
 // unit-lower 64x64 inverse and resolves the panel's 64 sequential row swaps
 // into one gather (source row of every panel row and of every outside row a
-// pivot names); lu_swap_apply_kernel then permutes each 64-column strip with
+// pivot names); lu_swap_apply_kernel then permutes each 32-column strip with
 // independent loads and multiplies by L11^{-1} on the FP64 tensor pipe.
 constexpr size_t kLinvStride = 2 * 64 * 64 + 128;  // doubles per matrix: Linv planes + swap map (ints)
 constexpr int kInvThreads = 256;
@@ -891,22 +891,26 @@ lu_l11_inverse_kernel(const double* A, size_t mstride, size_t plane, int n, int 
 
 constexpr int SAS = 68;  // padded smem stride (≡ 4 mod 16 doubles)
 constexpr int kApplyThreads = 256;
+constexpr int kApplyCols = 32;  // strip width: L11^{-1} + one strip = 104 KB smem, 2 CTAs per SM
 
-__global__ void __launch_bounds__(kApplyThreads)
+// One CTA per 32-column strip of the trailing columns: the panel rows of the
+// strip are permuted through registers (sources in smem, or straight from HBM
+// for the few outside rows a pivot names — every outside row receives a panel
+// row, so no staging buffer is needed), the outside rows are written from the
+// untouched strip, and U12 = L11^{-1} (P A12) runs on DMMA.
+__global__ void __launch_bounds__(kApplyThreads, 2)
 lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv) {
     extern __shared__ __align__(16) double ssm[];
     double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
     double* Li = Lr + 64 * SAS;
-    double* Xr = Li + 64 * SAS;       // [n][kk]
-    double* Xi = Xr + 64 * SAS;
-    double* Er = Xi + 64 * SAS;       // [n][j] original values of the outside rows
-    double* Ei = Er + 64 * 65;
+    double* Xr = Li + 64 * SAS;       // [n][kk], n < kApplyCols
+    double* Xi = Xr + kApplyCols * SAS;
     __shared__ SwapMap map;
     const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
-    const int col0 = k + 64 + blockIdx.x * 64;
-    const int ncols = min(64, n - col0);
+    const int col0 = k + 64 + blockIdx.x * kApplyCols;
+    const int ncols = min(kApplyCols, n - col0);
     const double* rec = linv + static_cast<size_t>(b) * kLinvStride;
     const double* L = rec;
     {
@@ -919,10 +923,8 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         Lr[kk * SAS + m] = L[kk * 64 + m];
         Li[kk * SAS + m] = L[64 * 64 + kk * 64 + m];
     }
-    __syncthreads();
-    const int ne = map.next;
-    // V = original panel rows (coalesced) and outside rows (one element per column)
-    for (int q = tid; q < 64 * 64; q += blockDim.x) {
+    // original panel rows of the strip (coalesced)
+    for (int q = tid; q < kApplyCols * 64; q += blockDim.x) {
         const int nn = q / 64, kk = q % 64;
         double vr = 0.0, vi = 0.0;
         if (nn < ncols) {
@@ -933,58 +935,54 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         Xr[nn * SAS + kk] = vr;
         Xi[nn * SAS + kk] = vi;
     }
-    for (int q = tid; q < 64 * ne; q += blockDim.x) {
-        const int nn = q / ne, j = q % ne;
-        double vr = 0.0, vi = 0.0;
-        if (nn < ncols) {
-            const size_t gi = static_cast<size_t>(col0 + nn) * ld + map.erow[j];
-            vr = Are[gi];
-            vi = Aim[gi];
-        }
-        Er[nn * 65 + j] = vr;
-        Ei[nn * 65 + j] = vi;
-    }
     __syncthreads();
-    auto vget = [&](int nn, int v, double& vr, double& vi) {
-        if (v < 64) { vr = Xr[nn * SAS + v]; vi = Xi[nn * SAS + v]; }
-        else { vr = Er[nn * 65 + v - 64]; vi = Ei[nn * 65 + v - 64]; }
-    };
-    // outside rows receive their sources
-    for (int q = tid; q < 64 * ne; q += blockDim.x) {
-        const int nn = q / ne, j = q % ne;
-        if (nn < ncols) {
-            double vr, vi;
-            vget(nn, map.esrc[j], vr, vi);
-            const size_t gi = static_cast<size_t>(col0 + nn) * ld + map.erow[j];
-            Are[gi] = vr;
-            Aim[gi] = vi;
-        }
-    }
-    // panel rows permuted in place through registers
-    {
-        constexpr int kPer = 64 * 64 / kApplyThreads;
-        double pr[kPer], pi[kPer];
+    const int ne = map.next;
+    // permuted panel rows into registers: panel sources from smem, outside
+    // sources (their original values) from HBM before any outside row is written
+    constexpr int kPer = kApplyCols * 64 / kApplyThreads;
+    double pr[kPer], pi[kPer];
 #pragma unroll
-        for (int p = 0; p < kPer; ++p) {
-            const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
-            vget(nn, map.psrc[kk], pr[p], pi[p]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int p = 0; p < kPer; ++p) {
-            const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
-            Xr[nn * SAS + kk] = pr[p];
-            Xi[nn * SAS + kk] = pi[p];
+    for (int p = 0; p < kPer; ++p) {
+        const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
+        const int v = map.psrc[kk];
+        if (v < 64) {
+            pr[p] = Xr[nn * SAS + v];
+            pi[p] = Xi[nn * SAS + v];
+        } else {
+            pr[p] = pi[p] = 0.0;
+            if (nn < ncols) {
+                const size_t gi = static_cast<size_t>(col0 + nn) * ld + map.erow[v - 64];
+                pr[p] = Are[gi];
+                pi[p] = Aim[gi];
+            }
         }
     }
     __syncthreads();
-    // 8 warps: 2 (rows of 32) x 4 (columns of 16)
+    // outside rows receive their (panel-row) sources from the untouched strip
+    for (int q = tid; q < kApplyCols * ne; q += blockDim.x) {
+        const int nn = q / ne, j = q % ne;
+        if (nn < ncols) {
+            const int v = map.esrc[j];
+            const size_t gi = static_cast<size_t>(col0 + nn) * ld + map.erow[j];
+            Are[gi] = Xr[nn * SAS + v];
+            Aim[gi] = Xi[nn * SAS + v];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < kPer; ++p) {
+        const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
+        Xr[nn * SAS + kk] = pr[p];
+        Xi[nn * SAS + kk] = pi[p];
+    }
+    __syncthreads();
+    // 8 warps: 2 (rows of 32) x 4 (columns of 8)
     const int wm = warp & 1, wn = warp >> 1;
-    double acr[4][2][2] = {}, aci[4][2][2] = {};
+    double acr[4][2] = {}, aci[4][2] = {};
 #pragma unroll 4
     for (int k4 = 0; k4 < 64; k4 += 4) {
         const int kr = k4 + (lane & 3);
-        double ar[4], ai[4], an[4], br[2], bi[2];
+        double ar[4], ai[4], an[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
             const int m = wm * 32 + mi * 8 + (lane >> 2);
@@ -992,41 +990,31 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
             ai[mi] = Li[kr * SAS + m];
             an[mi] = -ai[mi];
         }
+        const int nn = wn * 8 + (lane >> 2);
+        const double br = Xr[nn * SAS + kr], bi = Xi[nn * SAS + kr];
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-            const int nn = wn * 16 + ni * 8 + (lane >> 2);
-            br[ni] = Xr[nn * SAS + kr];
-            bi[ni] = Xi[nn * SAS + kr];
+        for (int mi = 0; mi < 4; ++mi) {
+            dmma(acr[mi][0], acr[mi][1], ar[mi], br);
+            dmma(aci[mi][0], aci[mi][1], ar[mi], bi);
         }
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                dmma(acr[mi][ni][0], acr[mi][ni][1], ar[mi], br[ni]);
-                dmma(aci[mi][ni][0], aci[mi][ni][1], ar[mi], bi[ni]);
-            }
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                dmma(acr[mi][ni][0], acr[mi][ni][1], an[mi], bi[ni]);
-                dmma(aci[mi][ni][0], aci[mi][ni][1], ai[mi], br[ni]);
-            }
+        for (int mi = 0; mi < 4; ++mi) {
+            dmma(acr[mi][0], acr[mi][1], an[mi], bi);
+            dmma(aci[mi][0], aci[mi][1], ai[mi], br);
+        }
     }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
         const int row = k + wm * 32 + mi * 8 + (lane >> 2);
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int cl = wn * 16 + ni * 8 + 2 * (lane & 3) + e;
-                if (cl < ncols) {
-                    const size_t gi = static_cast<size_t>(col0 + cl) * ld + row;
-                    Are[gi] = acr[mi][ni][e];
-                    Aim[gi] = aci[mi][ni][e];
-                }
+        for (int e = 0; e < 2; ++e) {
+            const int cl = wn * 8 + 2 * (lane & 3) + e;
+            if (cl < ncols) {
+                const size_t gi = static_cast<size_t>(col0 + cl) * ld + row;
+                Are[gi] = acr[mi][e];
+                Aim[gi] = aci[mi][e];
             }
+        }
     }
 }
 
@@ -1727,7 +1715,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
     cudaEvent_t te;
     profiler().begin(st, kProfLuTrsm, 0.0, te);
     if (NB == 64 && w == 64) {
-        const size_t asmem = (4 * 64 * SAS + 2 * 64 * 65) * sizeof(double);
+        const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
         const size_t ismem = (4 * 64 * 65 + 2 * 48 * 17) * sizeof(double);
         static bool aset = false;
         if (!aset) {
@@ -1739,7 +1727,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
         }
         FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, kInvThreads, ismem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
                    pb.ipiv, linv);
-        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, 64), pb.batch), kApplyThreads, asmem, st, pb.A, pb.mstride,
+        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A, pb.mstride,
                    pb.plane, pb.n, pb.ld, k, linv);
     } else {
         dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
