@@ -245,31 +245,40 @@ int fds_bem_create(const fds_bem_desc* d, fds_bem** out) {
         if (!d || !out) throw ValidationError("fds_bem_create: null argument");
         if (d->n_elements < 1 || d->n_vertices < 3 || !d->vertices || !d->triangles || !d->traction)
             throw ValidationError("fds_bem_create: empty mesh or load");
+        if (d->n_channels > 0 && !d->channels) throw ValidationError("fds_bem_create: null channel list");
+        if (d->max_batch < 0) throw ValidationError("fds_bem_create: max_batch must be >= 0");
+        // host-side validation first: bad input is reported as such, GPU or not
+        const int n = 3 * d->n_elements;
+        const BemParams params = make_bem_params(d->shear_modulus, d->poisson_ratio, d->density);
+        for (int i = 0; i < 3 * d->n_vertices; ++i)
+            if (!std::isfinite(d->vertices[i])) throw ValidationError("fds_bem_create: non-finite vertex coordinate");
+        for (int i = 0; i < n; ++i)
+            if (!std::isfinite(d->traction[i])) throw ValidationError("fds_bem_create: non-finite traction");
+        std::vector<double> geo;
+        std::vector<int> pairs, ptr;
+        bem_build_geometry(d->vertices, d->n_vertices, d->triangles, d->n_elements, geo, pairs, ptr);
+        std::vector<int> chans;
+        if (d->n_channels > 0) {
+            for (int i = 0; i < d->n_channels; ++i) {
+                if (d->channels[i] < 0 || d->channels[i] >= n)
+                    throw ValidationError("fds_bem_create: channel DOF out of range");
+                chans.push_back(d->channels[i]);
+            }
+        } else {
+            for (int i = 0; i < n; ++i) chans.push_back(i);
+        }
         device_info();
         auto* h = new fds_bem;
         try {
             h->ne = d->n_elements;
-            h->n = 3 * h->ne;
+            h->n = n;
             h->ld = lu_ld(h->n);
             h->plane = lu_plane(h->n);
             h->mstride = 2 * h->plane;
             h->max_batch = d->max_batch;
             h->dev.ne = h->ne;
-            h->dev.params = make_bem_params(d->shear_modulus, d->poisson_ratio, d->density);
-            std::vector<double> geo;
-            std::vector<int> pairs, ptr;
-            bem_build_geometry(d->vertices, d->n_vertices, d->triangles, h->ne, geo, pairs, ptr);
+            h->dev.params = params;
             h->dev.npairs = static_cast<int>(pairs.size() / 3);
-            std::vector<int> chans;
-            if (d->n_channels > 0) {
-                for (int i = 0; i < d->n_channels; ++i) {
-                    if (d->channels[i] < 0 || d->channels[i] >= h->n)
-                        throw ValidationError("fds_bem_create: channel DOF out of range");
-                    chans.push_back(d->channels[i]);
-                }
-            } else {
-                for (int i = 0; i < h->n; ++i) chans.push_back(i);
-            }
             h->K = static_cast<int>(chans.size());
             FDS_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
             for (auto& e : h->ev) FDS_CUDA(cudaEventCreate(&e));

@@ -115,3 +115,35 @@ def test_version_string_names_the_target():
     import paper_1511_04355_b200 as P
 
     assert "sm_100a" in P.api.version()
+
+
+@pytest.mark.parametrize("case", ["vertex_index", "degenerate", "material", "channel", "nan_vertex", "nan_traction"])
+def test_bem_create_validates_on_the_host(case):
+    """fds_bem_create rejects bad meshes / loads / materials / channels with
+    ValidationError before touching the device (so also without a GPU)."""
+    import numpy as np
+
+    import paper_1511_04355_b200 as P
+    from paper_1511_04355_b200 import mesh
+
+    V, F = mesh.icosphere(1)
+    tr = mesh.pressure_traction(V, F)
+    kw = {}
+    if case == "vertex_index":
+        F = F.copy()
+        F[3, 1] = len(V) + 5
+    elif case == "degenerate":
+        F = F.copy()
+        F[2] = [F[2, 0], F[2, 0], F[2, 1]]
+    elif case == "material":
+        kw = dict(nu=0.5)
+    elif case == "channel":
+        kw = dict(channels=[0, 3 * len(F)])
+    elif case == "nan_vertex":
+        V = V.copy()
+        V[0, 0] = np.nan
+    elif case == "nan_traction":
+        tr = tr.copy()
+        tr[1, 2] = np.inf
+    with pytest.raises(P.ValidationError):
+        P.BemSystem(V, F, tr, **kw)
