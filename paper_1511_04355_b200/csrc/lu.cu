@@ -1018,6 +1018,70 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
     }
 }
 
+// Rank-16 update of a sub-panel's window inside the 64-wide panel,
+// A[r][c0:c1) -= L[r][ks:ks+16) U[ks:ks+16)[c0:c1) for rows r >= ks + 16,
+// with the DMMA fragments loaded straight from HBM / L2 (sector-exact for the
+// m8n8k4 layouts) and no shared memory, so four CTAs per SM keep the short
+// load -> 16 DMMA -> store sequence of each tile overlapped.
+constexpr int kWinThreads = 256;  // 8 warps x one 8-row m-tile each: 64 rows per CTA
+
+__global__ void __launch_bounds__(kWinThreads, 4)
+lu_window_update_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int ks, int c0, int c1) {
+    const int b = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int r = ks + 16 + blockIdx.x * 64 + warp * 8 + (lane >> 2);  // fragment row (A / C)
+    const bool rok = r < n;
+    const int q = lane & 3;
+    // L fragments for the four k4 steps (negated: the update subtracts)
+    double nar[4], ai[4], nai[4];
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+        const size_t gi = static_cast<size_t>(ks + 4 * k4 + q) * ld + r;
+        const double xr = rok ? Are[gi] : 0.0, xi = rok ? Aim[gi] : 0.0;
+        nar[k4] = -xr;
+        ai[k4] = xi;
+        nai[k4] = -xi;
+    }
+    for (int n0 = c0; n0 < c1; n0 += 16) {  // two 8-column n-tiles per pass
+        double acr[2][2], aci[2][2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + 8 * t + 2 * q + e;
+                const size_t gi = static_cast<size_t>(col) * ld + r;
+                const bool ok = rok && col < c1;
+                acr[t][e] = ok ? Are[gi] : 0.0;
+                aci[t][e] = ok ? Aim[gi] : 0.0;
+            }
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int col = n0 + 8 * t + (lane >> 2);
+                const size_t gi = static_cast<size_t>(col) * ld + ks + 4 * k4 + q;
+                const double br = col < c1 ? Are[gi] : 0.0, bi = col < c1 ? Aim[gi] : 0.0;
+                dmma(acr[t][0], acr[t][1], nar[k4], br);
+                dmma(acr[t][0], acr[t][1], ai[k4], bi);
+                dmma(aci[t][0], aci[t][1], nar[k4], bi);
+                dmma(aci[t][0], aci[t][1], nai[k4], br);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + 8 * t + 2 * q + e;
+                if (rok && col < c1) {
+                    const size_t gi = static_cast<size_t>(col) * ld + r;
+                    Are[gi] = acr[t][e];
+                    Aim[gi] = aci[t][e];
+                }
+            }
+    }
+}
+
 // ------------------------------------------------------------------ 16-wide sub-panels
 // For batches the 64-wide panel is factored as four 16-wide sub-panels: a
 // 16-wide panel needs a quarter of the on-chip memory per matrix, so ~4x more
@@ -1867,6 +1931,14 @@ int lu_panel_width(int n) {
 
 namespace {
 
+bool window_kernel() {  // FDSWEEP_WINDOW=gemm routes the sub-panel window updates through lu_gemm_kernel
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_WINDOW");
+        return !(e && std::string(e) == "gemm");
+    }();
+    return on;
+}
+
 void subpanel_block(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t st, bool coop) {
     cudaEvent_t pe;
     profiler().begin(st, kProfLuPanel, 0.0, pe);
@@ -1877,9 +1949,15 @@ void subpanel_block(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStre
         FDS_LAUNCH(lu_sub_swap_trsm_kernel, pb.batch, 64, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, ks,
                    pb.ipiv);
         if (ks + kSub < k + 64) {
-            // rank-16 update of the panel's remaining columns on the DMMA GEMM
-            // (K = 16, column window [ks+16, k+64))
-            gemm_step(pb, ks, kSub, st, ks + kSub, k + 64);
+            // rank-16 update of the panel's remaining columns, window [ks+16, k+64)
+            const int rows = pb.n - ks - kSub;
+            if (rows > 0) {
+                if (window_kernel())
+                    FDS_LAUNCH(lu_window_update_kernel, dim3(ceil_div(rows, 64), pb.batch), kWinThreads, 0, st, pb.A,
+                               pb.mstride, pb.plane, pb.n, pb.ld, ks, ks + kSub, k + 64);
+                else
+                    gemm_step(pb, ks, kSub, st, ks + kSub, k + 64);
+            }
         }
     }
     profiler().enabled = keep;
