@@ -1765,8 +1765,23 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+constexpr size_t kInvSmem = (4 * 64 * 65 + 2 * 48 * 17) * sizeof(double);
+
+// L11^{-1} and the swap map of the 64-wide panel at k (lu_l11_inverse_kernel)
+void l11_inverse_step(const LuProblem& pb, int k, cudaStream_t st, double* linv) {
+    static bool iset = false;
+    if (!iset) {
+        FDS_CUDA(cudaFuncSetAttribute(lu_l11_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kInvSmem)));
+        iset = true;
+    }
+    FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, kInvThreads, kInvSmem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
+               pb.ipiv, linv);
+}
+
+// inverse_ready: the look-ahead schedule already formed L11^{-1} on its side stream
 template <int NB>
-void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv) {
+void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv, bool inverse_ready = false) {
     const int rest = pb.n - k - w;
     if (rest <= 0) return;
     static bool attr_set = false;
@@ -1780,17 +1795,13 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv)
     profiler().begin(st, kProfLuTrsm, 0.0, te);
     if (NB == 64 && w == 64) {
         const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
-        const size_t ismem = (4 * 64 * 65 + 2 * 48 * 17) * sizeof(double);
         static bool aset = false;
         if (!aset) {
             FDS_CUDA(cudaFuncSetAttribute(lu_swap_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(asmem)));
-            FDS_CUDA(cudaFuncSetAttribute(lu_l11_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(ismem)));
             aset = true;
         }
-        FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, kInvThreads, ismem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
-                   pb.ipiv, linv);
+        if (!inverse_ready) l11_inverse_step(pb, k, st, linv);
         FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A, pb.mstride,
                    pb.plane, pb.n, pb.ld, k, linv);
     } else {
@@ -2042,19 +2053,29 @@ void lu_factor_lookahead(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) 
     ws.ensure_side();
     cudaStream_t s_hi = ws.side;
     cudaEvent_t ev_a = ws.ev[0], ev_p = ws.ev[1];
-    double* linv = ws.linv(pb.batch);
+    // two L11^{-1} slots: the side stream forms the next panel's inverse while
+    // the current one is still applied
+    double* linv_buf = ws.linv(2 * pb.batch);
+    double* slot[2] = {linv_buf, linv_buf + static_cast<size_t>(pb.batch) * kLinvStride};
     subpanel_block(pb, ws, 0, 64, st, true);
+    bool ready = false;
     for (int k = 0; k < pb.n; k += 64) {
         const int w = std::min(64, pb.n - k);
-        trsm_step<64>(pb, k, w, st, linv);
+        double* linv = slot[(k / 64) & 1];
+        trsm_step<64>(pb, k, w, st, linv, ready);
         const int nx = k + w;
         if (nx >= pb.n) break;
         const int wn = std::min(64, pb.n - nx);
+        ready = false;
         if (wn == 64) {
             gemm_step(pb, k, w, st, nx, nx + 64);
             FDS_CUDA(cudaEventRecord(ev_a, st));
             FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_a, 0));
             subpanel_block(pb, ws, nx, 64, s_hi, false);
+            if (pb.n - nx - 64 > 0) {  // trsm_step of nx has trailing columns to apply
+                l11_inverse_step(pb, nx, s_hi, slot[(nx / 64) & 1]);
+                ready = true;
+            }
             FDS_CUDA(cudaEventRecord(ev_p, s_hi));
             gemm_step(pb, k, w, st, nx + 64, pb.n);
             FDS_CUDA(cudaStreamWaitEvent(st, ev_p, 0));
