@@ -624,6 +624,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+template <int W>
 __global__ void __launch_bounds__(kGemmThreads, 2)
 lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* A,
                    size_t mstride, size_t plane, int n, int ld, int k, int c0) {
@@ -633,7 +634,7 @@ lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const unsigned raw = static_cast<unsigned>(__cvta_generic_to_shared(gsm_raw));
     double* gsm = gsm_raw + ((128u - (raw & 127u)) & 127u) / sizeof(double);
     uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + kGemmSmemDoubles);
-    constexpr int w = 64, nk = w / GBK;
+    constexpr int w = W, nk = w / GBK;
     const int b = blockIdx.z;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
@@ -1875,17 +1876,22 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
     dim3 gg(ceil_div(rest, GBM), ceil_div(c1 - c0, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
-    if (w == 64 && use_tma_gemm()) {
+    if ((w == 64 || w == 128) && use_tma_gemm()) {
         static bool tset = false;
         if (!tset) {
-            FDS_CUDA(cudaFuncSetAttribute(lu_gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            FDS_CUDA(cudaFuncSetAttribute(lu_gemm_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kGemmSmemDoubles * sizeof(double) + kTmaSmemPad)));
+            FDS_CUDA(cudaFuncSetAttribute(lu_gemm_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kGemmSmemDoubles * sizeof(double) + kTmaSmemPad)));
             tset = true;
         }
         const TmaMaps& tm = tma_maps(pb);
-        FDS_LAUNCH(lu_gemm_tma_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st, tm.a,
-                   tm.b, pb.A,
-                   pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
+        if (w == 128)
+            FDS_LAUNCH(lu_gemm_tma_kernel<128>, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st,
+                       tm.a, tm.b, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
+        else
+            FDS_LAUNCH(lu_gemm_tma_kernel<64>, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st,
+                       tm.a, tm.b, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
     } else {
         FDS_LAUNCH(lu_gemm_kernel, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double), st, pb.A, pb.mstride,
                    pb.plane, pb.n, pb.ld, k, w, c0, c1);
