@@ -899,8 +899,12 @@ constexpr int kApplyCols = 32;  // strip width: L11^{-1} + one strip = 104 KB sm
 // for the few outside rows a pivot names — every outside row receives a panel
 // row, so no staging buffer is needed), the outside rows are written from the
 // untouched strip, and U12 = L11^{-1} (P A12) runs on DMMA.
+// mode 0: swap + TRSM; 1: swap only (the panel's interchanges applied to a
+// column range, e.g. an earlier panel's L columns); 2: TRSM only (rows already
+// in place). Columns [cb, ce).
 __global__ void __launch_bounds__(kApplyThreads, 2)
-lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv) {
+lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv, int cb, int ce,
+                     int mode) {
     extern __shared__ __align__(16) double ssm[];
     double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
     double* Li = Lr + 64 * SAS;
@@ -910,8 +914,8 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
     const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
-    const int col0 = k + 64 + blockIdx.x * kApplyCols;
-    const int ncols = min(kApplyCols, n - col0);
+    const int col0 = cb + blockIdx.x * kApplyCols;
+    const int ncols = min(kApplyCols, ce - col0);
     const double* rec = linv + static_cast<size_t>(b) * kLinvStride;
     const double* L = rec;
     {
@@ -919,11 +923,12 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         int* dst = reinterpret_cast<int*>(&map);
         for (int q = tid; q < static_cast<int>(sizeof(SwapMap) / sizeof(int)); q += blockDim.x) dst[q] = src[q];
     }
-    for (int q = tid; q < 64 * 64; q += blockDim.x) {
-        const int kk = q / 64, m = q % 64;
-        Lr[kk * SAS + m] = L[kk * 64 + m];
-        Li[kk * SAS + m] = L[64 * 64 + kk * 64 + m];
-    }
+    if (mode != 1)
+        for (int q = tid; q < 64 * 64; q += blockDim.x) {
+            const int kk = q / 64, m = q % 64;
+            Lr[kk * SAS + m] = L[kk * 64 + m];
+            Li[kk * SAS + m] = L[64 * 64 + kk * 64 + m];
+        }
     // original panel rows of the strip (coalesced)
     for (int q = tid; q < kApplyCols * 64; q += blockDim.x) {
         const int nn = q / 64, kk = q % 64;
@@ -937,7 +942,7 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         Xi[nn * SAS + kk] = vi;
     }
     __syncthreads();
-    const int ne = map.next;
+    const int ne = mode == 2 ? 0 : map.next;
     // permuted panel rows into registers: panel sources from smem, outside
     // sources (their original values) from HBM before any outside row is written
     constexpr int kPer = kApplyCols * 64 / kApplyThreads;
@@ -945,7 +950,7 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
 #pragma unroll
     for (int p = 0; p < kPer; ++p) {
         const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
-        const int v = map.psrc[kk];
+        const int v = mode == 2 ? kk : map.psrc[kk];
         if (v < 64) {
             pr[p] = Xr[nn * SAS + v];
             pi[p] = Xi[nn * SAS + v];
@@ -970,6 +975,18 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         }
     }
     __syncthreads();
+    if (mode == 1) {  // permuted panel rows straight back
+#pragma unroll
+        for (int p = 0; p < kPer; ++p) {
+            const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
+            if (nn < ncols) {
+                const size_t gi = static_cast<size_t>(col0 + nn) * ld + k + kk;
+                Are[gi] = pr[p];
+                Aim[gi] = pi[p];
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int p = 0; p < kPer; ++p) {
         const int q = tid + kApplyThreads * p, nn = q / 64, kk = q % 64;
@@ -1366,13 +1383,23 @@ __device__ __forceinline__ int swap_backward(int q, const int* pv, int k, int w)
     return q;
 }
 
-__global__ void __launch_bounds__(64)
-lu_pivflag_kernel(int n, int nb, const int* ipiv, int* pflag) {
-    const int b = blockIdx.y, m = blockIdx.x, nblk = (n + nb - 1) / nb;
-    const int r = m * nb + threadIdx.x;
-    const bool moved = threadIdx.x < nb && r < n && ipiv[static_cast<size_t>(b) * n + r] != r;
+// Interchange groups: 128-row super-panels below ks, nb-row panels from ks on.
+struct SwapGroups {
+    int n, nb, ks;
+    __device__ __forceinline__ int count() const { return (ks >> 7) + (n - ks + nb - 1) / nb; }
+    __device__ __forceinline__ int of(int r) const { return r < ks ? r >> 7 : (ks >> 7) + (r - ks) / nb; }
+    __device__ __forceinline__ int start(int g) const { return g < (ks >> 7) ? g << 7 : ks + (g - (ks >> 7)) * nb; }
+    __device__ __forceinline__ int size(int g) const { return min(g < (ks >> 7) ? 128 : nb, n - start(g)); }
+};
+
+// pflag[b][g] = interchange group g has an interchange
+__global__ void __launch_bounds__(128)
+lu_pivflag_kernel(SwapGroups sg, const int* ipiv, int* pflag) {
+    const int b = blockIdx.y, g = blockIdx.x;
+    const int r = sg.start(g) + threadIdx.x;
+    const bool moved = threadIdx.x < sg.size(g) && ipiv[static_cast<size_t>(b) * sg.n + r] != r;
     const int any = __syncthreads_or(moved);
-    if (threadIdx.x == 0) pflag[static_cast<size_t>(b) * nblk + m] = any;
+    if (threadIdx.x == 0) pflag[static_cast<size_t>(b) * sg.count() + g] = any;
 }
 
 // diagonal block rows/cols < w of matrix (Are, Aim) at (k, k) into smem, column-major [64][64] re then im
@@ -1460,7 +1487,7 @@ __device__ __forceinline__ cplx apply_diag(const double* dsm, const cplx* v, cpl
 
 template <int NB>
 __global__ void __launch_bounds__(kDfThreads, 2)
-lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, const int* ipiv,
+lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int ks, const int* ipiv,
                  const int* pflag, const cplx* rhs, size_t rstride, cplx* ybuf, int* flags, int* tickets) {
     extern __shared__ double dsm[];  // unit-lower diagonal block
     __shared__ cplx part[4][64];
@@ -1476,7 +1503,8 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, c
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     const int* pv = ipiv + static_cast<size_t>(b) * n;
-    const int* pf = pflag + static_cast<size_t>(b) * nblk;
+    const SwapGroups sg{n, nb, ks};
+    const int* pf = pflag + static_cast<size_t>(b) * sg.count();
     int* fl = flags + static_cast<size_t>(b) * nblk;
     cplx* yb = ybuf + static_cast<size_t>(b) * n;
     __shared__ cplx vsm[64];
@@ -1487,8 +1515,8 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, c
     const bool live = tr < w;
     int q = k + tr;
     if (live)
-        for (int p = m; p >= 0; --p)
-            if (pf[p]) q = swap_backward(q, pv, p * nb, min(nb, n - p * nb));
+        for (int p = sg.of(k); p >= 0; --p)
+            if (pf[p]) q = swap_backward(q, pv, sg.start(p), sg.size(p));
     double ar = 0.0, ai = 0.0;
     if (live && g == 0) {
         const cplx v = rhs[static_cast<size_t>(b) * rstride + q];
@@ -1498,7 +1526,10 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, c
     int ready = -1;  // furthest block known published (warp-uniform)
     for (int j = 0; j < m; ++j) {
         const int kj = j * nb;
-        if (live && pf[j]) q = swap_forward(q, pv, kj, nb);
+        if (live) {
+            const int gj = sg.of(kj);
+            if (sg.start(gj) == kj && pf[gj]) q = swap_forward(q, pv, kj, sg.size(gj));
+        }
         double lr[cpg], li[cpg];
         {
             const double* pr = Are + static_cast<size_t>(kj + g * cpg) * ld + q;
@@ -1803,8 +1834,8 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv,
             aset = true;
         }
         if (!inverse_ready) l11_inverse_step(pb, k, st, linv);
-        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A, pb.mstride,
-                   pb.plane, pb.n, pb.ld, k, linv);
+        FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
+                   pb.mstride, pb.plane, pb.n, pb.ld, k, linv, k + 64, pb.n, 0);
     } else {
         dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
         FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, kTrsmThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
@@ -1861,8 +1892,11 @@ const TmaMaps& tma_maps(const LuProblem& pb) {
 }
 
 // A22[:, c0:c1) -= L21 U12[:, c0:c1) for the rows below the panel (c0 >= k + w).
-void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, int c1 = -1) {
-    const int rest = pb.n - k - w;
+// A[k+w : r1)[c0 : c1) -= L U with the panel's w columns / rows (defaults: the
+// whole trailing matrix)
+void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, int c1 = -1, int r1 = -1) {
+    if (r1 < 0) r1 = pb.n;
+    const int rest = r1 - k - w;
     if (rest <= 0) return;
     if (c0 < 0) c0 = k + w;
     if (c1 < 0) c1 = pb.n;
@@ -2094,8 +2128,64 @@ void lu_factor_lookahead(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) 
 
 }  // namespace
 
+namespace {
+
+bool super_panels() {  // FDSWEEP_SUPER=0 (or FDSWEEP_SOLVE=blocked) keeps one trailing update per 64-column panel
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_SUPER");
+        const char* sv = std::getenv("FDSWEEP_SOLVE");
+        return !(e && std::string(e) == "0") && !(sv && std::string(sv) == "blocked");
+    }();
+    return on;
+}
+
+template <class F>
+void profiler_scope_trsm(cudaStream_t st, F f, double work) {
+    cudaEvent_t e;
+    profiler().begin(st, kProfLuTrsm, 0.0, e);
+    f();
+    profiler().end(st, e, kProfLuTrsm, work);
+}
+
+void swap_cols(const LuProblem& pb, int k, int cb, int ce, int mode, const double* linv, cudaStream_t st) {
+    if (ce <= cb) return;
+    const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
+    FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(ce - cb, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
+               pb.mstride, pb.plane, pb.n, pb.ld, k, linv, cb, ce, mode);
+}
+
+// Two 64-column panels P1 = [k, k+64), P2 = [k+64, k+128) with one rank-128
+// trailing update: P1 is factored, swapped into and solved against the
+// trailing columns (U12_1) and applied to P2's columns only; P2 is factored,
+// its interchanges are applied to P1's L columns and to the trailing columns,
+// P2's rows of the trailing columns take P1's update, U12_2 = L22^{-1} A12_2,
+// and rows/columns >= k+128 take [L21_1 L21_2][U12_1; U12_2] in one pass —
+// each trailing C tile is loaded and stored once per 128 columns of k instead
+// of twice. Inside the 128-column super-panel the interchanges are in LAPACK
+// order (P2's reach P1's L columns), across super-panels in LINPACK order.
+void super_panel_step(const LuProblem& pb, LuWorkspace& ws, int k, cudaStream_t st) {
+    double* linv = ws.linv(pb.batch);
+    const int k2 = k + 64, rest = pb.n - k - 128;
+    subpanel_block(pb, ws, k, 64, st, true);
+    trsm_step<64>(pb, k, 64, st, linv);
+    gemm_step(pb, k, 64, st, k2, k2 + 64);
+    subpanel_block(pb, ws, k2, 64, st, true);
+    profiler_scope_trsm(st, [&] {
+        l11_inverse_step(pb, k2, st, linv);
+        swap_cols(pb, k2, k, k2, 1, linv, st);
+        swap_cols(pb, k2, k + 128, pb.n, 1, linv, st);
+    }, 0.0);
+    if (rest <= 0) return;
+    gemm_step(pb, k, 64, st, k + 128, pb.n, k + 128);
+    profiler_scope_trsm(st, [&] { swap_cols(pb, k2, k + 128, pb.n, 2, linv, st); }, 4.0 * 64 * 64 * rest * pb.batch);
+    gemm_step(pb, k, 128, st);
+}
+
+}  // namespace
+
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     FDS_CUDA(cudaMemsetAsync(pb.info, 0, pb.batch * sizeof(int), st));
+    ws.super_end = 0;
     if (!use_calu() && lu_panel_width(pb.n) == 64 && use_pipeline(pb)) {
         lu_factor_pipelined(pb, ws, st);
         return;
@@ -2110,6 +2200,10 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
         if (use_calu()) {
             calu_panel_step(pb, ws.calu, k, w, st);
             trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
+        } else if (nb == 64 && w == 64 && use_subpanels(pb) && super_panels() && k + 128 <= pb.n) {
+            super_panel_step(pb, ws, k, st);
+            ws.super_end = k + 128;
+            k += 64;  // two panels
         } else if (nb == 64 && w == 64 && use_subpanels(pb)) {
             subpanel_block(pb, ws, k, w, st, true);
             trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
@@ -2156,20 +2250,23 @@ void lu_solve_blocked(const LuProblem& pb, cplx* rhs, size_t rstride, cudaStream
 }  // namespace
 
 void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, cudaStream_t st) {
-    if (!dataflow_solve()) {
+    if (!dataflow_solve() && ws.super_end == 0) {  // the per-panel solve follows nb-column interchange groups only
         lu_solve_blocked(pb, rhs, rstride, st);
         return;
     }
     const int nb = lu_panel_width(pb.n);
     const int nblk = ceil_div(pb.n, nb);
+    const int ks = nb == 64 ? ws.super_end : 0;
     ws.ensure_solve(pb.batch, pb.n, nblk);
-    int* pflag = ws.sflags;
+    int* pflag = ws.sflags;  // [batch][groups] fits in the [batch][nblk] slot
     int* ffl = pflag + static_cast<size_t>(pb.batch) * nblk;
     int* bfl = ffl + static_cast<size_t>(pb.batch) * nblk;
     int* tk = bfl + static_cast<size_t>(pb.batch) * nblk;
     FDS_CUDA(cudaMemsetAsync(ffl, 0, (2 * static_cast<size_t>(pb.batch) * nblk + 2) * sizeof(int), st));
     const size_t smem = 2 * 64 * 64 * sizeof(double);
-    FDS_LAUNCH(lu_pivflag_kernel, dim3(nblk, pb.batch), 64, 0, st, pb.n, nb, pb.ipiv, pflag);
+    const SwapGroups sg{pb.n, nb, ks};
+    const int groups = (ks >> 7) + ceil_div(pb.n - ks, nb);
+    FDS_LAUNCH(lu_pivflag_kernel, dim3(groups, pb.batch), 128, 0, st, sg, pb.ipiv, pflag);
     const int ctas = nblk * pb.batch;
     auto go = [&](auto fwd, auto bwd) {
         static bool attr = false;
@@ -2178,8 +2275,8 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
             FDS_CUDA(cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             attr = true;
         }
-        FDS_LAUNCH(fwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, pb.ipiv, pflag, rhs, rstride,
-                   ws.ybuf, ffl, tk);
+        FDS_LAUNCH(fwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ks, pb.ipiv, pflag, rhs,
+                   rstride, ws.ybuf, ffl, tk);
         FDS_LAUNCH(bwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ws.ybuf, rhs, rstride, bfl,
                    tk + 1);
     };

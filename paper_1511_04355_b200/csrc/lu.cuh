@@ -43,6 +43,10 @@ struct LuWorkspace {
     double* linv_buf = nullptr;  // [batch][2][64][64] L11^{-1} per panel
     int linv_cap = 0;
     double* linv(int batch);
+    // row-interchange groups of the last factorization: columns [0, super_end)
+    // were factored as 128-column super-panels (LAPACK order inside each), the
+    // rest as nb-column panels; LINPACK order across groups
+    int super_end = 0;
     // dataflow solve: forward results [batch][n], per-panel pivot flags, block flags, tickets
     cplx* ybuf = nullptr;
     size_t ybuf_cap = 0;

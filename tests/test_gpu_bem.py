@@ -66,9 +66,26 @@ def test_zgesv_dataflow_solve_many_blocks(n, B):
         assert rel_l2(A[i] @ x[i], b[i]) < 1e-11
 
 
+@pytest.mark.parametrize("n", [128, 129, 191, 192, 255, 256, 320, 449])
+def test_zgesv_super_panel_boundaries(n):
+    """Batches factor in 128-column super-panels (one rank-128 trailing update
+    per two panels; LAPACK interchange order inside a super-panel) and finish
+    with 64-column panels: every split of n around the 128 / 64 boundaries,
+    with forced pivoting (tiny diagonal)."""
+    rng = np.random.default_rng(1000 + n)
+    B = 2
+    A = rng.normal(size=(B, n, n)) + 1j * rng.normal(size=(B, n, n))
+    A[:, np.arange(n), np.arange(n)] *= 1e-7
+    b = rng.normal(size=(B, n)) + 1j * rng.normal(size=(B, n))
+    x = zgesv_batch(A, b)
+    for i in range(B):
+        assert rel_l2(x[i], np.linalg.solve(A[i], b[i])) < 1e-10
+
+
 def test_dataflow_solve_matches_blocked_solve(tmp_path):
-    """The dataflow substitution and the per-panel blocked substitution
-    (FDSWEEP_SOLVE=blocked, kept for comparison) agree to rounding."""
+    """The dataflow substitution after the super-panel factorization and the
+    per-panel blocked substitution after the per-panel factorization
+    (FDSWEEP_SOLVE=blocked selects both, kept for comparison) agree to rounding."""
     import subprocess, sys, os
 
     rng = np.random.default_rng(11)
