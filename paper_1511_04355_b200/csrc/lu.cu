@@ -2,24 +2,26 @@
 // independent frequency systems, for sm_100a (FP64).
 //
 // The reference has no BEM/LU; this is the solve inside the new
-// FrequencySystem::evaluate (systems.hpp:34-42). Per panel step k (width w<=NB):
-//   lu_panel_kernel      cooperative grid: G groups x P CTAs, one group per
-//                        matrix (groups stride over the batch). The panel rows
-//                        [k,n) are split across the group's CTAs and kept in
-//                        shared memory for all w columns. One group barrier per
-//                        column: every CTA publishes its local |re|+|im| argmax
-//                        (LAPACK izamax rule, first max wins) with the full
-//                        candidate row; after the barrier each CTA picks the
-//                        winner, swaps/scales/updates its own rows.
-//   lu_swap_trsm_kernel  applies the panel's row swaps to the trailing columns
-//                        and solves U12 = L11^{-1} A12, 128-column strips in smem
-//                        (L11 is re-read once per strip from L2).
-//   lu_gemm_kernel       A22 -= L21 U12 as a complex GEMM on the FP64 tensor
-//                        pipe: four real mma.sync.m8n8k4.f64 (DMMA) products per
-//                        complex tile, 64x64 complex CTA tiles, cp.async
-//                        double-buffered smem, bank-conflict-free padded layouts.
-// Row swaps are LAPACK-style inside a panel and LINPACK-style across panels
-// (earlier L columns are not permuted); lu_solve applies them in that order.
+// FrequencySystem::evaluate (systems.hpp:34-42). Per 64-column panel:
+//   panel                16-wide sub-panels (lu_panel_cluster_kernel: the rows
+//                        of one matrix across a thread-block cluster, pivot
+//                        candidates exchanged through distributed shared
+//                        memory, one cluster barrier per column; LAPACK izamax
+//                        rule, first max wins), lu_sub_swap_trsm_kernel and
+//                        lu_window_update_kernel between sub-panels;
+//                        lu_panel_kernel (global slots + atomic barrier) when a
+//                        matrix needs more than 16 CTAs.
+//   swap + TRSM          lu_l11_inverse_kernel (L11^{-1} and the panel's swaps
+//                        as one gather map) + lu_swap_apply_kernel (32-column
+//                        strips: gather, then L11^{-1} X on DMMA).
+//   trailing update      lu_gemm_tma_kernel: A22 -= L21 U12 as a complex GEMM on
+//                        the FP64 tensor pipe (four mma.sync.m8n8k4.f64 per
+//                        complex tile, 64x64 tiles, TMA-fed double buffer).
+// Batches go two panels at a time (super_panel_step): one rank-128 trailing
+// update per 128 columns, interchanges in LAPACK order inside the super-panel.
+// Single matrices use a look-ahead schedule (the next panel on a side stream).
+// Across panels / super-panels the row swaps are LINPACK-style (earlier L
+// columns are not permuted); lu_solve follows the same interchange groups.
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
