@@ -903,10 +903,12 @@ constexpr int kApplyCols = 32;  // strip width: L11^{-1} + one strip = 104 KB sm
 // untouched strip, and U12 = L11^{-1} (P A12) runs on DMMA.
 // mode 0: swap + TRSM; 1: swap only (the panel's interchanges applied to a
 // column range, e.g. an earlier panel's L columns); 2: TRSM only (rows already
-// in place). Columns [cb, ce).
+// in place); 3: swap, then the rank-64 update from the previous panel at kp
+// (X -= L[k.., kp..] U[kp.., strip], operands straight from L2 / HBM), then
+// TRSM — the second panel of a super-panel. Columns [cb, ce).
 __global__ void __launch_bounds__(kApplyThreads, 2)
 lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv, int cb, int ce,
-                     int mode) {
+                     int mode, int kp) {
     extern __shared__ __align__(16) double ssm[];
     double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
     double* Li = Lr + 64 * SAS;
@@ -998,6 +1000,53 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
     __syncthreads();
     // 8 warps: 2 (rows of 32) x 4 (columns of 8)
     const int wm = warp & 1, wn = warp >> 1;
+    if (mode == 3) {  // X -= L[k+m][kp+kk] U[kp+kk][col]: accumulators start from X
+        double ur[4][2], ui[4][2];
+        const int nn0 = wn * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int m = wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                ur[mi][e] = Xr[(nn0 + e) * SAS + m];
+                ui[mi][e] = Xi[(nn0 + e) * SAS + m];
+            }
+        }
+        const int nb_col = col0 + wn * 8 + (lane >> 2);
+        const bool bok = nb_col < ce;
+#pragma unroll 4
+        for (int k4 = 0; k4 < 64; k4 += 4) {
+            const int kk = kp + k4 + (lane & 3);
+            double nar[4], fai[4], nai[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const size_t gi = static_cast<size_t>(kk) * ld + k + wm * 32 + mi * 8 + (lane >> 2);
+                nar[mi] = -Are[gi];
+                fai[mi] = Aim[gi];
+                nai[mi] = -fai[mi];
+            }
+            const size_t gb = static_cast<size_t>(nb_col) * ld + kk;
+            const double br = bok ? Are[gb] : 0.0, bi = bok ? Aim[gb] : 0.0;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                dmma(ur[mi][0], ur[mi][1], nar[mi], br);
+                dmma(ur[mi][0], ur[mi][1], fai[mi], bi);
+                dmma(ui[mi][0], ui[mi][1], nar[mi], bi);
+                dmma(ui[mi][0], ui[mi][1], nai[mi], br);
+            }
+        }
+        __syncthreads();  // every warp has read X
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int m = wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                Xr[(nn0 + e) * SAS + m] = ur[mi][e];
+                Xi[(nn0 + e) * SAS + m] = ui[mi][e];
+            }
+        }
+        __syncthreads();
+    }
     double acr[4][2] = {}, aci[4][2] = {};
 #pragma unroll 4
     for (int k4 = 0; k4 < 64; k4 += 4) {
@@ -1837,7 +1886,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv,
         }
         if (!inverse_ready) l11_inverse_step(pb, k, st, linv);
         FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
-                   pb.mstride, pb.plane, pb.n, pb.ld, k, linv, k + 64, pb.n, 0);
+                   pb.mstride, pb.plane, pb.n, pb.ld, k, linv, k + 64, pb.n, 0, 0);
     } else {
         dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
         FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, kTrsmThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
@@ -2149,18 +2198,19 @@ void profiler_scope_trsm(cudaStream_t st, F f, double work) {
     profiler().end(st, e, kProfLuTrsm, work);
 }
 
-void swap_cols(const LuProblem& pb, int k, int cb, int ce, int mode, const double* linv, cudaStream_t st) {
+void swap_cols(const LuProblem& pb, int k, int cb, int ce, int mode, const double* linv, cudaStream_t st, int kp = 0) {
     if (ce <= cb) return;
     const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
     FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(ce - cb, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
-               pb.mstride, pb.plane, pb.n, pb.ld, k, linv, cb, ce, mode);
+               pb.mstride, pb.plane, pb.n, pb.ld, k, linv, cb, ce, mode, kp);
 }
 
 // Two 64-column panels P1 = [k, k+64), P2 = [k+64, k+128) with one rank-128
 // trailing update: P1 is factored, swapped into and solved against the
 // trailing columns (U12_1) and applied to P2's columns only; P2 is factored,
 // its interchanges are applied to P1's L columns and to the trailing columns,
-// P2's rows of the trailing columns take P1's update, U12_2 = L22^{-1} A12_2,
+// P2's rows of the trailing columns take P1's update and U12_2 = L22^{-1} A12_2
+// (one strip kernel, mode 3),
 // and rows/columns >= k+128 take [L21_1 L21_2][U12_1; U12_2] in one pass —
 // each trailing C tile is loaded and stored once per 128 columns of k instead
 // of twice. Inside the 128-column super-panel the interchanges are in LAPACK
@@ -2174,12 +2224,11 @@ void super_panel_step(const LuProblem& pb, LuWorkspace& ws, int k, cudaStream_t 
     subpanel_block(pb, ws, k2, 64, st, true);
     profiler_scope_trsm(st, [&] {
         l11_inverse_step(pb, k2, st, linv);
-        swap_cols(pb, k2, k, k2, 1, linv, st);
-        swap_cols(pb, k2, k + 128, pb.n, 1, linv, st);
-    }, 0.0);
+        swap_cols(pb, k2, k, k2, 1, linv, st);  // P2's interchanges into P1's L columns
+        // trailing strips: P2's interchanges, P1's rank-64 update of P2's rows, L22^{-1}
+        swap_cols(pb, k2, k + 128, pb.n, 3, linv, st, k);
+    }, (4.0 + 8.0) * 64 * 64 * std::max(rest, 0) * pb.batch);
     if (rest <= 0) return;
-    gemm_step(pb, k, 64, st, k + 128, pb.n, k + 128);
-    profiler_scope_trsm(st, [&] { swap_cols(pb, k2, k + 128, pb.n, 2, linv, st); }, 4.0 * 64 * 64 * rest * pb.batch);
     gemm_step(pb, k, 128, st);
 }
 
