@@ -241,8 +241,14 @@ def run_ours(args, world, rank, local, dist):
     far = dict(ms=ms.value, evaluations=wk.value)
     P.api._check(L.fds_profile_enable(0))
     peak, peak_src = measured_fp64_peak()
-    achieved = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
-    traffic = ncu_traffic("lu_gemm_tma_kernel")
+    # the library's GEMM work counter is the algorithmic complex count 8 rest^2 w; the
+    # default 3M kernel executes three real products per complex MAC (6 rest^2 w)
+    four_m = os.environ.get("FDSWEEP_GEMM", "") in ("4m", "cpasync")
+    executed = 1.0 if four_m else 0.75
+    effective = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
+    achieved = effective * executed if effective else None
+    gemm_kernel = "lu_gemm_tma_kernel" if four_m else "lu_gemm3m_tma_kernel"
+    traffic = ncu_traffic(gemm_kernel)
     n = 3 * F.shape[0]
     lu_flops = B * 8.0 * n ** 3 / 3.0
     result = {
@@ -254,10 +260,17 @@ def run_ours(args, world, rank, local, dist):
                    "global_batch": B * world, "parallelism": f"replicas x{world}",
                    "l2": "inputs larger than L2 (129 x 236 MB matrices)"},
         "e2e": e2e,
-        "roofline": {"bound": "tensor", "kernel": "lu_gemm_tma_kernel (TMA-fed DMMA complex GEMM)", "achieved": achieved,
+        "roofline": {"bound": "tensor",
+                     "kernel": (gemm_kernel + (" (TMA-fed DMMA complex GEMM)" if four_m else
+                                               " (TMA-fed DMMA complex GEMM, 3 real products per complex MAC; "
+                                               "timing includes lu_g3_prep_kernel)")),
+                     "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                      "peak_source": peak_src, "traffic": traffic,
-                     "work_def": "8*rest^2*w FP64 flops per launch (A22 -= L21 U12)",
+                     "work_def": ("8*rest^2*w FP64 flops per launch (A22 -= L21 U12)" if four_m else
+                                  "6*rest^2*w FP64 flops executed per launch (A22 -= L21 U12 as 3 real GEMMs)"),
+                     "effective_complex_tflops": effective,
+                     "effective_work_def": "8*rest^2*w (conventional complex GEMM count) / time",
                      "share_of_lu": gemm["ms"] / max(gemm["ms"] + panel["ms"] + trsm["ms"], 1e-9)},
         "stages_ms": {"assembly": stage["assembly_ms"], "lu": stage["lu_ms"], "solve": stage["solve_ms"],
                       "lu_panel": panel["ms"], "lu_trsm": trsm["ms"], "lu_gemm": gemm["ms"]},

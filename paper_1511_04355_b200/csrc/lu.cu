@@ -445,6 +445,7 @@ lu_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int 
 
 // ------------------------------------------------------------------ DMMA GEMM
 constexpr int GBM = 64, GBN = 64, GBK = 16, GSTAGES = 2;
+constexpr int kG3Rows = 136;  // U12 sum-plane column length: 128 panel rows + TMA over-read
 constexpr int GAS = GBM + 4;  // A tile row stride (doubles) ≡ 4 (mod 16): conflict-free fragments
 constexpr int GBS = GBK + 4;  // B tile row stride
 constexpr int kGemmThreads = 256;
@@ -733,6 +734,166 @@ lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                     const size_t gi = static_cast<size_t>(col) * ld + row;
                     Are[gi] = acr[mi][ni][e];
                     Aim[gi] = aci[mi][ni][e];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 3M (three real products) trailing GEMM
+// The same update with three real DMMA products per complex MAC instead of four:
+//   t1 = Ar (Br + Bi),  t2 = (Ar + Ai) Bi,  t3 = (Ai - Ar) Br
+//   Re(A B) = t1 - t2,  Im(A B) = t1 + t3
+// so C - A B = (Cre + t2 - t1, Cim - t3 - t1): accumulators Q = Cre (preloaded)
+// += t2, R = Cim (preloaded) -= t3 and P = t1 from zero, stored as Q - P, R - P.
+// The operand sums come pre-formed from lu_g3_prep_kernel (three TMA planes
+// per operand); in-register sums stalled the DMMA stream (shared FP64 pipe). Three accumulators per output need 1.5x the registers of the
+// four-product kernel, so the tile is BN = 32 columns wide with 16x16 warp
+// tiles (2 CTAs/SM) — or 64 wide at 1 CTA/SM. Error: normwise like ZGEMM
+// (Higham, "Stability of a method for multiplying complex matrices with three
+// real matrix multiplications"), componentwise slightly weaker in Im.
+template <int BN>
+constexpr int g3_smem_doubles() { return GSTAGES * 3 * (GBK * GAS + BN * GBS); }
+
+// Operand planes of one trailing update, formed once per (panel, matrix) so the
+// GEMM's inner loop is DMMA-only (FP64 adds there contend with DMMA for the
+// same pipe): L21 planes Re+Im, Re-Im at [b][p][kk][m] (absolute row m, panel
+// column kk, ld rows per column), U12 plane Re+Im at [b][c][kk] (kG3Rows per column).
+__global__ void lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, size_t plane, int n, int ld, int k,
+                                  int w, int c0, int c1, double* __restrict__ g3, int do_l) {
+    const int b = blockIdx.y;
+    const double* Are = A + static_cast<size_t>(b) * mstride;
+    const double* Aim = Are + plane;
+    double* L = g3 + static_cast<size_t>(b) * 2 * 128 * ld;
+    double* U = g3 + static_cast<size_t>(gridDim.y) * 2 * 128 * ld + static_cast<size_t>(b) * ld * kG3Rows;
+    const int rows = do_l ? n - k - w : 0;
+    const long long nl = static_cast<long long>(rows) * w, nu = static_cast<long long>(c1 - c0) * w;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < nl + nu;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        if (q < nl) {
+            const int kk = static_cast<int>(q / rows), m = k + w + static_cast<int>(q % rows);
+            const size_t gi = static_cast<size_t>(k + kk) * ld + m;
+            const double x = Are[gi], y = Aim[gi];
+            L[static_cast<size_t>(kk) * ld + m] = x + y;
+            L[static_cast<size_t>(128 + kk) * ld + m] = x - y;
+        } else {
+            const long long u = q - nl;
+            const int c = c0 + static_cast<int>(u / w), kk = static_cast<int>(u % w);
+            const size_t gi = static_cast<size_t>(c) * ld + k + kk;
+            U[static_cast<size_t>(c) * kG3Rows + kk] = Are[gi] + Aim[gi];
+        }
+    }
+}
+
+template <int W, int BN, int WGM, int MINB, int NT = kGemmThreads>
+__global__ void __launch_bounds__(NT, MINB)
+lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmU, double* A,
+                     size_t mstride, size_t plane, int n, int ld, int k, int c0) {
+    constexpr int WGN = (NT / 32) / WGM;
+    constexpr int MI = GBM / WGM / 8, NI = BN / WGN / 8;
+    constexpr int nk = W / GBK;
+    constexpr unsigned kStageBytes = 3u * (GBK * GAS + BN * GBS) * sizeof(double);
+    extern __shared__ double gsm_raw[];
+    const unsigned raw = static_cast<unsigned>(__cvta_generic_to_shared(gsm_raw));
+    double* gsm = gsm_raw + ((128u - (raw & 127u)) & 127u) / sizeof(double);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + g3_smem_doubles<BN>());
+    const int b = blockIdx.z;
+    double* Are = A + static_cast<size_t>(b) * mstride;
+    double* Aim = Are + plane;
+    const int m0 = k + W + blockIdx.x * GBM;
+    const int n0 = c0 + blockIdx.y * BN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % WGM, wn = warp / WGM;
+    // A planes: Re L21, Re+Im, Re-Im; B planes: Re U12, Im U12, Re+Im
+    auto As = [&](int st, int pl) { return gsm + (st * 3 + pl) * (GBK * GAS); };
+    auto Bs = [&](int st, int pl) { return gsm + GSTAGES * 3 * (GBK * GAS) + (st * 3 + pl) * (BN * GBS); };
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < GSTAGES; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int st, int kc) {  // thread 0 only
+        mbar_expect_tx(&bar[st], kStageBytes);
+        tma_load_3d(As(st, 0), &tmA, &bar[st], m0, k + kc * GBK, 2 * b);
+        tma_load_3d(As(st, 1), &tmL, &bar[st], m0, kc * GBK, 2 * b);
+        tma_load_3d(As(st, 2), &tmL, &bar[st], m0, kc * GBK, 2 * b + 1);
+        tma_load_3d(Bs(st, 0), &tmB, &bar[st], k + kc * GBK, n0, 2 * b);
+        tma_load_3d(Bs(st, 1), &tmB, &bar[st], k + kc * GBK, n0, 2 * b + 1);
+        tma_load_3d(Bs(st, 2), &tmU, &bar[st], kc * GBK, n0, b);
+    };
+    if (tid == 0) issue(0, 0);
+    double q[MI][NI][2], r[MI][NI][2], p[MI][NI][2];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+        const int row = m0 + wm * (GBM / WGM) + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn * (BN / WGN) + ni * 8 + 2 * (lane & 3) + e;
+                const size_t gi = static_cast<size_t>(col) * ld + row;
+                q[mi][ni][e] = Are[gi];
+                r[mi][ni][e] = Aim[gi];
+                p[mi][ni][e] = 0.0;
+            }
+    }
+#pragma unroll 1
+    for (int kc = 0; kc < nk; ++kc) {
+        if (tid == 0 && kc + 1 < nk) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue((kc + 1) % GSTAGES, kc + 1);
+        }
+        const int st = kc % GSTAGES;
+        mbar_wait(&bar[st], (kc / GSTAGES) & 1);
+        const double* ar = As(st, 0);
+        const double* as = As(st, 1);
+        const double* ad = As(st, 2);
+        const double* br = Bs(st, 0);
+        const double* bi = Bs(st, 1);
+        const double* bs = Bs(st, 2);
+#pragma unroll
+        for (int k4 = 0; k4 < GBK; k4 += 4) {
+            double fa[MI], fs[MI], fd[MI], fbr[NI], fbi[NI], fbs[NI];
+            const int kr = k4 + (lane & 3);
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+                const int m = wm * (GBM / WGM) + mi * 8 + (lane >> 2);
+                fa[mi] = ar[kr * GAS + m];
+                fs[mi] = as[kr * GAS + m];  // Ar + Ai  (t2, accumulated with +)
+                fd[mi] = ad[kr * GAS + m];  // Ar - Ai = -(Ai - Ar) (t3, accumulated into R with -)
+            }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const int nn = wn * (BN / WGN) + ni * 8 + (lane >> 2);
+                fbr[ni] = br[nn * GBS + kr];
+                fbi[ni] = bi[nn * GBS + kr];
+                fbs[ni] = bs[nn * GBS + kr];
+            }
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) {
+                    dmma(p[mi][ni][0], p[mi][ni][1], fa[mi], fbs[ni]);
+                    dmma(q[mi][ni][0], q[mi][ni][1], fs[mi], fbi[ni]);
+                    dmma(r[mi][ni][0], r[mi][ni][1], fd[mi], fbr[ni]);
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+        const int row = m0 + wm * (GBM / WGM) + mi * 8 + (lane >> 2);
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn * (BN / WGN) + ni * 8 + 2 * (lane & 3) + e;
+                if (row < n && col < n) {
+                    const size_t gi = static_cast<size_t>(col) * ld + row;
+                    Are[gi] = q[mi][ni][e] - p[mi][ni][e];
+                    Aim[gi] = r[mi][ni][e] - p[mi][ni][e];
                 }
             }
         }
@@ -1700,6 +1861,16 @@ void LuWorkspace::ensure_side() {
     for (auto& e : ev) FDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
+double* LuWorkspace::g3_planes(const LuProblem& pb) {
+    const size_t need = static_cast<size_t>(pb.batch) * pb.ld * (2 * 128 + kG3Rows);
+    if (need > g3_cap) {
+        if (g3) cudaFree(g3);
+        FDS_CUDA(cudaMalloc(&g3, need * sizeof(double)));
+        g3_cap = need;
+    }
+    return g3;
+}
+
 double* LuWorkspace::linv(int batch) {
     if (batch > linv_cap) {
         if (linv_buf) cudaFree(linv_buf);
@@ -1710,6 +1881,9 @@ double* LuWorkspace::linv(int batch) {
 }
 
 void LuWorkspace::release() {
+    if (g3) cudaFree(g3);
+    g3 = nullptr;
+    g3_cap = 0;
     if (ybuf) cudaFree(ybuf);
     if (sflags) cudaFree(sflags);
     ybuf = nullptr;
@@ -1898,8 +2072,23 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv,
 // Tensor maps of a batch (rows x columns x planes, planes = 2 per matrix), cached
 // per (base pointer, ld, batch): the box of A (L21 chunk) and of B (U12 chunk).
 struct TmaMaps {
-    CUtensorMap a, b;
+    CUtensorMap a, b, b32;  // b32: 32-column U12 boxes of the 3M kernel's narrow tiles
 };
+
+// Trailing-update kernel: 1 = 3M with 64x32 tiles, 2 CTAs/SM (default); 0 = the
+// four-product kernel (FDSWEEP_GEMM=4m: bit-identical results across batch
+// sizes / schedules); 2 = 3M 64x64 at 1 CTA/SM, 3 = 3M 64x64 with 16 warps
+// (FDSWEEP_GEMM=3m64 / 3m64w16, measured slower: 524 / 541 vs 480 ms on cfg2).
+int gemm_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("FDSWEEP_GEMM");
+        if (e && std::string(e) == "4m") return 0;
+        if (e && std::string(e) == "3m64") return 2;
+        if (e && std::string(e) == "3m64w16") return 3;
+        return 1;
+    }();
+    return v;
+}
 
 bool use_tma_gemm() {
     static const bool on = [] {
@@ -1909,13 +2098,7 @@ bool use_tma_gemm() {
     return on;
 }
 
-const TmaMaps& tma_maps(const LuProblem& pb) {
-    static std::mutex mu;
-    static std::map<std::tuple<const void*, int, int, size_t>, TmaMaps> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_tuple(static_cast<const void*>(pb.A), pb.ld, pb.batch, pb.plane);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -1923,6 +2106,17 @@ const TmaMaps& tma_maps(const LuProblem& pb) {
         if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
+    return encode;
+}
+
+const TmaMaps& tma_maps(const LuProblem& pb) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, size_t>, TmaMaps> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(static_cast<const void*>(pb.A), pb.ld, pb.batch, pb.plane);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
     if (pb.mstride != 2 * pb.plane) throw ValidationError("lu: TMA path needs re/im planes back to back");
     TmaMaps m{};
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(pb.ld), static_cast<cuuint64_t>(pb.ld),
@@ -1937,8 +2131,54 @@ const TmaMaps& tma_maps(const LuProblem& pb) {
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     };
+    const cuuint32_t boxb32[3] = {static_cast<cuuint32_t>(kTmaBBox0), 32, 1};
     enc(&m.a, boxa);
     enc(&m.b, boxb);
+    enc(&m.b32, boxb32);
+    return cache.emplace(key, m).first->second;
+}
+
+// The 3M kernel's pre-formed operand planes (LuWorkspace::g3): L21 sums as a
+// [2 batch][128][ld] tensor (boxes 68 x 16 like tmA), U12 sums as [batch][ld][kG3Rows]
+// (boxes 20 x BN like tmB).
+struct G3Maps {
+    double* base = nullptr;
+    CUtensorMap l, u32, u64;
+};
+
+// set by lu_factor for the schedules whose updates run in stream order on one
+// workspace (not the opt-in half-batch pipeline): enables the 3M update
+thread_local LuWorkspace* t_g3_ws = nullptr;
+
+const G3Maps& g3_maps(const LuProblem& pb, LuWorkspace& ws) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int>, G3Maps> cache;
+    double* base = ws.g3_planes(pb);
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(static_cast<const void*>(base), pb.ld, pb.batch);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    G3Maps m{};
+    m.base = base;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    auto enc = [&](CUtensorMap* t, void* ptr, const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+        const CUresult r = tensor_map_encoder()(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ptr, dims, strides, box, estr,
+                                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    };
+    const cuuint64_t ldims[3] = {static_cast<cuuint64_t>(pb.ld), 128, static_cast<cuuint64_t>(2) * pb.batch};
+    const cuuint64_t lstr[2] = {static_cast<cuuint64_t>(pb.ld) * sizeof(double),
+                                static_cast<cuuint64_t>(pb.ld) * 128 * sizeof(double)};
+    const cuuint32_t lbox[3] = {static_cast<cuuint32_t>(kTmaABox0), GBK, 1};
+    enc(&m.l, base, ldims, lstr, lbox);
+    double* ubase = base + static_cast<size_t>(pb.batch) * 2 * 128 * pb.ld;
+    const cuuint64_t udims[3] = {kG3Rows, static_cast<cuuint64_t>(pb.ld), static_cast<cuuint64_t>(pb.batch)};
+    const cuuint64_t ustr[2] = {kG3Rows * sizeof(double), static_cast<cuuint64_t>(pb.ld) * kG3Rows * sizeof(double)};
+    const cuuint32_t ubox32[3] = {static_cast<cuuint32_t>(kTmaBBox0), 32, 1};
+    const cuuint32_t ubox64[3] = {static_cast<cuuint32_t>(kTmaBBox0), 64, 1};
+    enc(&m.u32, ubase, udims, ustr, ubox32);
+    enc(&m.u64, ubase, udims, ustr, ubox64);
     return cache.emplace(key, m).first->second;
 }
 
@@ -1971,7 +2211,43 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
             tset = true;
         }
         const TmaMaps& tm = tma_maps(pb);
-        if (w == 128)
+        const int gv = gemm_variant();
+        if (gv != 0 && t_g3_ws) {
+            const G3Maps& gm = g3_maps(pb, *t_g3_ws);
+            // operand planes: L21 once per (A, k, w) (the look-ahead window and the rest
+            // share it; both run on this stream), U12 for this call's columns
+            const bool do_l = !(t_g3_ws->g3_key_A == pb.A && t_g3_ws->g3_key_k == k && t_g3_ws->g3_key_w == w);
+            t_g3_ws->g3_key_A = pb.A;
+            t_g3_ws->g3_key_k = k;
+            t_g3_ws->g3_key_w = w;
+            const long long work = (do_l ? static_cast<long long>(pb.n - k - w) * w : 0) +
+                                   static_cast<long long>(c1 - c0) * w;
+            FDS_LAUNCH(lu_g3_prep_kernel, dim3(static_cast<unsigned>(std::min<long long>(ceil_div(work, 256LL), 64)), pb.batch),
+                       256, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? 1 : 0);
+            auto go = [&](auto kern, int bn, const CUtensorMap& mu, int nt = kGemmThreads) {
+                const size_t sm = (bn == 32 ? g3_smem_doubles<32>() : g3_smem_doubles<64>()) * sizeof(double) +
+                                  kTmaSmemPad;
+                static bool set[6] = {};
+                const int slot = (bn == 32 ? 0 : (nt == kGemmThreads ? 2 : 4)) + (w == 128 ? 1 : 0);
+                if (!set[slot]) {
+                    FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+                    set[slot] = true;
+                }
+                dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, bn), pb.batch);
+                FDS_LAUNCH(kern, g3, nt, sm, st, tm.a, bn == 32 ? tm.b32 : tm.b, gm.l, mu, pb.A, pb.mstride, pb.plane,
+                           pb.n, pb.ld, k, c0);
+            };
+            if (gv == 1) {
+                if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>, 32, gm.u32);
+                else go(lu_gemm3m_tma_kernel<64, 32, 4, 2>, 32, gm.u32);
+            } else if (gv == 3) {
+                if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 4, 1, 512>, 64, gm.u64, 512);
+                else go(lu_gemm3m_tma_kernel<64, 64, 4, 1, 512>, 64, gm.u64, 512);
+            } else {
+                if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 2, 1>, 64, gm.u64);
+                else go(lu_gemm3m_tma_kernel<64, 64, 2, 1>, 64, gm.u64);
+            }
+        } else if (w == 128)
             FDS_LAUNCH(lu_gemm_tma_kernel<128>, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st,
                        tm.a, tm.b, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
         else
@@ -2241,6 +2517,14 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
         lu_factor_pipelined(pb, ws, st);
         return;
     }
+    struct G3Scope {  // the 3M update's operand planes live in this workspace
+        explicit G3Scope(LuWorkspace* w) {
+            w->g3_key_A = nullptr;
+            w->g3_key_k = w->g3_key_w = -1;
+            t_g3_ws = w;
+        }
+        ~G3Scope() { t_g3_ws = nullptr; }
+    } g3scope(&ws);
     if (!use_calu() && lu_panel_width(pb.n) == 64 && subpanels_enabled() && pb.n >= 128 && use_lookahead(pb)) {
         lu_factor_lookahead(pb, ws, st);
         return;

@@ -43,6 +43,13 @@ struct LuWorkspace {
     double* linv_buf = nullptr;  // [batch][2][64][64] L11^{-1} per panel
     int linv_cap = 0;
     double* linv(int batch);
+    // 3M trailing update: pre-formed operand planes (Re+Im, Re-Im of L21 [batch][2][128][ld];
+    // Re+Im of U12 [batch][ld][kG3Rows]) and the (A, ld, batch) they were encoded for
+    double* g3 = nullptr;
+    size_t g3_cap = 0;
+    double* g3_planes(const LuProblem& pb);
+    const double* g3_key_A = nullptr;  // L21 planes currently formed for (A, k, w)
+    int g3_key_k = -1, g3_key_w = -1;
     // row-interchange groups of the last factorization: columns [0, super_end)
     // were factored as 128-column super-panels (LAPACK order inside each), the
     // rest as nb-column panels; LINPACK order across groups

@@ -46,7 +46,8 @@ def test_gmres_vs_lu_full_size_cfg2():
 
 def test_gmres_stagnation_falls_back_to_lu():
     """A frequency whose GMRES misses tol within max_iter is solved by LU: the
-    batch still returns the LU solution for it (bit-identical to the LU path)."""
+    batch still returns the LU solution for it (to rounding: the fallback factors
+    with another LU schedule)."""
     V, F = mesh.icosphere(2)
     g = P.BemSystem(V, F, mesh.pressure_traction(V, F))
     s = np.array([0.25 + 3j, 0.25 + 7j])
@@ -54,6 +55,6 @@ def test_gmres_stagnation_falls_back_to_lu():
     g.set_solver("gmres", tol=1e-15, restart=2, max_iter=3)
     ug = g.evaluate_batch(s)
     assert g.last_gmres()["lu_fallbacks"] == 2
-    np.testing.assert_array_equal(ug, ul)
+    assert np.linalg.norm(ug - ul) / np.linalg.norm(ul) < 1e-13  # rounding: other LU schedule
     with pytest.raises(P.ValidationError):
         g.set_solver("gmres", tol=-1.0)

@@ -60,14 +60,15 @@ if __name__ == "__main__":
     json.dump({"command": "python bench.py --steps 1 --warmup 1 --no-extra --no-cpu",
                "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)",
                "total_ms": round(tot, 3), "kernels": summ}, open(f"profiles/{tag}_launches_summary.json", "w"), indent=1)
-    f = full("gpurun_out/prof_gemm_r1.ncu-rep", "lu_gemm_tma")
-    json.dump({"command": "ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:tma_kernel<.int.128>' -s 10 -c 1 python bench.py --steps 1 --warmup 1 --no-extra --no-cpu",
+    kern = sys.argv[2] if len(sys.argv) > 2 else "lu_gemm3m_tma_kernel"
+    f = full("gpurun_out/prof_gemm_r1.ncu-rep", kern)
+    json.dump({"command": f"ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:{kern}<.int.128' -s 10 -c 1 python bench.py --steps 1 --warmup 1 --no-extra --no-cpu",
                "units": "GB, ms",
                "kernels": f}, open(f"profiles/{tag}_lu_gemm_ncu_full.json", "w"), indent=1)
     g = f[0]
     traffic = (float(g["dram__bytes_read.sum"]) + float(g["dram__bytes_write.sum"])) * 1e9  # GB -> bytes
-    json.dump({"lu_gemm_tma_kernel": {"bytes_per_launch": traffic,
-                                      "launch": "11th rank-128 trailing update (lu_gemm_tma_kernel<128>, super-panel k = 10*128) of cfg2",
+    json.dump({kern: {"bytes_per_launch": traffic,
+                                      "launch": f"11th rank-128 trailing update ({kern}<128>, super-panel k = 10*128) of cfg2",
                                       "gpu_time_ms": float(g["gpu__time_duration.sum"])}},
               open("profiles/ncu_traffic.json", "w"), indent=1)
     print(json.dumps(summ, indent=0)[:1500])
