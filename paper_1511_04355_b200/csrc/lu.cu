@@ -798,6 +798,7 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const unsigned raw = static_cast<unsigned>(__cvta_generic_to_shared(gsm_raw));
     double* gsm = gsm_raw + ((128u - (raw & 127u)) & 127u) / sizeof(double);
     uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + g3_smem_doubles<BN>());
+    unsigned* freed = reinterpret_cast<unsigned*>(bar + GSTAGES);  // per stage: warps done with it
     const int b = blockIdx.z;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
@@ -810,7 +811,10 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     auto Bs = [&](int st, int pl) { return gsm + GSTAGES * 3 * (GBK * GAS) + (st * 3 + pl) * (BN * GBS); };
     if (tid == 0) {
 #pragma unroll
-        for (int st = 0; st < GSTAGES; ++st) mbar_init(&bar[st], 1);
+        for (int st = 0; st < GSTAGES; ++st) {
+            mbar_init(&bar[st], 1);
+            freed[st] = 0;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -823,7 +827,8 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         tma_load_3d(Bs(st, 1), &tmB, &bar[st], k + kc * GBK, n0, 2 * b + 1);
         tma_load_3d(Bs(st, 2), &tmU, &bar[st], kc * GBK, n0, b);
     };
-    if (tid == 0) issue(0, 0);
+    if (tid == 0)
+        for (int st = 0; st < GSTAGES && st < nk; ++st) issue(st, st);
     double q[MI][NI][2], r[MI][NI][2], p[MI][NI][2];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
@@ -839,12 +844,11 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 p[mi][ni][e] = 0.0;
             }
     }
+    // No CTA barrier per k-chunk: each warp's lane 0 counts itself out of a stage
+    // once its fragment loads have been consumed, and the last warp out refills the
+    // stage with chunk kc + GSTAGES (fast warps never wait for slow ones).
 #pragma unroll 1
     for (int kc = 0; kc < nk; ++kc) {
-        if (tid == 0 && kc + 1 < nk) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            issue((kc + 1) % GSTAGES, kc + 1);
-        }
         const int st = kc % GSTAGES;
         mbar_wait(&bar[st], (kc / GSTAGES) & 1);
         const double* ar = As(st, 0);
@@ -880,7 +884,18 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     dmma(r[mi][ni][0], r[mi][ni][1], fd[mi], fbr[ni]);
                 }
         }
-        __syncthreads();
+        if (kc + GSTAGES < nk) {
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                const unsigned old = atomicAdd(&freed[st], 1u);
+                if (old % (NT / 32) == NT / 32 - 1) {
+                    __threadfence_block();
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    issue(st, kc + GSTAGES);
+                }
+            }
+        }
     }
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
@@ -2226,7 +2241,7 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                        256, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? 1 : 0);
             auto go = [&](auto kern, int bn, const CUtensorMap& mu, int nt = kGemmThreads) {
                 const size_t sm = (bn == 32 ? g3_smem_doubles<32>() : g3_smem_doubles<64>()) * sizeof(double) +
-                                  kTmaSmemPad;
+                                  kTmaSmemPad + GSTAGES * sizeof(unsigned);
                 static bool set[6] = {};
                 const int slot = (bn == 32 ? 0 : (nt == kGemmThreads ? 2 : 4)) + (w == 128 ? 1 : 0);
                 if (!set[slot]) {
