@@ -859,30 +859,26 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const double* bs = Bs(st, 2);
 #pragma unroll
         for (int k4 = 0; k4 < GBK; k4 += 4) {
-            double fa[MI], fs[MI], fd[MI], fbr[NI], fbi[NI], fbs[NI];
             const int kr = k4 + (lane & 3);
+            // three passes (P: Re A x (Re+Im) B, Q: (Re+Im) A x Im B, R: (Re-Im) A x Re B),
+            // each holding only its own MI + NI fragments
 #pragma unroll
-            for (int mi = 0; mi < MI; ++mi) {
-                const int m = wm * (GBM / WGM) + mi * 8 + (lane >> 2);
-                fa[mi] = ar[kr * GAS + m];
-                fs[mi] = as[kr * GAS + m];  // Ar + Ai  (t2, accumulated with +)
-                fd[mi] = ad[kr * GAS + m];  // Ar - Ai = -(Ai - Ar) (t3, accumulated into R with -)
+            for (int pass = 0; pass < 3; ++pass) {
+                const double* pa = pass == 0 ? ar : (pass == 1 ? as : ad);
+                const double* pb = pass == 0 ? bs : (pass == 1 ? bi : br);
+                double fa[MI], fb[NI];
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi) fa[mi] = pa[kr * GAS + wm * (GBM / WGM) + mi * 8 + (lane >> 2)];
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) fb[ni] = pb[(wn * (BN / WGN) + ni * 8 + (lane >> 2)) * GBS + kr];
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) {
+                        double(&acc)[MI][NI][2] = pass == 0 ? p : (pass == 1 ? q : r);
+                        dmma(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
+                    }
             }
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) {
-                const int nn = wn * (BN / WGN) + ni * 8 + (lane >> 2);
-                fbr[ni] = br[nn * GBS + kr];
-                fbi[ni] = bi[nn * GBS + kr];
-                fbs[ni] = bs[nn * GBS + kr];
-            }
-#pragma unroll
-            for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-                for (int ni = 0; ni < NI; ++ni) {
-                    dmma(p[mi][ni][0], p[mi][ni][1], fa[mi], fbs[ni]);
-                    dmma(q[mi][ni][0], q[mi][ni][1], fs[mi], fbi[ni]);
-                    dmma(r[mi][ni][0], r[mi][ni][1], fd[mi], fbr[ni]);
-                }
         }
         if (kc + GSTAGES < nk) {
             __syncwarp();
@@ -2100,6 +2096,7 @@ int gemm_variant() {
         if (e && std::string(e) == "4m") return 0;
         if (e && std::string(e) == "3m64") return 2;
         if (e && std::string(e) == "3m64w16") return 3;
+        if (e && std::string(e) == "3m64x2") return 4;
         return 1;
     }();
     return v;
@@ -2242,8 +2239,9 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
             auto go = [&](auto kern, int bn, const CUtensorMap& mu, int nt = kGemmThreads) {
                 const size_t sm = (bn == 32 ? g3_smem_doubles<32>() : g3_smem_doubles<64>()) * sizeof(double) +
                                   kTmaSmemPad + GSTAGES * sizeof(unsigned);
-                static bool set[6] = {};
-                const int slot = (bn == 32 ? 0 : (nt == kGemmThreads ? 2 : 4)) + (w == 128 ? 1 : 0);
+                static bool set[8] = {};
+                const int slot = (bn == 32 ? 0 : (nt == kGemmThreads ? 2 : nt == 512 ? 4 : 6)) + (w == 128 ? 1 : 0);
+                if (nt == kGemmThreads + 1) nt = kGemmThreads;
                 if (!set[slot]) {
                     FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
                     set[slot] = true;
@@ -2255,6 +2253,9 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
             if (gv == 1) {
                 if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>, 32, gm.u32);
                 else go(lu_gemm3m_tma_kernel<64, 32, 4, 2>, 32, gm.u32);
+            } else if (gv == 4) {
+                if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 2, 2>, 64, gm.u64, kGemmThreads + 1);
+                else go(lu_gemm3m_tma_kernel<64, 64, 2, 2>, 64, gm.u64, kGemmThreads + 1);
             } else if (gv == 3) {
                 if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 4, 1, 512>, 64, gm.u64, 512);
                 else go(lu_gemm3m_tma_kernel<64, 64, 4, 1, 512>, 64, gm.u64, 512);
