@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -28,6 +30,21 @@ inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define FDS_CUDA(x) ::fdsb::cuda_check((x), #x)
+
+// Opt a kernel into `bytes` of dynamic shared memory (> 48 KB needs the
+// attribute), tracked per kernel — several template instances launched from
+// one generic lambda must not share one "already set" flag.
+inline void ensure_dynamic_smem(const void* fn, size_t bytes) {
+    if (bytes <= 48 * 1024) return;
+    static std::mutex mu;
+    static std::map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[fn];
+    if (bytes <= have) return;
+    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+               "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    have = bytes;
+}
 // Every kernel launch of the library goes through this (launch accounting +
 // immediate launch-error check).
 #define FDS_LAUNCH(kernel, grid, block, smem, stream, ...)                        \

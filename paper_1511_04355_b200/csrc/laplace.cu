@@ -900,22 +900,21 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
                    tw, wout);
         const int R = L / 32;
         if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1) {
-            // frequency-major spectra: CTA-cooperative groups of adjacent DOFs
-            auto go = [&](auto kern, int W, int P, int D) {
-                const size_t ssm = (static_cast<size_t>(P) * D * kFsmStride + kFsmL) * sizeof(cplx);
-                static int per_sm = 0;  // one variant per process (FDSWEEP_FSM_TILE is read once)
-                if (per_sm == 0) {
-                    FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm)));
-                    FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
-                }
-                const int ctas = std::min(ceil_div(K, D), std::max(1, per_sm) * device_info().sms);
-                FDS_LAUNCH(kern, ctas, W * 32, ssm, st, K, half_dev, sk, si, hanning ? 1 : 0, eta * dt, post, tw,
-                           wout, out_dev);
-            };
+            // frequency-major spectra: CTA-cooperative groups of adjacent DOFs.
             // 8 warps x 16-DOF groups x 2-deep ring (148 KB smem, 1 CTA/SM). Measured on the
             // 300k-DOF cfg5 spectra: 0.69 ms vs 0.77 ms for warp-private DOF pairs; 8-DOF
-            // groups (2 CTAs/SM), a 3-deep ring and 16 warps were 0.73-0.80 ms.
-            go(fsm_stockham256_tile_kernel<8, 2, 16>, 8, 2, 16);
+            // groups (2 CTAs/SM), 24-DOF groups, a 3-deep ring and 16 warps were 0.73-0.80 ms.
+            constexpr int W = 8, P = 2, D = 16;
+            auto kern = fsm_stockham256_tile_kernel<W, P, D>;
+            const size_t ssm = (static_cast<size_t>(P) * D * kFsmStride + kFsmL) * sizeof(cplx);
+            static int per_sm = 0;
+            if (per_sm == 0) {
+                ensure_dynamic_smem(reinterpret_cast<const void*>(kern), ssm);
+                FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
+            }
+            const int ctas = std::min(ceil_div(K, D), std::max(1, per_sm) * device_info().sms);
+            FDS_LAUNCH(kern, ctas, W * 32, ssm, st, K, half_dev, sk, si, hanning ? 1 : 0, eta * dt, post, tw, wout,
+                       out_dev);
         } else if (L == kFsmL && fsm_stockham()) {
             // 4 warps x 2-deep ring of DOF pairs: 74 KB smem, 2 CTAs (8 warps) per SM
             constexpr int W = 4, P = 2, D = 2;
@@ -944,11 +943,7 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
                                4 * (4 * static_cast<size_t>(L + 1) + OP + 2) * sizeof(cplx);
             const int ctas = std::min(ceil_div(ceil_div(K, 2), 4), 8 * device_info().sms);
             auto go = [&](auto kern) {
-                static size_t a = 0;
-                if (wsm > 48 * 1024 && wsm > a) {
-                    FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
-                    a = wsm;
-                }
+                ensure_dynamic_smem(reinterpret_cast<const void*>(kern), wsm);
                 FDS_LAUNCH(kern, ctas, 128, wsm, st, K, half_dev, sk, si, win, post, tw, wout, out_dev);
             };
             if (R == 1) go(fsm_warp_kernel<1>);

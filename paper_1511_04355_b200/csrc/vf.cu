@@ -744,11 +744,7 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
         const int ctas = std::min(ceil_div(K, 4 * 8 * kResNI), 8 * device_info().sms);
         const int mt = std::min(8, ceil_div(M, 8));  // m-tiles of the first (largest) slice
         auto go = [&](auto kern) {
-            static size_t mattr = 0;
-            if (msmem > 48 * 1024 && msmem > mattr) {
-                FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
-                mattr = msmem;
-            }
+            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), msmem);
             FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 128, msmem, st, J, K, M, P, values_dev, dW, res_dev);
         };
         if (PF == 5) {

@@ -302,3 +302,27 @@ def test_afs_bem_identical_sequence():
     np.testing.assert_array_equal(r["history"][:, :3], o["history"][:, :3])
     np.testing.assert_allclose(r["history"][:, 7], o["history"][:, 7], rtol=1e-6)
     assert worst_match(r["poles"], o["poles"]) < 1e-6
+
+
+def test_identify_residues_kernel_tiers_in_one_process():
+    """Residue kernels of different m-tile tiers with > 48 KB of shared memory in
+    one process: each instance gets its own dynamic-smem opt-in (a shared flag
+    once made the second launch fail with 'invalid argument' inside AFS)."""
+    rng = np.random.default_rng(3)
+
+    def poles(pairs):
+        p = []
+        for m in range(pairs):
+            a = complex(-0.2 - 0.01 * m, 1.0 + 0.9 * m)
+            p += [a, a.conjugate()]
+        return np.array(p)
+
+    for J, pairs in ((60, 2), (50, 20), (44, 8)):
+        s = 0.3 + 1j * np.linspace(0.5, 40.0, J)
+        v = rng.normal(size=(J, 9)) + 1j * rng.normal(size=(J, 9))
+        pl = poles(pairs)
+        res, rms = P.identify_residues(s, v, pl)
+        for k in (0, 8):
+            ro, rmso = O.identify_residues(s, v[:, k], pl)
+            assert rel_l2(res[k], ro) < 1e-10
+            assert rms[k] == pytest.approx(rmso, rel=1e-8)
