@@ -119,7 +119,9 @@ struct fds_bem {
         if (max_batch > 0) return max_batch;
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
-        const size_t per = mstride * sizeof(double) + dev.pstride * sizeof(cplx) + 4096 * 64;
+        // matrix + b-partials + the 3M update's operand planes (LuWorkspace::g3_planes) + slack
+        const size_t per = mstride * sizeof(double) + dev.pstride * sizeof(cplx) +
+                           static_cast<size_t>(ld) * (2 * 128 + 136) * sizeof(double) + 4096 * 64;
         const size_t budget = static_cast<size_t>(0.85 * (fr + static_cast<size_t>(cap) * per));
         return std::max<int>(1, static_cast<int>(budget / std::max<size_t>(per, 1)));
     }
