@@ -14,9 +14,13 @@
 //   swap + TRSM          lu_l11_inverse_kernel (L11^{-1} and the panel's swaps
 //                        as one gather map) + lu_swap_apply_kernel (32-column
 //                        strips: gather, then L11^{-1} X on DMMA).
-//   trailing update      lu_gemm_tma_kernel: A22 -= L21 U12 as a complex GEMM on
-//                        the FP64 tensor pipe (four mma.sync.m8n8k4.f64 per
-//                        complex tile, 64x64 tiles, TMA-fed double buffer).
+//   trailing update      lu_gemm3m_tma_kernel (default): A22 -= L21 U12 as a
+//                        complex GEMM on the FP64 tensor pipe with three real
+//                        mma.sync.m8n8k4.f64 products per complex MAC (3M),
+//                        64x32 tiles, operand sum planes from lu_g3_prep_kernel,
+//                        TMA-fed double buffer refilled by the last warp out;
+//                        lu_gemm_tma_kernel (FDSWEEP_GEMM=4m): four products,
+//                        64x64 tiles.
 // Batches go two panels at a time (super_panel_step): one rank-128 trailing
 // update per 128 columns, interchanges in LAPACK order inside the super-panel.
 // Single matrices use a look-ahead schedule (the next panel on a side stream).
