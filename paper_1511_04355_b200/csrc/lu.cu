@@ -2427,7 +2427,8 @@ bool use_lookahead(const LuProblem& pb) {
     if (env >= 0) return env != 0;
     // measured: single N = 15360 399 -> 368 ms; N = 36864 4.33 -> 4.45 s (the
     // panel share is small there and the co-running panel costs GEMM slots);
-    // batched N = 3840 x 129 697 -> 731 ms
+    // batched N = 3840 x 129 697 -> 731 ms. With the 3M update: N = 15360
+    // 326 -> 306 ms with look-ahead, N = 36864 3.88 -> 4.07 s (kept off)
     return pb.batch == 1 && pb.n <= 24576;
 }
 
