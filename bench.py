@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the B200 BEM / VF / FSM hot path (BASELINE.json metric).
 
-Headline workload (configs[1]): spherical cavity, 1280-triangle icosphere
-(N = 3840 unknowns), Heaviside pressure, the full FSM contour of T = 20,
-N_s = 256 (N_c = N_s/2 + 1 = 129 frequencies, s_k = 5/T + i k 2π/T) solved as one
-batch of independent dense systems; displacement at 16 collocation points
-(48 DOFs). One step = assembly + batched LU + solve of all 129 systems.
+Headline workload (configs[3], the north_star's N = 15360): spherical cavity,
+5120-triangle icosphere (N = 15360 unknowns, 3.77 GB per complex matrix) under
+the seeded random traction (xorshift64 + Box-Muller, seed 0), Heaviside in
+time; the full FSM contour of T = 20, N_s = 512 (N_c = N_s/2 + 1 = 257
+frequencies, s_k = 5/T + i k 2 pi/T). One step = one 32-frequency sub-batch of
+that contour (step i takes frequencies 32 (i mod 8) ... 32 (i mod 8) + 31),
+solved as independent dense systems: assembly + batched LU + solve, with the
+displacement of 16 collocation points (48 DOFs, draw_indices(5120, 16, 0)) as
+the channels.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Under torchrun (N > 1) every rank solves its own 129-frequency sweep (replicas
-only: the path has no exchange step), the step time is the max
-over ranks, and value = total solves / time ("scaling": "weak").
+Under torchrun (N > 1) every rank solves its own sub-batches (replicas only:
+the path has no exchange step), the step time is the max over
+ranks, and value = total solves / time ("scaling": "weak").
 ``--impl reference`` times the CPU oracle port of the same path (OpenMP
-assembly + OpenBLAS zgetrf on all host cores) — the reference has no BEM.
+assembly + OpenBLAS zgetrf/zgetrs on all host cores), one cfg4 frequency per
+step — the reference has no BEM.
 """
 from __future__ import annotations
 
@@ -34,8 +39,32 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "BEM frequency solves/sec (assembly+LU)"
 UNIT = "solves/s"
-T_PERIOD, NS = 20.0, 256
+T_PERIOD = 20.0
 ETA = 5.0 / T_PERIOD
+NS4 = 512                 # cfg4: N_s = 512 -> N_c = 257 contour frequencies
+SUB = 32                  # one step = one 32-frequency sub-batch of the contour
+NSUB = (NS4 // 2 + 1) // SUB  # 8 full sub-batches (frequencies 0..255)
+
+
+def contour(ns):
+    return ETA + 1j * (2 * math.pi / T_PERIOD) * np.arange(ns // 2 + 1)
+
+
+def cfg4_inputs():
+    """configs[3]: icosphere(4) (5120 triangles, N = 15360), random traction seed 0,
+    16 collocation points x 3 DOFs as channels, the N_s = 512 contour."""
+    from paper_1511_04355_b200 import mesh
+
+    V, F = mesh.icosphere(4)
+    tr = mesh.random_traction(F.shape[0], seed=0)
+    pts = mesh.draw_indices(F.shape[0], 16, 0)
+    dofs = [3 * p + i for p in pts for i in range(3)]
+    return V, F, tr, dofs, contour(NS4)
+
+
+def sub_batch(s, i):
+    j = i % NSUB
+    return s[SUB * j: SUB * (j + 1)]
 
 
 def cfg2_inputs():
@@ -45,9 +74,7 @@ def cfg2_inputs():
     tr = mesh.pressure_traction(V, F)
     pts = mesh.draw_indices(F.shape[0], 16, 0)
     dofs = [3 * p + i for p in pts for i in range(3)]
-    nc = NS // 2 + 1
-    s = ETA + 1j * (2 * math.pi / T_PERIOD) * np.arange(nc)
-    return V, F, tr, dofs, s
+    return V, F, tr, dofs, contour(256)
 
 
 class ClockSampler:
@@ -144,39 +171,59 @@ def barrier(dist):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_oracle_solves(n_freq: int, warm: int = 0):
-    """Oracle port: OpenMP assembly + OpenBLAS zgetrf/zgetrs, all host cores."""
+def _oracle():
     sys.path.insert(0, str(ROOT / "oracle"))
     import pyoracle as O
 
-    V, F, tr, dofs, s = cfg2_inputs()
-    bem = O.Bem(V, F, tr)
-    ob = O.openblas_path()
-    for i in range(warm):
-        bem.solve_openblas(s[1 + i], ob)
+    return O
+
+
+def cpu_warmup(O):
+    """Spins up OpenMP / OpenBLAS threads on a small system (cfg1 mesh) — untimed."""
+    from paper_1511_04355_b200 import mesh
+
+    V, F = mesh.icosphere(2)
+    O.Bem(V, F, mesh.pressure_traction(V, F)).solve_openblas(complex(ETA, 1.0), O.openblas_path())
+
+
+def cpu_cfg4_solve(O, bem, s):
+    """Oracle port of one cfg4 frequency: OpenMP assembly + OpenBLAS zgetrf/zgetrs
+    on all host cores. Returns (seconds, [assembly_s, factor+solve_s])."""
     t0 = time.perf_counter()
-    for i in range(n_freq):
-        bem.solve_openblas(s[1 + (i % (len(s) - 1))], ob)
-    return time.perf_counter() - t0
+    _, t = bem.solve_openblas(s, O.openblas_path())
+    return time.perf_counter() - t0, [float(t[0]), float(t[1])]
 
 
 def run_reference(args, world, rank):
+    """Reference arm: the CPU path on the box's host cores, one cfg4 frequency
+    (N = 15360) per step, the frequencies walking the same contour sub-batches."""
     if rank != 0:
         return
-    per = []
-    cpu_oracle_solves(0, warm=min(args.warmup, 1))
-    for _ in range(args.steps):
-        per.append(cpu_oracle_solves(1))
+    O = _oracle()
+    V, F, tr, dofs, s = cfg4_inputs()
+    cpu_warmup(O)
+    bem = O.Bem(V, F, tr)
+    per, split = [], []
+    for i in range(args.steps):
+        dt, sp = cpu_cfg4_solve(O, bem, sub_batch(s, i)[i % SUB])
+        per.append(dt)
+        split.append(sp)
     dt = float(np.mean(per))
     v = 1.0 / dt
+    cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": "cfg2 sphere 1280 tri N=3840, one FSM frequency per step (bounded CPU sample)",
-                   "sample": "1 frequency solve per step"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                         "sample": "oracle BEM (OpenMP assembly) + OpenBLAS zgetrf/zgetrs, 1 frequency of cfg2 per step"},
+        "config": {"workload": "cfg4: sphere cavity, 5120-tri icosphere, N=15360, random traction seed 0, "
+                               "FSM contour T=20 Ns=512 eta=5/T (257 frequencies), 48 channels",
+                   "sample": "1 contour frequency per step (bounded CPU sample of the 32-frequency sub-batch step)",
+                   "warmup": "one untimed cfg1-size solve (thread pools); a cfg4 warm-up solve would add ~30 s each"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "oracle BEM assembly (OpenMP, all cores) + OpenBLAS zgetrf/zgetrs (all cores), "
+                                   "1 cfg4 frequency per step"},
+        "stage_s": {"assembly": float(np.mean([x[0] for x in split])),
+                    "factor_solve": float(np.mean([x[1] for x in split]))},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -189,111 +236,145 @@ def run_reference(args, world, rank):
 ASM_FLOPS_PER_EVAL = 439.0
 
 
+def profile_stages(P, L):
+    import ctypes
+
+    out = {}
+    for name, kind in (("gemm", 0), ("panel", 1), ("trsm", 2), ("far", 3), ("near", 4)):
+        c, ms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        P.api._check(L.fds_profile_read(kind, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
+        out[name] = dict(launches=c.value, ms=ms.value, work=wk.value)
+    return out
+
+
+def gemm_roofline(prof, n, B, label):
+    peak, peak_src = measured_fp64_peak()
+    g = prof["gemm"]
+    # the library's GEMM work counter is the conventional complex count 8 rest^2 w;
+    # the 3M kernel executes three real products per complex MAC (6 rest^2 w)
+    effective = g["work"] / (g["ms"] * 1e-3) / 1e12
+    achieved = 0.75 * effective
+    return {"bound": "tensor",
+            "kernel": "lu_gemm3m_tma_kernel (TMA-fed DMMA complex GEMM, 3 real products per complex MAC; "
+                      "timing includes lu_g3_prep_kernel)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_source": peak_src, "traffic": ncu_traffic("lu_gemm3m_tma_kernel@" + label),
+            "traffic_def": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one rank-128 launch "
+                           "(profiles/ncu_traffic.json)",
+            "work_def": "6*rest^2*w FP64 flops executed per launch (A22 -= L21 U12 as 3 real GEMMs), "
+                        "summed over the step's launches / their CUDA-event time on the launching stream",
+            "effective_complex_tflops": effective,
+            "effective_work_def": "8*rest^2*w (conventional complex GEMM count) / time",
+            "launches_per_step": g["launches"],
+            "share_of_lu": g["ms"] / max(g["ms"] + prof["panel"]["ms"] + prof["trsm"]["ms"], 1e-9),
+            "lu_tflops_conventional": B * 8.0 * n ** 3 / 3.0}
+
+
 def run_ours(args, world, rank, local, dist):
     import paper_1511_04355_b200 as P
     from paper_1511_04355_b200 import BemSystem
 
     L = P.lib()
     P.api._check(L.fds_set_device(local))
-    V, F, tr, dofs, s = cfg2_inputs()
-    B = len(s)
-    sysb = BemSystem(V, F, tr, channels=dofs, max_batch=B)
-    for _ in range(args.warmup):
-        sysb.evaluate_batch_device(s)
+    V, F, tr, dofs, s = cfg4_inputs()
+    n = 3 * F.shape[0]
+    sysb = BemSystem(V, F, tr, channels=dofs, max_batch=SUB)
+    for i in range(args.warmup):
+        sysb.evaluate_batch_device(sub_batch(s, i))
     barrier(dist)
     launches0 = P.kernel_launches()
-    dev_ms = []
+    dev_ms, stage = [], dict(assembly_ms=0.0, lu_ms=0.0, solve_ms=0.0)
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            sysb.evaluate_batch_device(s)
+        for i in range(args.steps):
+            sysb.evaluate_batch_device(sub_batch(s, i))
             t = sysb.last_timing()
             dev_ms.append(t["assembly_ms"] + t["lu_ms"] + t["solve_ms"])
+            for k in stage:
+                stage[k] += t[k] / args.steps
         wall = time.perf_counter() - t0
     launches = (P.kernel_launches() - launches0) // args.steps
-    stage = sysb.last_timing()
     total_ms = allreduce_max(dist, float(np.sum(dev_ms)))
     ms_step = total_ms / args.steps
-    value = B * world / (ms_step * 1e-3)
+    value = SUB * world / (ms_step * 1e-3)
 
-    # end to end through the public C-ABI with host buffers (H2D s, D2H values)
+    # end to end through the public C-ABI with host buffers: the 8 full sub-batches
+    # of the contour (frequencies 0..255), H2D of s and D2H of the 48-channel
+    # responses inside the timed region; frequency 256 is solved untimed so the
+    # full 257-frequency spectra feed the FSM reconstruction below
     barrier(dist)
+    spectra = np.zeros((len(s), len(dofs)), np.complex128)
+    e2e_stage = dict(assembly_ms=0.0, lu_ms=0.0, solve_ms=0.0)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        sysb.evaluate_batch(s)
-    e2e_s = allreduce_max(dist, time.perf_counter() - t0) / args.steps
-    e2e = {"value": B * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * B,
-           "d2h_bytes_per_step": 16 * B * len(dofs)}
+    for i in range(NSUB):
+        spectra[SUB * i: SUB * (i + 1)] = sysb.evaluate_batch(sub_batch(s, i))
+        t = sysb.last_timing()
+        for k in e2e_stage:
+            e2e_stage[k] += t[k]
+    e2e_s = allreduce_max(dist, time.perf_counter() - t0) / NSUB
+    e2e = {"value": SUB * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * SUB,
+           "d2h_bytes_per_step": 16 * SUB * len(dofs), "steps": NSUB,
+           "note": "the 8 full 32-frequency sub-batches of the contour through fds_bem_evaluate_batch"}
+    t1 = time.perf_counter()
+    spectra[NSUB * SUB:] = sysb.evaluate_batch(s[NSUB * SUB:])
+    tail_s = time.perf_counter() - t1
+    t1 = time.perf_counter()
+    hist = P.fsm_invert(T_PERIOD, NS4, ETA, spectra.T.copy())
+    fsm_api_ms = (time.perf_counter() - t1) * 1e3
+    fsm_sweep = {"frequencies": len(s), "wall_s": e2e_s * NSUB + tail_s,
+                 "solves_per_s": len(s) / (e2e_s * NSUB + tail_s),
+                 "assembly_s": e2e_stage["assembly_ms"] * 1e-3, "lu_s": e2e_stage["lu_ms"] * 1e-3,
+                 "solve_s": e2e_stage["solve_ms"] * 1e-3,
+                 "reconstruction_ms": fsm_api_ms, "channels": len(dofs), "time_steps": NS4,
+                 "max_abs_displacement": float(np.max(np.abs(hist))),
+                 "note": "frequencies 0..255 from the e2e loop (stage times summed) + frequency 256 alone; "
+                         "reconstruction = fsm_invert (host API, incl. copies)"}
 
-    # roofline of the dominant kernel (LU trailing GEMM on the FP64 tensor pipe)
+    # roofline of the dominant kernel (the LU trailing GEMM on the FP64 tensor pipe)
     P.api._check(L.fds_profile_enable(1))
-    sysb.evaluate_batch_device(s)
-    import ctypes
-
-    c, ms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
-    P.api._check(L.fds_profile_read(0, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
-    gemm = dict(launches=c.value, ms=ms.value, flops=wk.value)
-    P.api._check(L.fds_profile_read(1, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
-    panel = dict(launches=c.value, ms=ms.value)
-    P.api._check(L.fds_profile_read(2, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
-    trsm = dict(launches=c.value, ms=ms.value)
-    P.api._check(L.fds_profile_read(3, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(wk)))
-    far = dict(ms=ms.value, evaluations=wk.value)
+    sysb.evaluate_batch_device(sub_batch(s, 0))
+    prof = profile_stages(P, L)
     P.api._check(L.fds_profile_enable(0))
-    peak, peak_src = measured_fp64_peak()
-    # the library's GEMM work counter is the algorithmic complex count 8 rest^2 w; the
-    # default 3M kernel executes three real products per complex MAC (6 rest^2 w)
-    four_m = os.environ.get("FDSWEEP_GEMM", "") in ("4m", "cpasync")
-    executed = 1.0 if four_m else 0.75
-    effective = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
-    achieved = effective * executed if effective else None
-    gemm_kernel = "lu_gemm_tma_kernel" if four_m else "lu_gemm3m_tma_kernel"
-    traffic = ncu_traffic(gemm_kernel)
-    n = 3 * F.shape[0]
-    lu_flops = B * 8.0 * n ** 3 / 3.0
+    sysb.close()
+    roof = gemm_roofline(prof, n, SUB, "cfg4")
+    lu_flops = SUB * 8.0 * n ** 3 / 3.0
+    far = prof["far"]
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic",
-        "config": {"workload": "cfg2: sphere cavity, 1280-tri icosphere, N=3840, 129-frequency FSM batch "
-                               "(T=20, Ns=256, eta=5/T), 16 collocation points",
-                   "global_batch": B * world, "parallelism": f"replicas x{world}",
-                   "l2": "inputs larger than L2 (129 x 236 MB matrices)"},
+        "config": {"workload": "cfg4: sphere cavity, 5120-tri icosphere, N=15360, random traction seed 0, "
+                               "32-frequency sub-batch of the FSM contour (T=20, Ns=512, eta=5/T, 257 frequencies) "
+                               "per step, 16 collocation points x 3 DOFs",
+                   "global_batch": SUB * world, "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2 (32 x 3.77 GB matrices per step)"},
         "e2e": e2e,
-        "roofline": {"bound": "tensor",
-                     "kernel": (gemm_kernel + (" (TMA-fed DMMA complex GEMM)" if four_m else
-                                               " (TMA-fed DMMA complex GEMM, 3 real products per complex MAC; "
-                                               "timing includes lu_g3_prep_kernel)")),
-                     "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
-                     "peak_source": peak_src, "traffic": traffic,
-                     "work_def": ("8*rest^2*w FP64 flops per launch (A22 -= L21 U12)" if four_m else
-                                  "6*rest^2*w FP64 flops executed per launch (A22 -= L21 U12 as 3 real GEMMs)"),
-                     "effective_complex_tflops": effective,
-                     "effective_work_def": "8*rest^2*w (conventional complex GEMM count) / time",
-                     "share_of_lu": gemm["ms"] / max(gemm["ms"] + panel["ms"] + trsm["ms"], 1e-9)},
+        "roofline": roof,
         "stages_ms": {"assembly": stage["assembly_ms"], "lu": stage["lu_ms"], "solve": stage["solve_ms"],
-                      "lu_panel": panel["ms"], "lu_trsm": trsm["ms"], "lu_gemm": gemm["ms"]},
+                      "lu_panel": prof["panel"]["ms"], "lu_trsm": prof["trsm"]["ms"], "lu_gemm": prof["gemm"]["ms"]},
         "lu_tflops": lu_flops / (stage["lu_ms"] * 1e-3) / 1e12,
-        # assembly far field: kernel evaluations x a per-evaluation FP64 flop
-        # constant taken from the kernel's SASS op counts (DFMA = 2), profiles/r01_assembly_ncu_full.json
-        "assembly_far": {"ms": far["ms"], "kernel_evaluations": far["evaluations"],
+        "assembly_far": {"ms": far["ms"], "kernel_evaluations": far["work"],
                          "flops_per_evaluation": ASM_FLOPS_PER_EVAL,
-                         "tflops": ASM_FLOPS_PER_EVAL * far["evaluations"] / max(far["ms"], 1e-9) / 1e9,
-                         "fp64_frac": ASM_FLOPS_PER_EVAL * far["evaluations"] / max(far["ms"], 1e-9) / 1e9 / peak},
+                         "tflops": ASM_FLOPS_PER_EVAL * far["work"] / max(far["ms"], 1e-9) / 1e9,
+                         "fp64_frac": ASM_FLOPS_PER_EVAL * far["work"] / max(far["ms"], 1e-9) / 1e9 /
+                         measured_fp64_peak()[0]},
         "wall_ms_per_step": wall * 1e3 / args.steps,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    sysb.close()
     if rank == 0 and world == 1 and not args.no_extra:
-        result["extra"] = extra_configs(args)
+        result["extra"] = extra_configs(args, fsm_sweep)
     if rank == 0 and world == 1 and not args.no_cpu:
-        ncpu = 2
-        dt = cpu_oracle_solves(ncpu, warm=1)
-        result["cpu_baseline"] = {"value": ncpu / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                  "sample": f"{ncpu} frequencies of cfg2 (N=3840): oracle BEM assembly (OpenMP) "
-                                            "+ OpenBLAS zgetrf/zgetrs"}
+        O = _oracle()
+        cpu_warmup(O)
+        dt, sp = cpu_cfg4_solve(O, O.Bem(V, F, tr), s[7])
+        result["cpu_baseline"] = {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                  "sample": "1 cfg4 frequency (k=7, N=15360): oracle BEM assembly (OpenMP) "
+                                            f"{sp[0]:.1f} s + OpenBLAS zgetrf/zgetrs {sp[1]:.1f} s, all host cores"}
+        try:
+            result.setdefault("extra", {})["cfg5_cpu_baseline"] = cpu_vf_fsm_baseline(O)
+        except Exception as e:  # noqa: BLE001
+            result.setdefault("extra", {})["cfg5_cpu_error"] = repr(e)
     if rank == 0:
         print(json.dumps(result), flush=True)
 
@@ -430,59 +511,173 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
         "fsm_chan_major_gbs": b_fsm / (kc * 1e-3) / 1e9, "fsm_chan_major_hbm_frac": b_fsm / (kc * 1e-3) / 1e9 / hbm,
         "fsm_layouts": "fsm = frequency-major [i][k] spectra as the batched BEM emits them (gather-bound); "
                        "fsm_chan_major = per-channel [k][i] spectra, the reference fsm_invert layout",
-        "vf_fsm_dof_per_s": D / ((kr + kt) * 1e-3),
+        "vf_fsm_dof_per_s": D / ((t_res + t_rat) * 1e-3),
+        "vf_fsm_dof_per_s_def": "D / (API-level residue identification + rational_invert time: CUDA events "
+                                "around the whole C-ABI call, including the shared QR and the W operator)",
+        "api_dof_per_s": {"residue_id": D / (t_res * 1e-3), "rational_invert": D / (t_rat * 1e-3),
+                          "fsm": D / (t_fsm * 1e-3), "fsm_chan_major": D / (t_fsm_cm * 1e-3)},
+        "api_hbm_frac": {"residue_id": b_res / (t_res * 1e-3) / 1e9 / hbm, "fsm": b_fsm / (t_fsm * 1e-3) / 1e9 / hbm,
+                         "fsm_chan_major": b_fsm / (t_fsm_cm * 1e-3) / 1e9 / hbm},
+        "kernel_dof_per_s_vf_fsm": D / ((kr + kt) * 1e-3),
         "bytes_per_dof": {"residue_id": b_res / D, "fsm": b_fsm / D}, "flops_per_dof_rational": f_rat / D,
         "pinned": "Chebyshev J=40, Omega_s=1.2 max Im a, T=pi*512/Omega_s, eta=3ln10/T, torch CUDA seed 0",
     }
     return out
 
 
-def extra_configs(args):
-    """Secondary measurements (not the headline): cfg4 single N=15360 solve, cfg5 VF/FSM."""
+def cfg4_afs(fsm_sweep):
+    """cfg4 FSM sweep versus AFS at the reference defaults on the LU path
+    (afs.hpp:21-39: J0 16, E1 1e-4, E2 2e-3, max_iterations 500, 5 ORFs drawn with
+    seed 0, all 48 channels tested; Omega = Omega_s of the N_s = 512 contour)."""
+    import paper_1511_04355_b200 as P
+    from paper_1511_04355_b200 import BemSystem
+
+    V, F, tr, dofs, s = cfg4_inputs()
+    sysb = BemSystem(V, F, tr, channels=dofs, max_batch=16)
+    cfg = dict(omega_max=math.pi * NS4 / T_PERIOD, eta=ETA, period=T_PERIOD, max_iterations=500)
+    t0 = time.perf_counter()
+    try:
+        r = P.run_afs(sysb, **cfg)
+        res = {"converged": r["converged"], "n_c": r["n_c"], "solver_calls": r["solver_calls"],
+               "order": int(len(r["poles"])), "iterations": int(len(r["history"])), "orf": r["orf"]}
+    except P.Error as e:  # the reference algorithm's own failure classes (types.hpp:14-36)
+        pa = getattr(e, "partial", {})
+        hist = pa.get("history", np.zeros((0, 8)))
+        res = {"error_class": type(e).__name__, "error": str(e), "n_c": pa.get("n_c"),
+               "solver_calls": pa.get("solver_calls"), "iterations_completed": int(len(hist)),
+               "failed_at_J": int(pa.get("n_c", 0)), "orf": pa.get("orf"),
+               "last_history": hist[-1].tolist() if len(hist) else None}
+    wall = time.perf_counter() - t0
+    ct = sysb.cumulative_timing()
+    sysb.close()
+    solver_s = (ct["assembly_ms"] + ct["lu_ms"] + ct["solve_ms"]) * 1e-3
+    res.update(wall_s=wall, assembly_s=ct["assembly_ms"] * 1e-3, lu_s=ct["lu_ms"] * 1e-3,
+               solve_s=ct["solve_ms"] * 1e-3, frequencies_solved=ct["frequencies"],
+               vf_and_driver_s=wall - solver_s,
+               config="reference defaults (afs.hpp:21-39), Omega = pi*512/T, eta = 5/T, 48 channels "
+                      "(16 points x 3), LU solves (batch of the J0 initial frequencies, then one per iteration)")
+    return {"fsm_sweep": fsm_sweep, "afs": res,
+            "fsm_solves": fsm_sweep["frequencies"], "afs_solves": res.get("frequencies_solved")}
+
+
+def extra_configs(args, fsm_sweep):
+    """Secondary measurements (not the headline)."""
     from paper_1511_04355_b200 import BemSystem, mesh
 
     out = {}
-    try:  # the headline batch through the iterative solver (SURVEY §8f f4; not the BASELINE metric)
-        V, F = mesh.icosphere(3)
-        sysg = BemSystem(V, F, mesh.pressure_traction(V, F), channels=list(range(48)), max_batch=129)
-        sysg.set_solver("gmres", tol=1e-12, restart=60, max_iter=2000)
-        sg = 0.25 + 1j * 2 * math.pi / 20.0 * np.arange(129)
-        sysg.evaluate_batch_device(sg)
-        sysg.evaluate_batch_device(sg)
-        tg = sysg.last_timing()
-        out["cfg2_gmres_batch"] = {**tg, **sysg.last_gmres(),
-                                   "solves_per_s": 129.0 / ((tg["assembly_ms"] + tg["lu_ms"] + tg["solve_ms"]) * 1e-3),
-                                   "note": "lu_ms is the lockstep GMRES time for all 129 systems (tol 1e-12)"}
-        sysg.close()
-    except Exception as e:  # noqa: BLE001
-        out["cfg2_gmres_error"] = repr(e)
     try:
         out["cfg5_vf_fsm_300k"] = cfg5_vf_fsm()
     except Exception as e:  # noqa: BLE001
         out["cfg5_error"] = repr(e)
-    try:
-        V, F = mesh.icosphere(4)
-        tr = mesh.random_traction(F.shape[0], seed=0)
-        sysb = BemSystem(V, F, tr, channels=list(range(48)), max_batch=1)
-        s = np.array([0.25 + 1j * 2 * math.pi / 20.0])
-        sysb.evaluate_batch_device(s)
-        sysb.evaluate_batch_device(s)
+    try:  # configs[1]: the round-1 headline (129-frequency batch, N = 3840)
+        V, F, tr, dofs, s = cfg2_inputs()
+        sysb = BemSystem(V, F, tr, channels=dofs, max_batch=len(s))
+        for _ in range(2):
+            sysb.evaluate_batch_device(s)
+        ms = []
+        for _ in range(3):
+            sysb.evaluate_batch_device(s)
+            t = sysb.last_timing()
+            ms.append(t["assembly_ms"] + t["lu_ms"] + t["solve_ms"])
         t = sysb.last_timing()
         n = 3 * F.shape[0]
-        out["cfg4_N15360_single_solve"] = {**{k: v for k, v in t.items()},
-                                           "lu_tflops": 8.0 * n ** 3 / 3 / (t["lu_ms"] * 1e-3) / 1e12}
-        # iterative alternative (SURVEY §8f f4): restarted GMRES on the same assembled system
+        out["cfg2_N3840_batch129"] = {**t, "solves_per_s": len(s) / (np.mean(ms) * 1e-3),
+                                      "lu_tflops": len(s) * 8.0 * n ** 3 / 3 / (t["lu_ms"] * 1e-3) / 1e12}
+        sysb.close()
+    except Exception as e:  # noqa: BLE001
+        out["cfg2_error"] = repr(e)
+    try:  # configs[3] one frequency: the single-matrix (look-ahead) LU schedule, plus GMRES
+        V, F, tr, dofs, s = cfg4_inputs()
+        sysb = BemSystem(V, F, tr, channels=dofs, max_batch=1)
+        for _ in range(2):
+            sysb.evaluate_batch_device(s[7:8])
+        t = sysb.last_timing()
+        n = 3 * F.shape[0]
+        out["cfg4_N15360_single_solve"] = {**t, "lu_tflops": 8.0 * n ** 3 / 3 / (t["lu_ms"] * 1e-3) / 1e12}
         sysb.set_solver("gmres", tol=1e-12, restart=60, max_iter=2000)
-        sysb.evaluate_batch_device(s)
-        sysb.evaluate_batch_device(s)
+        for _ in range(2):
+            sysb.evaluate_batch_device(s[7:8])
         tg = sysb.last_timing()
         gm = sysb.last_gmres()
-        out["cfg4_N15360_gmres"] = {**{k: v for k, v in tg.items()}, **gm,
-                                    "matvec_gbs_effective": 16.0 * n * n * (gm["iterations"] + 1) / (tg["lu_ms"] * 1e-3) / 1e9,
+        out["cfg4_N15360_gmres"] = {**tg, **gm,
+                                    "matvec_gbs_effective": 16.0 * n * n * (gm["iterations"] + 1) /
+                                    (tg["lu_ms"] * 1e-3) / 1e9,
                                     "note": "lu_ms is the GMRES time (iterations + restarts' true residual products)"}
         sysb.close()
     except Exception as e:  # noqa: BLE001
         out["cfg4_error"] = repr(e)
+    try:  # configs[2] one frequency: N = 36864 (21.7 GB), the largest single-GPU config
+        V, F = mesh.cube_cavity(32)
+        sysb = BemSystem(V, F, mesh.pressure_traction(V, F), channels=list(range(48)), max_batch=1)
+        s3 = np.array([complex(ETA, 2 * math.pi / T_PERIOD * 7)])
+        for _ in range(2):
+            sysb.evaluate_batch_device(s3)
+        t = sysb.last_timing()
+        n = 3 * F.shape[0]
+        out["cfg3_N36864_single_solve"] = {**t, "lu_tflops": 8.0 * n ** 3 / 3 / (t["lu_ms"] * 1e-3) / 1e12,
+                                           "solves_per_s": 1e3 / (t["assembly_ms"] + t["lu_ms"] + t["solve_ms"])}
+        sysb.close()
+    except Exception as e:  # noqa: BLE001
+        out["cfg3_error"] = repr(e)
+    try:
+        out["cfg4_fsm_vs_afs"] = cfg4_afs(fsm_sweep)
+    except Exception as e:  # noqa: BLE001
+        out["cfg4_afs_error"] = repr(e)
+    return out
+
+
+def cpu_vf_fsm_baseline(O, D_sample=3000):
+    """CPU baseline of the cfg5 VF + FSM stages on a DOF subset (the reference
+    path is single-threaded: vecfit.cpp:356-408 per channel, laplace.cpp:89-125
+    with one FFTW plan per channel, :127-164). identify_residues runs the oracle
+    restatement per channel on 1 thread and on all cores; fsm_invert and
+    rational_invert run as vectorised numpy ports on one thread (numpy's
+    pocketfft stands in for FFTW; the oracle's own DFT is a direct O(N^2) sum).
+    DOF/s extrapolate linearly (every DOF is independent)."""
+    import threadpoolctl
+
+    rng = np.random.default_rng(0)
+    pairs, J, Ts, Ns = 24, 40, 512, 512
+    heads = -(0.01 + 0.49 * rng.random(pairs)) + 1j * 40.0 * rng.random(pairs)
+    poles = np.stack([heads, heads.conj()], 1).reshape(-1)
+    wmax = 1.2 * heads.imag.max()
+    T = math.pi * 512 / wmax
+    eta = 3 * math.log(10) / T
+    s = eta + 1j * wmax * (1 - np.cos(np.arange(J) * math.pi / (2 * (J - 1))))
+    rh = rng.normal(size=(D_sample, pairs)) + 1j * rng.normal(size=(D_sample, pairs))
+    res = np.stack([rh, rh.conj()], 2).reshape(D_sample, -1)
+    vals = (1.0 / (s[:, None] - poles[None, :])) @ res.T
+    vals += 1e-3 * (rng.normal(size=vals.shape) + 1j * rng.normal(size=vals.shape))
+    out = {"dofs_sampled": D_sample, "cores_all": os.cpu_count()}
+    t0 = time.perf_counter()
+    O.identify_residues_many(s, vals, poles, threads=1)
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    R = O.identify_residues_many(s, vals, poles, threads=os.cpu_count())
+    tN = time.perf_counter() - t0
+    out["residue_id_dof_per_s_1core"] = D_sample / t1
+    out["residue_id_dof_per_s_allcores"] = D_sample / tN
+    tgrid = np.arange(Ts) * T / Ts
+    sk = eta + 1j * (2 * math.pi / T) * np.arange(Ns // 2 + 1)
+    half = res @ (1.0 / (sk[None, :] - poles[:, None]))  # (D, 257)
+    with threadpoolctl.threadpool_limits(1):
+        t0 = time.perf_counter()
+        E = np.exp(np.outer(poles, tgrid))  # laplace.cpp:127-164: h = Re sum r e^{a t}
+        np.real(R @ E)
+        tr = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        k = np.arange(Ns // 2 + 1)
+        w = 0.5 * (1 + np.cos(2 * math.pi * k / Ns))  # laplace.cpp:67-72 Hanning on the half spectrum
+        w[0] = 1.0
+        h = np.fft.irfft(half * w[None, :], n=Ns, axis=1) * (Ns / T)  # conjugate fill + inverse DFT
+        h *= np.exp(eta * np.arange(Ns) * (T / Ns))[None, :]
+        tf = time.perf_counter() - t0
+    out["rational_invert_dof_per_s_1core"] = D_sample / tr
+    out["fsm_dof_per_s_1core"] = D_sample / tf
+    out["vf_fsm_dof_per_s_1core"] = D_sample / (t1 + tr)
+    out["kind"] = "port"
+    out["sample"] = (f"{D_sample} DOFs of the cfg5 distribution (J=40, M=48, 512 steps); oracle identify_residues "
+                     "per channel (C, 1 thread / all cores); numpy rational_invert and irfft-based FSM on 1 thread")
     return out
 
 
@@ -490,7 +685,7 @@ def main():
     faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true")

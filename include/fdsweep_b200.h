@@ -89,6 +89,15 @@ int fds_bem_evaluate_batch(fds_bem* bem, const fds_c64* s, int B, fds_c64* out);
 int fds_bem_evaluate_batch_device(fds_bem* bem, const fds_c64* s, int B, const fds_c64** dev_out);
 /* Debug / parity: assembled A(s) (column-major N x N) and b(s) to host. */
 int fds_bem_assemble_host(fds_bem* bem, fds_c64 s, fds_c64* A, fds_c64* b);
+/* Verification at sizes where A(s) should not cross PCIe: assembles A(s), b(s)
+ * on the device and returns A[rows[i], cols[i]] for i < count (and b if
+ * non-NULL, n entries). Pins the assembly kernels against the CPU oracle's
+ * BemOracle::assemble entrywise (no reference counterpart: SPEC.md:9). */
+int fds_bem_assemble_entries(fds_bem* bem, fds_c64 s, int count, const int* rows, const int* cols,
+                             fds_c64* A_entries, fds_c64* b);
+/* Backward error of a solution u (n unknowns, host): assembles A(s), b(s) on
+ * the device; norms[0..3] = ||A u - b||_2, ||A||_inf, ||u||_2, ||b||_2. */
+int fds_bem_residual(fds_bem* bem, fds_c64 s, const fds_c64* u, double* norms);
 /* Per-stage device times of the last evaluate_batch call (ms): assembly, LU, solve;
  * and the number of kernel launches it issued. */
 int fds_bem_last_timing(const fds_bem* bem, double* assembly_ms, double* lu_ms, double* solve_ms,
@@ -101,6 +110,9 @@ int fds_bem_last_timing(const fds_bem* bem, double* assembly_ms, double* lu_ms, 
  * tol within max_iter (e.g. near an interior resonance) is solved by LU
  * instead. For large N one O(N^2) product per iteration beats the O(N^3)
  * factorization. */
+/* Device stage times summed over every solve since create (or the last reset):
+ * out[0..3] = assembly ms, LU (or GMRES) ms, solve ms, frequencies solved. */
+int fds_bem_cumulative_timing(fds_bem* bem, double* out, int reset);
 int fds_bem_set_solver(fds_bem* bem, int kind, double tol, int restart, int max_iter);
 /* Of the last evaluate: largest GMRES iteration count, largest true relative
  * residual of the GMRES-solved frequencies, number of LU fallbacks. */
@@ -195,13 +207,18 @@ typedef struct {
     int solver_calls;
     int n_history;
     int order;              /* M_H of the final model */
+    int n_orf;              /* ORF channels the driver used (drawn with the seed when cfg->n_orf == 0, */
+    int orf_indices[8];     /* afs.cpp:234-236); the first min(n_orf, 8) are listed */
 } fds_afs_summary;
 
 /* Callback system for non-BEM systems: fills out[K] at s; returns 0 on success. */
 typedef int (*fds_system_fn)(void* user, fds_c64 s, fds_c64* out);
 
 /* samples_s[cap], history[cap*8] rows {J, MH, ML, has_s_new, re, im, E1, E2},
- * poles[cap], residues[K*cap] (final model over all channels, [k*order+m]). */
+ * poles[cap], residues[K*cap] (final model over all channels, [k*order+m]).
+ * On an error status (the reference's exception classes) the samples, sample
+ * values, history and summary (order = 0) still hold the iterations completed
+ * before the failure, so a caller can report where the sweep stopped. */
 int fds_run_afs_bem(fds_bem* bem, const fds_afs_config* cfg, int cap, fds_c64* samples_s,
                     fds_c64* sample_values, double* history, fds_c64* poles, fds_c64* residues,
                     fds_afs_summary* summary);

@@ -159,6 +159,8 @@ inline AfsResult run_afs_bem(const BemSystem& sys, const AfsConfig& cfg) {
         r.history.push_back(it);
     }
     r.orf_indices = cfg.orf_indices;
+    if (r.orf_indices.empty())  // drawn by the driver (afs.cpp:234-236)
+        r.orf_indices.assign(sm.orf_indices, sm.orf_indices + std::min(sm.n_orf, 8));
     if (cfg.test_indices.empty())
         for (int k = 0; k < K; ++k) r.test_indices.push_back(k);
     else

@@ -290,6 +290,40 @@ void BemOracle::self_block(int e, C s, C Ui[9], C Ti[9]) const {
     }
 }
 
+// Integrals of U*, T* over source element e seen from the centroid of c (no ½I).
+void BemOracle::block(int c, int e, C s, C Ui[9], C Ti[9]) const {
+    for (int i = 0; i < 9; ++i) Ui[i] = Ti[i] = C(0.0, 0.0);
+    if (e == c) {
+        self_block(e, s, Ui, Ti);
+        return;
+    }
+    const Rule7 rule = make_rule7();
+    const Elem ec = elem_of(&geo_[static_cast<size_t>(c) * 16]);
+    const Elem ee = elem_of(&geo_[static_cast<size_t>(e) * 16]);
+    const int L = subdivision_level(norm(sub(ec.c, ee.c)), ee.h);
+    integrate_tri(kc_, rule, ec.c, ee.v[0], ee.v[1], ee.v[2], ee.n, L, s, Ui, Ti);
+}
+
+C BemOracle::entry(int row, int col, C s) const {
+    C Ui[9], Ti[9];
+    const int c = row / 3, i = row % 3, e = col / 3, j = col % 3;
+    block(c, e, s, Ui, Ti);
+    C v = Ti[3 * i + j];
+    if (c == e && i == j) v += 0.5;
+    return v;
+}
+
+C BemOracle::rhs(int row, C s) const {
+    const int c = row / 3, i = row % 3;
+    C acc(0.0, 0.0);
+    for (int e = 0; e < ne_; ++e) {
+        C Ui[9], Ti[9];
+        block(c, e, s, Ui, Ti);
+        for (int j = 0; j < 3; ++j) acc += Ui[3 * i + j] * traction_[3 * e + j];
+    }
+    return acc * (1.0 / s);
+}
+
 void BemOracle::assemble(C s, std::vector<C>& A, std::vector<C>& b) const {
     const int ne = ne_, n = 3 * ne_;
     A.assign(static_cast<size_t>(n) * n, C(0.0, 0.0));

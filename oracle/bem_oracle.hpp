@@ -34,6 +34,10 @@ class BemOracle {
     std::vector<std::complex<double>> solve(std::complex<double> s) const;
     void self_block(int e, std::complex<double> s, std::complex<double> U[9],
                     std::complex<double> T[9]) const;
+    // Single entries at full-size configs (same arithmetic as assemble()).
+    void block(int c, int e, std::complex<double> s, std::complex<double> U[9], std::complex<double> T[9]) const;
+    std::complex<double> entry(int row, int col, std::complex<double> s) const;
+    std::complex<double> rhs(int row, std::complex<double> s) const;
     const KernelCoeffs& coeffs() const { return kc_; }
 
   private:

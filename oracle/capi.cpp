@@ -16,6 +16,7 @@
 #include <string>
 
 #include "bem_oracle.hpp"
+#include "linalg.hpp"
 #include "fdsweep/afs.hpp"
 #include "fdsweep/io.hpp"
 #include "fdsweep/laplace.hpp"
@@ -146,11 +147,87 @@ int orc_relocate_poles(int J, int K, const double* s, const double* vals, int M,
     });
 }
 
+// ---- linear-algebra test hooks (tests/test_oracle_crosscheck.py) ----
+// Dimensions of the last relocation's stacked sigma system; has_h = 1 when the
+// companion matrix was formed (the rank test passed).
+int orc_last_relocation_dims(int* rows, int* cols, int* has_h) {
+    return guarded([&] {
+        const auto& c = oracle::reloc_capture();
+        *rows = c.stacked.rows;
+        *cols = c.stacked.cols;
+        *has_h = c.has_h ? 1 : 0;
+    });
+}
+int orc_last_relocation(double* stacked, double* rhs, double* h) {
+    return guarded([&] {
+        const auto& c = oracle::reloc_capture();
+        std::copy(c.stacked.a.begin(), c.stacked.a.end(), stacked);
+        std::copy(c.rhs.begin(), c.rhs.end(), rhs);
+        if (c.has_h && h) std::copy(c.h.a.begin(), c.h.a.end(), h);
+    });
+}
+// The oracle's ColPivHouseholderQR on a column-major m x n matrix: |R_ii| in
+// factor order, the column permutation, Eigen's rank, nonzero pivots, max
+// pivot, and the basic least-squares solution for rhs b.
+int orc_colpivqr(int m, int n, const double* a, const double* b, double* rdiag, int* perm, int* rank,
+                 int* nonzero_pivots, double* maxpivot, double* x) {
+    return guarded([&] {
+        oracle::Mat A(m, n);
+        std::copy(a, a + static_cast<size_t>(m) * n, A.a.begin());
+        const oracle::ColPivQR qr(std::move(A));
+        const int size = std::min(m, n);
+        for (int i = 0; i < size; ++i) rdiag[i] = std::abs(qr.qr(i, i));
+        for (int j = 0; j < n; ++j) perm[j] = qr.perm[j];
+        *rank = qr.rank();
+        *nonzero_pivots = qr.nonzero_pivots;
+        *maxpivot = qr.maxpivot;
+        if (x) {
+            const auto y = qr.solve(std::vector<double>(b, b + m));
+            std::copy(y.begin(), y.end(), x);
+        }
+    });
+}
+// The oracle's EigenSolver restatement (Hessenberg + Francis double shift).
+int orc_real_eigenvalues(int n, const double* h, double* ev) {
+    return guarded([&] {
+        oracle::Mat H(n, n);
+        std::copy(h, h + static_cast<size_t>(n) * n, H.a.begin());
+        std::vector<Complex> e;
+        if (!oracle::real_eigenvalues(std::move(H), e)) throw fdsweep::NumericError("eigenvalue iteration failed");
+        cput(e, ev);
+    });
+}
+
 int orc_identify_residues(int J, const double* s, const double* vals, int M,
                           const double* poles, double* res_out, double* rms) {
     return guarded([&] {
         const auto r = fdsweep::identify_residues(cvec(s, J), cvec(vals, J), cvec(poles, M), rms);
         cput(r, res_out);
+    });
+}
+
+// CPU baseline of identify_residues over K channels (vecfit.cpp:356-408, one
+// call per channel as the reference's final fit does, afs.cpp:386-393) on
+// `threads` OpenMP threads. vals [j][k]; residues out [k][m].
+int orc_identify_residues_many(int J, int K, const double* s, const double* vals, int M, const double* poles,
+                               int threads, double* res_out) {
+    return guarded([&] {
+        const std::vector<Complex> sv = cvec(s, J), pv = cvec(poles, M);
+        std::string err;
+#pragma omp parallel for schedule(static) num_threads(threads)
+        for (int k = 0; k < K; ++k) {
+            std::vector<Complex> v(J);
+            for (int j = 0; j < J; ++j)
+                v[j] = Complex(vals[2 * (static_cast<size_t>(j) * K + k)], vals[2 * (static_cast<size_t>(j) * K + k) + 1]);
+            try {
+                const auto r = fdsweep::identify_residues(sv, v, pv, nullptr);
+                cput(r, res_out + 2 * static_cast<size_t>(k) * M);
+            } catch (const std::exception& e) {
+#pragma omp critical
+                err = e.what();
+            }
+        }
+        if (!err.empty()) throw fdsweep::NumericError(err);
     });
 }
 
@@ -318,7 +395,20 @@ int orc_run_afs(void* h, const double* cfg_d, const int* cfg_i, int n_orf, const
         cfg.n_relocations = cfg_i[6];
         cfg.orf_indices.assign(orf, orf + n_orf);
         cfg.test_indices.assign(test, test + n_test);
-        const auto r = fdsweep::run_afs(*static_cast<OracleSystem*>(h)->sys, cfg);
+        // on_sample (afs.cpp:296) records every solved frequency as it happens, so
+        // the samples taken before a reference exception stay visible to the caller
+        *n_c = 0;
+        *solver_calls = 0;
+        *n_hist = 0;
+        auto on_sample = [&](const fdsweep::FrequencySample& smp) {
+            if (*n_c < cap) {
+                samples_s[2 * *n_c] = smp.s.real();
+                samples_s[2 * *n_c + 1] = smp.s.imag();
+            }
+            ++*n_c;
+            ++*solver_calls;
+        };
+        const auto r = fdsweep::run_afs(*static_cast<OracleSystem*>(h)->sys, cfg, {}, on_sample);
         const int nc = static_cast<int>(r.samples.size());
         if (nc > cap || static_cast<int>(r.history.size()) > cap || r.model_high.order() > cap)
             throw fdsweep::ValidationError("orc_run_afs: output capacity too small");
@@ -368,6 +458,24 @@ int orc_bem_assemble(void* h, double sr, double si, double* A_out, double* b_out
         static_cast<oracle::BemOracle*>(h)->assemble(Complex(sr, si), A, b);
         cput(A, A_out);
         cput(b, b_out);
+    });
+}
+int orc_bem_entries(void* h, double sr, double si, int count, const int* rows, const int* cols, double* out) {
+    return guarded([&] {
+        auto* bem = static_cast<oracle::BemOracle*>(h);
+        std::vector<Complex> v(count);
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int i = 0; i < count; ++i) v[i] = bem->entry(rows[i], cols[i], Complex(sr, si));
+        cput(v, out);
+    });
+}
+int orc_bem_rhs_rows(void* h, double sr, double si, int count, const int* rows, double* out) {
+    return guarded([&] {
+        auto* bem = static_cast<oracle::BemOracle*>(h);
+        std::vector<Complex> v(count);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int i = 0; i < count; ++i) v[i] = bem->rhs(rows[i], Complex(sr, si));
+        cput(v, out);
     });
 }
 int orc_bem_solve(void* h, double sr, double si, double* u_out) {

@@ -321,4 +321,18 @@ inline bool real_eigenvalues(Mat h, std::vector<std::complex<double>>& ev) {
     return true;
 }
 
+// Inputs of the last relocate_poles call's stacked sigma least squares and
+// companion eigenproblem (test hook: lets tests/test_oracle_crosscheck.py run
+// the same systems through LAPACK). Not thread-safe; tests call it serially.
+struct RelocCapture {
+    Mat stacked;               // K*red x M (vecfit.cpp:281)
+    std::vector<double> rhs;   // K*red
+    Mat h;                     // M x M (vecfit.cpp:324), valid when has_h
+    bool has_h = false;
+};
+inline RelocCapture& reloc_capture() {
+    static RelocCapture c;
+    return c;
+}
+
 }  // namespace oracle

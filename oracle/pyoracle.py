@@ -115,12 +115,55 @@ def relocate_poles(s, vals, poles):
     return out, rms, float(mv[0])
 
 
+def last_relocation():
+    """Stacked sigma system (rows x M), its rhs and the companion matrix H (or None)
+    of the last relocate_poles call (oracle test hook, vecfit.cpp:281,324)."""
+    r, c, hh = (np.zeros(1, np.int32) for _ in range(3))
+    call("orc_last_relocation_dims", r, c, hh)
+    rows, M = int(r[0]), int(c[0])
+    A = np.zeros((rows, M), order="F")
+    b = np.zeros(rows)
+    H = np.zeros((M, M), order="F")
+    call("orc_last_relocation", A, b, H)
+    return A, b, (H if hh[0] else None)
+
+
+def colpivqr(A, b=None):
+    """The oracle's ColPivHouseholderQR: dict(rdiag, perm, rank, nonzero_pivots, maxpivot, x)."""
+    A = np.asfortranarray(A, np.float64)
+    m, n = A.shape
+    bb = np.zeros(m) if b is None else np.ascontiguousarray(b, np.float64)
+    rd = np.zeros(min(m, n))
+    perm = np.zeros(n, np.int32)
+    rank, npv = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    mp = np.zeros(1)
+    x = np.zeros(n)
+    call("orc_colpivqr", m, n, A, bb, rd, perm, rank, npv, mp, x)
+    return dict(rdiag=rd, perm=perm, rank=int(rank[0]), nonzero_pivots=int(npv[0]), maxpivot=float(mp[0]), x=x)
+
+
+def real_eigenvalues(H):
+    H = np.asfortranarray(H, np.float64)
+    ev = np.zeros(H.shape[0], np.complex128)
+    call("orc_real_eigenvalues", H.shape[0], H, ev)
+    return ev
+
+
 def identify_residues(s, vals, poles):
     s, vals, poles = _c(s), _c(vals), _c(poles)
     out = np.zeros(len(poles), np.complex128)
     rms = np.zeros(1)
     call("orc_identify_residues", len(s), s, vals, len(poles), poles, out, rms)
     return out, float(rms[0])
+
+
+def identify_residues_many(s, vals, poles, threads=1):
+    """identify_residues per channel (vals (J, K)) on `threads` OpenMP threads -> (K, M)."""
+    s, vals, poles = _c(s), _c(vals), _c(poles)
+    J, K = vals.shape
+    out = np.zeros((K, len(poles)), np.complex128)
+    call("orc_identify_residues_many", J, K, s, vals, len(poles), poles, int(threads), out)
+    return out
 
 
 def vector_fit(s, vals, orf, order, n_reloc=3):
@@ -287,8 +330,12 @@ def run_afs(system: System, *, omega_max, eta, period, orf=(), test=(), initial_
     poles = np.zeros(cap, np.complex128)
     orf_used = np.zeros(max(system.channels, 8), np.int32)
     res = np.zeros((system.channels, cap), np.complex128)
-    call("orc_run_afs", system.h, cd, ci, len(orf), orf, len(test), test, cap, ss, nc, conv, calls, hist,
-         nh, poles, order, orf_used, norf, res)
+    try:
+        call("orc_run_afs", system.h, cd, ci, len(orf), orf, len(test), test, cap, ss, nc, conv, calls, hist,
+             nh, poles, order, orf_used, norf, res)
+    except OracleError as e:  # samples solved before the reference threw (on_sample, afs.cpp:296)
+        e.partial = dict(samples=ss[: int(nc[0])].copy(), n_c=int(nc[0]), solver_calls=int(calls[0]))
+        raise
     n = int(nc[0])
     M = int(order[0])
     resid = np.ascontiguousarray(res.reshape(-1)[: system.channels * M].reshape(system.channels, M))
@@ -324,6 +371,20 @@ class Bem:
         t = np.zeros(2)
         call("orc_bem_solve_openblas", self.h, str(openblas_path).encode(), float(np.real(s)), float(np.imag(s)), u, t)
         return u, t
+
+    def entries(self, s, rows, cols):
+        """A(s)[rows[i], cols[i]] (same arithmetic as assemble; full-size spot checks)."""
+        r = np.ascontiguousarray(rows, np.int32)
+        c = np.ascontiguousarray(cols, np.int32)
+        out = np.zeros(len(r), np.complex128)
+        call("orc_bem_entries", self.h, float(np.real(s)), float(np.imag(s)), len(r), r, c, out)
+        return out
+
+    def rhs_rows(self, s, rows):
+        r = np.ascontiguousarray(rows, np.int32)
+        out = np.zeros(len(r), np.complex128)
+        call("orc_bem_rhs_rows", self.h, float(np.real(s)), float(np.imag(s)), len(r), r, out)
+        return out
 
     def self_block(self, e, s):
         U = np.zeros(9, np.complex128)

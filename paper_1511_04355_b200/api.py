@@ -95,7 +95,8 @@ class AfsConfigC(ctypes.Structure):
 
 class AfsSummaryC(ctypes.Structure):
     _fields_ = [("n_c", ctypes.c_int), ("converged", ctypes.c_int), ("solver_calls", ctypes.c_int),
-                ("n_history", ctypes.c_int), ("order", ctypes.c_int)]
+                ("n_history", ctypes.c_int), ("order", ctypes.c_int), ("n_orf", ctypes.c_int),
+                ("orf_indices", ctypes.c_int * 8)]
 
 
 SYSTEM_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _C64, ctypes.c_void_p)
@@ -229,11 +230,36 @@ class BemSystem:
         _check(lib().fds_bem_assemble_host(self._h, _C64(float(np.real(s)), float(np.imag(s))), _p(A), _p(b)))
         return A, b
 
+    def assemble_entries(self, s, rows, cols, with_rhs=False):
+        """A(s)[rows[i], cols[i]] assembled on the device (and b(s) if with_rhs)."""
+        r = np.ascontiguousarray(rows, np.int32)
+        c = np.ascontiguousarray(cols, np.int32)
+        out = np.zeros(len(r), np.complex128)
+        b = np.zeros(self.unknowns, np.complex128) if with_rhs else None
+        _check(lib().fds_bem_assemble_entries(self._h, _C64(float(np.real(s)), float(np.imag(s))), len(r), _p(r),
+                                              _p(c), _p(out), _p(b)))
+        return (out, b) if with_rhs else out
+
+    def residual(self, s, u):
+        """Device backward-error norms of a full solution u: dict(res, a_inf, u, b)."""
+        u = _cz(u)
+        if u.shape != (self.unknowns,):
+            raise ValidationError("residual: u must hold every unknown")
+        nr = np.zeros(4)
+        _check(lib().fds_bem_residual(self._h, _C64(float(np.real(s)), float(np.imag(s))), _p(u), _p(nr)))
+        return dict(res=nr[0], a_inf=nr[1], u=nr[2], b=nr[3])
+
     def last_timing(self):
         a, l_, s, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
         _check(lib().fds_bem_last_timing(self._h, ctypes.byref(a), ctypes.byref(l_), ctypes.byref(s),
                                          ctypes.byref(n)))
         return dict(assembly_ms=a.value, lu_ms=l_.value, solve_ms=s.value, launches=n.value)
+
+    def cumulative_timing(self, reset=False):
+        """Stage times summed over every solve since create / the last reset."""
+        out = np.zeros(4)
+        _check(lib().fds_bem_cumulative_timing(self._h, _p(out), int(bool(reset))))
+        return dict(assembly_ms=out[0], lu_ms=out[1], solve_ms=out[2], frequencies=int(out[3]))
 
     def set_solver(self, kind: str = "lu", tol: float = 1e-12, restart: int = 60, max_iter: int = 1000):
         """'lu' (batched LU, default) or 'gmres' (restarted GMRES, all frequencies
@@ -392,8 +418,21 @@ def run_afs(system, cap=1024, **cfg):
     poles = np.zeros(cap, np.complex128)
     res = np.zeros(K * cap, np.complex128)
     summ = AfsSummaryC()
+
+    def partial():
+        n = summ.n_c
+        return dict(samples=ss[:n].copy(), values=vals[:n].copy(), n_c=n, solver_calls=summ.solver_calls,
+                    history=hist[: summ.n_history].copy(), orf=list(summ.orf_indices[: min(summ.n_orf, 8)]))
+
+    def check(rc):
+        try:
+            _check(rc)
+        except Error as e:  # the iterations completed before the reference algorithm failed
+            e.partial = partial()
+            raise
+
     if isinstance(system, BemSystem):
-        _check(lib().fds_run_afs_bem(system.handle, ctypes.byref(c), cap, _p(ss), _p(vals), _p(hist), _p(poles),
+        check(lib().fds_run_afs_bem(system.handle, ctypes.byref(c), cap, _p(ss), _p(vals), _p(hist), _p(poles),
                                      _p(res), ctypes.byref(summ)))
     else:
         err = []
@@ -412,11 +451,11 @@ def run_afs(system, cap=1024, **cfg):
                                         _p(res), ctypes.byref(summ))
         if err:
             raise err[0]
-        _check(rc)
+        check(rc)
     n, M = summ.n_c, summ.order
     return dict(samples=ss[:n].copy(), values=vals[:n].copy(), n_c=n, converged=bool(summ.converged),
                 solver_calls=summ.solver_calls, history=hist[: summ.n_history].copy(), poles=poles[:M].copy(),
-                residues=res[: K * M].reshape(K, M).copy())
+                residues=res[: K * M].reshape(K, M).copy(), orf=list(summ.orf_indices[: min(summ.n_orf, 8)]))
 
 
 def damping_eta(kappa, period):

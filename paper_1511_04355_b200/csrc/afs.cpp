@@ -114,9 +114,9 @@ double afs_error_e1(const std::vector<double>& t, const std::vector<double>& cur
     return worst;
 }
 
-AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
+void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut& r) {
     validate(cfg);
-    AfsOut r;
+    r = AfsOut{};
     r.orf = cfg.orf.empty() ? draw_channels(channels, std::min(5, channels), cfg.seed) : cfg.orf;
     if (cfg.test.empty()) {
         r.test.resize(channels);
@@ -293,7 +293,6 @@ AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg) {
     r.residues.assign(static_cast<size_t>(channels) * M, Cx(0, 0));
     for (int k = 0; k < channels; ++k)
         for (int m = 0; m < M; ++m) r.residues[static_cast<size_t>(k) * M + m] = rmk[static_cast<size_t>(m) * channels + k];
-    return r;
 }
 
 }  // namespace fdsb

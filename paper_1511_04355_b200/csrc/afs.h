@@ -40,7 +40,9 @@ struct AfsOut {
 // Evaluates a batch of frequencies: out[b*channels + k].
 using BatchEval = std::function<void(const std::vector<Cx>&, std::vector<Cx>&)>;
 
-AfsOut run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg);
+// Fills r as it goes: when the reference algorithm throws, r keeps the
+// samples and history of the iterations completed before the failure.
+void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut& r);
 std::vector<int> draw_channels(int n, int k, uint64_t seed);
 std::vector<Cx> afs_initial_frequencies(int j0, double eta, double omega_max);
 std::pair<int, int> afs_fit_orders(int J, double ah, double al);

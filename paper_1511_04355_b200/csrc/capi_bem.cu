@@ -57,6 +57,78 @@ void KernelProfile::end(cudaStream_t st, cudaEvent_t a, int kind, double work) {
     recs.push_back({a, b, work, kind});
 }
 
+// A[rows[i], cols[i]] from the planar column-major matrix (verification entry point).
+__global__ void gather_entries_kernel(const double* __restrict__ A, size_t plane, int ld, const int* __restrict__ rc,
+                                      int count, cplx* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const size_t g = static_cast<size_t>(rc[count + i]) * ld + rc[i];
+    out[i] = {A[g], A[plane + g]};
+}
+
+// Residual r = A u - b, partial over a slice of columns: one thread per row,
+// CTA (row block, column slice), u slice staged in shared memory. Writes the
+// slice's partial sums and partial |A_ij| row sums; a second kernel reduces.
+constexpr int kResRows = 256, kResCols = 512;
+__global__ void __launch_bounds__(kResRows) residual_partial_kernel(const double* __restrict__ A, size_t plane,
+                                                                    int ld, int n, const cplx* __restrict__ u,
+                                                                    cplx* __restrict__ part,
+                                                                    double* __restrict__ absrow) {
+    __shared__ cplx us[kResCols];
+    const int i = blockIdx.x * kResRows + threadIdx.x;
+    const int j0 = blockIdx.y * kResCols, j1 = min(n, j0 + kResCols);
+    for (int j = j0 + threadIdx.x; j < j1; j += kResRows) us[j - j0] = u[j];
+    __syncthreads();
+    if (i >= n) return;
+    cplx acc = {0.0, 0.0};
+    double ab = 0.0;
+    for (int j = j0; j < j1; ++j) {
+        const size_t g = static_cast<size_t>(j) * ld + i;
+        const cplx a = {A[g], A[plane + g]};
+        acc = acc + a * us[j - j0];
+        ab += sqrt(abs2(a));
+    }
+    part[static_cast<size_t>(blockIdx.y) * n + i] = acc;
+    absrow[static_cast<size_t>(blockIdx.y) * n + i] = ab;
+}
+
+// One CTA: norms[0] = ||A u - b||_2, [1] = ||A||_inf, [2] = ||u||_2, [3] = ||b||_2 (fixed order).
+__global__ void residual_reduce_kernel(const cplx* __restrict__ part, const double* __restrict__ absrow, int slices,
+                                       int n, const cplx* __restrict__ b, const cplx* __restrict__ u,
+                                       double* __restrict__ norms) {
+    __shared__ double red[4][256];
+    double rr = 0.0, am = 0.0, uu = 0.0, bb = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        cplx r = {-b[i].re, -b[i].im};
+        double ab = 0.0;
+        for (int q = 0; q < slices; ++q) {
+            r = r + part[static_cast<size_t>(q) * n + i];
+            ab += absrow[static_cast<size_t>(q) * n + i];
+        }
+        rr += abs2(r);
+        am = fmax(am, ab);
+        uu += abs2(u[i]);
+        bb += abs2(b[i]);
+    }
+    red[0][threadIdx.x] = rr; red[1][threadIdx.x] = am; red[2][threadIdx.x] = uu; red[3][threadIdx.x] = bb;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + w];
+            red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + w]);
+            red[2][threadIdx.x] += red[2][threadIdx.x + w];
+            red[3][threadIdx.x] += red[3][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        norms[0] = sqrt(red[0][0]);
+        norms[1] = red[1][0];
+        norms[2] = sqrt(red[2][0]);
+        norms[3] = sqrt(red[3][0]);
+    }
+}
+
 __global__ void gather_channels_kernel(const cplx* __restrict__ rhs, size_t rstride, const int* __restrict__ ch,
                                        int K, int B, cplx* __restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -95,6 +167,7 @@ struct fds_bem {
     cudaEvent_t ev[4] = {};
     double t_asm = 0, t_lu = 0, t_solve = 0;
     int launches = 0;
+    double cum[4] = {0, 0, 0, 0};  // assembly / LU / solve ms and frequencies since create or reset
 
     void ensure(int B) {
         if (B <= cap) return;
@@ -200,6 +273,10 @@ struct fds_bem {
         FDS_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
         t_solve = ms;
         launches = static_cast<int>(g_launches.load() - l0);
+        cum[0] += t_asm;
+        cum[1] += t_lu;
+        cum[2] += t_solve;
+        cum[3] += B;
     }
 };
 
@@ -390,6 +467,63 @@ int fds_bem_assemble_host(fds_bem* h, fds_c64 s, fds_c64* A, fds_c64* b) {
     });
 }
 
+int fds_bem_assemble_entries(fds_bem* h, fds_c64 s, int count, const int* rows, const int* cols, fds_c64* out,
+                             fds_c64* b) {
+    return fds_guard([&] {
+        if (!h || count < 0 || (count > 0 && (!rows || !cols || !out)))
+            throw ValidationError("fds_bem_assemble_entries: bad argument");
+        for (int i = 0; i < count; ++i)
+            if (rows[i] < 0 || rows[i] >= h->n || cols[i] < 0 || cols[i] >= h->n)
+                throw ValidationError("fds_bem_assemble_entries: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->ensure(1);
+        FDS_CUDA(cudaMemcpyAsync(h->svec, &s, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+        bem_assemble(h->dev, h->svec, 1, h->A, h->mstride, h->plane, h->ld, h->rhs, h->ld, h->st);
+        if (count > 0) {
+            int* drc = nullptr;
+            cplx* dout = nullptr;
+            FDS_CUDA(cudaMallocAsync(&drc, 2 * static_cast<size_t>(count) * sizeof(int), h->st));
+            FDS_CUDA(cudaMallocAsync(&dout, static_cast<size_t>(count) * sizeof(cplx), h->st));
+            FDS_CUDA(cudaMemcpyAsync(drc, rows, count * sizeof(int), cudaMemcpyHostToDevice, h->st));
+            FDS_CUDA(cudaMemcpyAsync(drc + count, cols, count * sizeof(int), cudaMemcpyHostToDevice, h->st));
+            FDS_LAUNCH(gather_entries_kernel, ceil_div(count, 256), 256, 0, h->st, h->A, h->plane, h->ld, drc, count,
+                       dout);
+            FDS_CUDA(cudaMemcpyAsync(out, dout, count * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+            FDS_CUDA(cudaFreeAsync(drc, h->st));
+            FDS_CUDA(cudaFreeAsync(dout, h->st));
+        }
+        if (b) FDS_CUDA(cudaMemcpyAsync(b, h->rhs, h->n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+        FDS_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+int fds_bem_residual(fds_bem* h, fds_c64 s, const fds_c64* u, double* norms) {
+    return fds_guard([&] {
+        if (!h || !u || !norms) throw ValidationError("fds_bem_residual: null argument");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->ensure(1);
+        FDS_CUDA(cudaMemcpyAsync(h->svec, &s, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+        bem_assemble(h->dev, h->svec, 1, h->A, h->mstride, h->plane, h->ld, h->rhs, h->ld, h->st);
+        const int n = h->n, slices = ceil_div(n, kResCols);
+        cplx *du = nullptr, *part = nullptr;
+        double *absrow = nullptr, *dn = nullptr;
+        FDS_CUDA(cudaMallocAsync(&du, n * sizeof(cplx), h->st));
+        FDS_CUDA(cudaMallocAsync(&part, static_cast<size_t>(slices) * n * sizeof(cplx), h->st));
+        FDS_CUDA(cudaMallocAsync(&absrow, static_cast<size_t>(slices) * n * sizeof(double), h->st));
+        FDS_CUDA(cudaMallocAsync(&dn, 4 * sizeof(double), h->st));
+        FDS_CUDA(cudaMemcpyAsync(du, u, n * sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+        FDS_LAUNCH(residual_partial_kernel, dim3(ceil_div(n, kResRows), slices), kResRows, 0, h->st, h->A, h->plane,
+                   h->ld, n, du, part, absrow);
+        FDS_LAUNCH(residual_reduce_kernel, 1, 256, 0, h->st, part, absrow, slices, n, h->rhs, du, dn);
+        FDS_CUDA(cudaMemcpyAsync(norms, dn, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        FDS_CUDA(cudaFreeAsync(du, h->st));
+        FDS_CUDA(cudaFreeAsync(part, h->st));
+        FDS_CUDA(cudaFreeAsync(absrow, h->st));
+        FDS_CUDA(cudaFreeAsync(dn, h->st));
+        FDS_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
 int fds_bem_last_timing(const fds_bem* h, double* a, double* l, double* s, int* launches) {
     if (!h) return FDS_EVALIDATION;
     if (a) *a = h->t_asm;
@@ -397,6 +531,16 @@ int fds_bem_last_timing(const fds_bem* h, double* a, double* l, double* s, int* 
     if (s) *s = h->t_solve;
     if (launches) *launches = h->launches;
     return FDS_OK;
+}
+
+int fds_bem_cumulative_timing(fds_bem* h, double* out, int reset) {
+    return fds_guard([&] {
+        if (!h || !out) throw ValidationError("fds_bem_cumulative_timing: null argument");
+        std::lock_guard<std::mutex> lk(h->mu);
+        for (int i = 0; i < 4; ++i) out[i] = h->cum[i];
+        if (reset)
+            for (double& c : h->cum) c = 0.0;
+    });
 }
 
 int fds_bem_set_solver(fds_bem* h, int kind, double tol, int restart, int max_iter) {

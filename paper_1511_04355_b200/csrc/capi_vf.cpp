@@ -270,7 +270,27 @@ void export_afs(const AfsOut& r, int channels, int cap, fds_c64* samples, fds_c6
     sum->solver_calls = r.solver_calls;
     sum->n_history = static_cast<int>(r.history.size());
     sum->order = static_cast<int>(r.poles.size());
+    sum->n_orf = static_cast<int>(r.orf.size());
+    for (int i = 0; i < 8; ++i) sum->orf_indices[i] = i < sum->n_orf ? r.orf[i] : -1;
     (void)channels;
+}
+
+// Runs the driver; on an exception the completed iterations are exported
+// before the error propagates (fds_run_afs_* contract in fdsweep_b200.h).
+void run_and_export(const BatchEval& eval, int channels, const fds_afs_config* cfg, int cap, fds_c64* samples,
+                    fds_c64* values, double* hist, fds_c64* poles, fds_c64* residues, fds_afs_summary* sum) {
+    AfsOut r;
+    try {
+        run_afs_impl(eval, channels, cfg_of(cfg), r);
+    } catch (...) {
+        r.poles.clear();
+        r.residues.clear();
+        r.converged = false;
+        if (static_cast<int>(r.samples.size()) <= cap && static_cast<int>(r.history.size()) <= cap)
+            export_afs(r, channels, cap, samples, values, hist, poles, residues, sum);
+        throw;
+    }
+    export_afs(r, channels, cap, samples, values, hist, poles, residues, sum);
 }
 
 }  // namespace
@@ -288,8 +308,7 @@ int fds_run_afs_bem(fds_bem* bem, const fds_afs_config* cfg, int cap, fds_c64* s
             if (rc == FDS_ECONVERGENCE) throw ConvergenceError(fds_last_error());
             if (rc != FDS_OK) throw CudaError(fds_last_error());
         };
-        const AfsOut r = run_afs_impl(eval, K, cfg_of(cfg));
-        export_afs(r, K, cap, samples, values, hist, poles, residues, sum);
+        run_and_export(eval, K, cfg, cap, samples, values, hist, poles, residues, sum);
     });
 }
 
@@ -304,8 +323,7 @@ int fds_run_afs_callback(fds_system_fn fn, void* user, int channels, const fds_a
                     throw NumericError("run_afs: system evaluation failed");
             }
         };
-        const AfsOut r = run_afs_impl(eval, channels, cfg_of(cfg));
-        export_afs(r, channels, cap, samples, values, hist, poles, residues, sum);
+        run_and_export(eval, channels, cfg, cap, samples, values, hist, poles, residues, sum);
     });
 }
 

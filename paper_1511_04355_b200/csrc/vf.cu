@@ -25,7 +25,7 @@
 #include <cmath>
 #include <limits>
 
-#include "host_linalg.h"
+#include "eig_host.h"
 #include "vf.cuh"
 
 namespace fdsb {
@@ -621,44 +621,32 @@ RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const
         gwork = dev<double>(cx.qr, static_cast<size_t>(rows) * cols * K);
         smem = 0;
     } else {
-        static size_t attr = 0;
-        if (smem > attr) {
-            FDS_CUDA(cudaFuncSetAttribute(vf_reloc_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-            attr = smem;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(vf_reloc_qr_kernel), smem);
     }
     FDS_LAUNCH(vf_reloc_qr_kernel, K, 256, smem, cx.st, J, M, K, dvals, dphi, dsc, dsc + M, gwork, dr22, dbeta,
                dtail);
-    std::vector<double> hr(static_cast<size_t>(K) * red * M), hb(static_cast<size_t>(K) * red), ht(K);
-    FDS_CUDA(cudaMemcpyAsync(hr.data(), dr22, hr.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
-    FDS_CUDA(cudaMemcpyAsync(hb.data(), dbeta, hb.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
-    FDS_CUDA(cudaMemcpyAsync(ht.data(), dtail, ht.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    // stacked sigma least squares (vecfit.cpp:281-285) and the per-channel RMS
+    // (:287-295) on the device; only y, the RMS and the rank come back
+    double* dy = dev<double>(cx.lsq_io, static_cast<size_t>(M) + K + 2 * sizeof(VfLsqStatus) / sizeof(double) + 2);
+    double* drms = dy + M;
+    auto* dstat = reinterpret_cast<VfLsqStatus*>(drms + K);
+    vf_lsq_launch(K * red, M, dr22, M, 1, dbeta, dy, nullptr, nullptr, dstat, cx.st);
+    vf_reloc_rms_launch(K, red, M, J, dr22, dbeta, dtail, dy, drms, cx.st);
+    std::vector<double> hy(static_cast<size_t>(M) + K);
+    VfLsqStatus hst;
+    FDS_CUDA(cudaMemcpyAsync(&hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(hy.data(), dy, hy.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
     FDS_CUDA(cudaStreamSynchronize(cx.st));
-    // stacked sigma least squares (vecfit.cpp:281-285)
-    hla::Dense st(K * red, M);
-    std::vector<double> rhs(static_cast<size_t>(K) * red);
-    for (int k = 0; k < K; ++k)
-        for (int i = 0; i < red; ++i) {
-            for (int c = 0; c < M; ++c) st.at(k * red + i, c) = hr[(static_cast<size_t>(k) * red + i) * M + c];
-            rhs[static_cast<size_t>(k) * red + i] = hb[static_cast<size_t>(k) * red + i];
-        }
-    const hla::PivotedQR solver(st);
-    if (solver.rank() < M) throw NumericError("relocate_poles: rank-deficient least-squares system");
-    const std::vector<double> y = solver.solve(rhs);
+    if (hst.rank < M) throw NumericError("relocate_poles: rank-deficient least-squares system");
+    const std::vector<double> y(hy.begin(), hy.begin() + M);
     RelocResult out;
-    out.rms.assign(K, 0.0);
-    for (int k = 0; k < K; ++k) {  // vecfit.cpp:287-295
-        double c2 = 0.0;
-        for (int i = 0; i < red; ++i) {
-            double v = -hb[static_cast<size_t>(k) * red + i];
-            for (int c = 0; c < M; ++c) v += hr[(static_cast<size_t>(k) * red + i) * M + c] * y[c];
-            c2 += v * v;
-        }
-        out.rms[k] = std::sqrt((c2 + ht[k]) / J);
-    }
+    out.rms.assign(hy.begin() + M, hy.end());
     // zeros of sigma: eig(blockdiag(poles) - b c^T) (vecfit.cpp:297-324)
-    hla::Dense h(M, M);
+    struct {
+        int m;
+        std::vector<double> v;
+        double& at(int i, int j) { return v[static_cast<size_t>(j) * m + i]; }
+    } h{M, std::vector<double>(static_cast<size_t>(M) * M, 0.0)};
     std::vector<double> bv(M), cr(M);
     for (int m = 0; m < M;) {
         if (poles[m].imag() != 0.0) {
@@ -681,7 +669,7 @@ RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const
     for (int i = 0; i < M; ++i)
         for (int c = 0; c < M; ++c) h.at(i, c) -= bv[i] * cr[c];
     std::vector<Cx> ev;
-    if (!hla::eigenvalues(h, ev)) throw NumericError("relocate_poles: eigenvalue iteration failed");
+    if (!eig::eigenvalues(M, h.v.data(), ev)) throw NumericError("relocate_poles: eigenvalue iteration failed");
     std::vector<Cx> heads, reals;
     int neg = 0;
     for (Cx e : ev) {
@@ -705,29 +693,34 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
     if (2 * J < M) throw ValidationError("identify_residues: too few samples for the order");
     require_distinct(s);
     const std::vector<Cx> phi = basis(s, poles);
-    hla::Dense a(2 * J, M);
-    std::vector<double> scale(M);
+    const int rows = 2 * J;
+    std::vector<double> a(static_cast<size_t>(rows) * M), scale(M);  // column-major [Re Phi; Im Phi]
     for (int m = 0; m < M; ++m) {
         double n2 = 0.0;
         for (int j = 0; j < J; ++j) {
             const Cx v = phi[static_cast<size_t>(m) * J + j];
-            a.at(2 * j, m) = v.real();
-            a.at(2 * j + 1, m) = v.imag();
+            a[static_cast<size_t>(m) * rows + 2 * j] = v.real();
+            a[static_cast<size_t>(m) * rows + 2 * j + 1] = v.imag();
             n2 += v.real() * v.real() + v.imag() * v.imag();
         }
         const double n = std::sqrt(n2);
         scale[m] = n > 0.0 ? 1.0 / n : 1.0;
-        for (int i = 0; i < 2 * J; ++i) a.at(i, m) *= scale[m];
+        for (int i = 0; i < rows; ++i) a[static_cast<size_t>(m) * rows + i] *= scale[m];
     }
-    const hla::PivotedQR qr(a);
-    if (qr.rank() < M) throw NumericError("identify_residues: rank-deficient least-squares system");
-    const hla::Dense W0 = qr.solve_operator();  // M x 2J
-    std::vector<double> W(static_cast<size_t>(M) * 2 * J);
-    for (int m = 0; m < M; ++m)
-        for (int i = 0; i < 2 * J; ++i) W[static_cast<size_t>(m) * 2 * J + i] = scale[m] * W0.at(m, i);
+    // one shared pivoted QR (vecfit.cpp:389) turned into the solve operator
+    // W (M x 2J, rows pre-scaled) on the device
     auto& cx = VfContext::get();
-    double* dW = dev<double>(cx.W, W.size());
-    FDS_CUDA(cudaMemcpyAsync(dW, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    double* da = dev<double>(cx.lsq_io, a.size() + M + 2 * sizeof(VfLsqStatus) / sizeof(double) + 2);
+    double* dscale = da + a.size();
+    auto* dstat = reinterpret_cast<VfLsqStatus*>(dscale + M);
+    double* dW = dev<double>(cx.W, static_cast<size_t>(M) * rows);
+    FDS_CUDA(cudaMemcpyAsync(da, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    FDS_CUDA(cudaMemcpyAsync(dscale, scale.data(), M * sizeof(double), cudaMemcpyHostToDevice, st));
+    vf_lsq_launch(rows, M, da, 1, rows, nullptr, nullptr, dW, dscale, dstat, st);
+    VfLsqStatus hst;
+    FDS_CUDA(cudaMemcpyAsync(&hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, st));
+    FDS_CUDA(cudaStreamSynchronize(st));
+    if (hst.rank < M) throw NumericError("identify_residues: rank-deficient least-squares system");
     const int P = pair_count(poles);
     const size_t smem = static_cast<size_t>(kResChunk) * 2 * J * sizeof(double);
     static size_t attr = 0;

@@ -20,9 +20,22 @@ struct VfContext {
         size_t bytes = 0;
         void* get(size_t need);
     };
-    Buf values, resid, W, phi, rms, tab, tab2, out, misc, misc2, qr;
+    Buf values, resid, W, phi, rms, tab, tab2, out, misc, misc2, qr, lsq, lsq_io;
     static VfContext& get();
 };
+
+// ------------------------------------------------------------------ device least squares (vf_lsq.cu)
+struct VfLsqStatus {
+    int rank, nonzero;
+    double maxpivot;
+};
+// Column-pivoted QR least squares of the m x n system in(i, j) = in[i*rs + j*cs]
+// on one CTA: x_out = solution for rhs, or w_out[c*m + i] = wscale[c] W(c, i)
+// (explicit solve operator). status->rank < n means rank-deficient (no output).
+void vf_lsq_launch(int m, int n, const double* in, long long rs, long long cs, const double* rhs, double* x_out,
+                   double* w_out, const double* wscale, VfLsqStatus* status, cudaStream_t st);
+void vf_reloc_rms_launch(int K, int red, int M, int J, const double* r22, const double* beta, const double* tail,
+                         const double* y, double* rms, cudaStream_t st);
 
 // ------------------------------------------------------------------ host helpers
 std::vector<Cx> canonical_order(const std::vector<Cx>& poles);  // vecfit.cpp:134-169

@@ -1,0 +1,175 @@
+"""Oracle parity at the north_star's own sizes and on the AFS path with BEM data.
+
+* cfg4 (5120-triangle sphere, N = 15360, random traction seed 0): the GPU
+  solution against the CPU oracle (oracle assembly + OpenBLAS zgetrf/zgetrs)
+  at two frequencies of the T = 20 contour, rel-L2 < 1e-9 (the contract of
+  `FrequencySystem::evaluate`, /root/reference/proj/include/fdsweep/systems.hpp:34-42),
+  through both LU schedules (single-matrix look-ahead, batched super-panels);
+  plus ~10^4 entries of A(s) and 64 entries of b(s) against the oracle's
+  assembly at 1e-12 of max|A|.
+* cfg3 (unit-cube cavity, N = 36864, 21.7 GB): LU-path backward error computed
+  on the device, and sampled A(s), b(s) entries against the oracle.
+* AFS on BEM responses with finite, converging thresholds: the product
+  run_afs (GPU BEM + GPU VF) against the reference's own run_afs
+  (/root/reference/proj/src/afs.cpp:226-396, compiled unmodified in the oracle)
+  on the oracle BEM: identical sampled-frequency sequence, identical orders,
+  E1 and E2 columns.
+* Failure-mode parity at the reference defaults (afs.hpp:21-39) on the
+  pressurised cfg1 sphere: the same exception class after the same samples.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1511_04355_b200 as P
+import pyoracle as O
+from helpers import worst_match
+from paper_1511_04355_b200 import mesh
+
+pytestmark = pytest.mark.gpu
+
+T_PERIOD = 20.0
+
+
+def contour(k):
+    return complex(5.0 / T_PERIOD, 2 * math.pi / T_PERIOD * k)
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def _sample_entries(V, F, n_random, n_elems, seed):
+    """Random (row, col) pairs plus every entry of the self block and of the
+    8 nearest source elements (near-singular subdivision levels) of n_elems
+    random collocation elements."""
+    rng = np.random.default_rng(seed)
+    ne = F.shape[0]
+    n = 3 * ne
+    rows = list(rng.integers(0, n, n_random))
+    cols = list(rng.integers(0, n, n_random))
+    cen = V[F].mean(axis=1)
+    for c in rng.choice(ne, n_elems, replace=False):
+        d = np.linalg.norm(cen - cen[c], axis=1)
+        for e in np.argsort(d)[:9]:  # includes c itself (self block)
+            for i in range(3):
+                for j in range(3):
+                    rows.append(3 * c + i)
+                    cols.append(3 * e + j)
+    return np.array(rows, np.int32), np.array(cols, np.int32)
+
+
+@pytest.fixture(scope="module")
+def cfg4():
+    V, F = mesh.icosphere(4)
+    tr = mesh.random_traction(F.shape[0], seed=0)
+    return V, F, tr
+
+
+def test_cfg4_solution_matches_oracle_n15360(cfg4):
+    V, F, tr = cfg4
+    s7, s200 = contour(7), contour(200)
+    orc = O.Bem(V, F, tr)
+    ob = O.openblas_path()
+    uo7, _ = orc.solve_openblas(s7, ob)
+    uo200, _ = orc.solve_openblas(s200, ob)
+    gpu = P.BemSystem(V, F, tr, max_batch=2)
+    u_single = gpu.evaluate(s7)  # look-ahead schedule (one matrix)
+    u_batch = gpu.evaluate_batch([s7, s200])  # super-panel schedule (batch)
+    e = [rel_l2(u_single, uo7), rel_l2(u_batch[0], uo7), rel_l2(u_batch[1], uo200)]
+    print(f"cfg4 rel-L2 vs oracle: single k=7 {e[0]:.2e}, batch k=7 {e[1]:.2e}, batch k=200 {e[2]:.2e}")
+    assert max(e) < 1e-9
+    gpu.close()
+
+
+def test_cfg4_assembly_entries_match_oracle(cfg4):
+    V, F, tr = cfg4
+    rows, cols = _sample_entries(V, F, 9000, 12, seed=4)
+    assert len(rows) >= 9000 + 12 * 81
+    orc = O.Bem(V, F, tr)
+    gpu = P.BemSystem(V, F, tr, max_batch=1)
+    brow = np.random.default_rng(5).choice(3 * F.shape[0], 64, replace=False)
+    for k in (7, 200):
+        s = contour(k)
+        ag, bg = gpu.assemble_entries(s, rows, cols, with_rhs=True)
+        ao = orc.entries(s, rows, cols)
+        scale = np.abs(ao).max()
+        err = np.abs(ag - ao).max() / scale
+        bo = orc.rhs_rows(s, brow)
+        berr = np.abs(bg[brow] - bo).max() / np.abs(bo).max()
+        print(f"cfg4 k={k}: A entries max err {err:.2e} of max|A|, b rows {berr:.2e}")
+        assert err < 1e-12 and berr < 1e-12
+    gpu.close()
+
+
+def test_cfg3_lu_backward_error_and_entries_n36864():
+    V, F = mesh.cube_cavity(32)
+    tr = mesh.pressure_traction(V, F)
+    assert F.shape[0] == 12288
+    s = contour(7)
+    gpu = P.BemSystem(V, F, tr, max_batch=1)
+    u = gpu.evaluate(s)
+    nr = gpu.residual(s, u)
+    back = nr["res"] / (nr["a_inf"] * nr["u"] + nr["b"])
+    print(f"cfg3 N=36864: ||Au-b||/(||A|| ||u|| + ||b||) = {back:.2e}, ||Au-b||/||b|| = {nr['res'] / nr['b']:.2e}")
+    assert back < 1e-13 and nr["res"] / nr["b"] < 1e-10
+    rows, cols = _sample_entries(V, F, 2000, 6, seed=3)
+    orc = O.Bem(V, F, tr)
+    ag, bg = gpu.assemble_entries(s, rows, cols, with_rhs=True)
+    ao = orc.entries(s, rows, cols)
+    assert np.abs(ag - ao).max() < 1e-12 * np.abs(ao).max()
+    brow = np.random.default_rng(6).choice(3 * F.shape[0], 16, replace=False)
+    bo = orc.rhs_rows(s, brow)
+    assert np.abs(bg[brow] - bo).max() < 1e-12 * np.abs(bo).max()
+    gpu.close()
+
+
+def _normal_channels(V, F, count):
+    el = np.arange(0, F.shape[0], F.shape[0] // count)[:count]
+    nrm = np.cross(V[F[el, 1]] - V[F[el, 0]], V[F[el, 2]] - V[F[el, 0]])
+    return [int(3 * e + np.argmax(np.abs(n))) for e, n in zip(el, nrm)]
+
+
+def test_afs_bem_finite_thresholds_identical_sequence():
+    """cfg1 mesh (320 triangles) under the Heaviside pressure, 32 channels (the
+    normal-dominant displacement DOF of every 10th element), J0 = 8 and
+    E1 = E2 = 1e-3: both drivers converge after the same adaptively selected
+    frequencies (51 samples), through the reference's convergence test and
+    validation streak (afs.cpp:359-361)."""
+    V, F = mesh.icosphere(2)
+    tr = mesh.pressure_traction(V, F)
+    ch = _normal_channels(V, F, 32)
+    kw = dict(omega_max=math.pi * 256 / T_PERIOD, eta=0.25, period=T_PERIOD, initial_count=8,
+              e1_threshold=1e-3, e2_threshold=1e-3)
+    o = O.run_afs(O.System.bem(O.Bem(V, F, tr), ch), **kw)
+    r = P.run_afs(P.BemSystem(V, F, tr, channels=ch, max_batch=8), **kw)
+    assert o["converged"] and r["converged"]
+    assert r["n_c"] == o["n_c"] and r["solver_calls"] == o["solver_calls"]
+    np.testing.assert_array_equal(r["samples"], o["samples"])
+    np.testing.assert_array_equal(r["history"][:, :6], o["history"][:, :6])
+    np.testing.assert_allclose(r["history"][:, 7], o["history"][:, 7], rtol=1e-6)  # E2
+    e1o, e1r = o["history"][1:, 6], r["history"][1:, 6]  # E1 (first row is inf in both)
+    assert np.isinf(o["history"][0, 6]) and np.isinf(r["history"][0, 6])
+    np.testing.assert_allclose(e1r, e1o, rtol=1e-6)
+    assert worst_match(r["poles"], o["poles"]) < 1e-6
+    assert r["orf"] == list(o["orf"])
+
+
+def test_afs_reference_defaults_failure_mode_pressurised_sphere():
+    """Reference defaults (afs.hpp:21-39; every DOF a channel, 5 ORFs drawn with
+    seed 0) on the pressurised cfg1 sphere: the reference algorithm throws
+    NumericError from relocate_poles. The product must raise the
+    same class after solving the same frequencies."""
+    V, F = mesh.icosphere(2)
+    tr = mesh.pressure_traction(V, F)
+    kw = dict(omega_max=math.pi * 256 / T_PERIOD, eta=0.25, period=T_PERIOD)
+    with pytest.raises(O.OracleError) as eo:
+        O.run_afs(O.System.bem(O.Bem(V, F, tr), list(range(3 * F.shape[0]))), **kw)
+    with pytest.raises(P.Error) as er:
+        P.run_afs(P.BemSystem(V, F, tr, max_batch=16), **kw)
+    assert eo.value.kind == "NumericError" and type(er.value).__name__ == eo.value.kind
+    po, pr = eo.value.partial, er.value.partial
+    print(f"reference defaults: {eo.value.kind} after {po['n_c']} samples (product {pr['n_c']})")
+    assert pr["n_c"] == po["n_c"]
+    np.testing.assert_array_equal(pr["samples"], po["samples"])
