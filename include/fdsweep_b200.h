@@ -57,8 +57,15 @@ int fds_set_device(int device);
  * Laplace-domain 3D elastodynamic collocation BEM on constant flat
  * triangles; unknowns element-major u[3e + {x,y,z}]; load = per-element
  * traction vector x Heaviside factor 1/s. The handle is immutable after
- * create; evaluate is deterministic (bit-identical for equal s) and
- * reentrant (calls are serialised per handle on its own stream).
+ * create; evaluate is reentrant (calls are serialised per handle on its own
+ * stream; factorizations of different handles in one process are serialised
+ * per device) and deterministic: a frequency solved in a batch of the same
+ * size gives bit-identical results on every call (all reductions have a fixed
+ * order; the batch chunk size of a handle with max_batch = 0 is fixed at its
+ * first evaluate). Across batch sizes the 3M trailing update groups its
+ * rank-64 (single matrix) or rank-128 (batch) updates differently, so the
+ * same s agrees to rounding (~1e-15 relative), not bit for bit;
+ * FDSWEEP_GEMM=4m restores bit-identity across batch sizes.
  * ---------------------------------------------------------------------- */
 typedef struct fds_bem fds_bem;
 
@@ -73,7 +80,7 @@ typedef struct {
     const double* traction;   /* [n_elements][3], multiplied by p(s) = 1/s */
     int n_channels;           /* output DOFs; 0 => all 3*n_elements */
     const int* channels;      /* DOF indices into u */
-    int max_batch;            /* frequencies solved concurrently; 0 => auto from free HBM */
+    int max_batch;            /* frequencies solved concurrently; 0 => from the free HBM at the first evaluate */
 } fds_bem_desc;
 
 int fds_bem_create(const fds_bem_desc* desc, fds_bem** out);

@@ -18,21 +18,23 @@ namespace fdsb {
 std::atomic<int64_t> g_launches{0};
 
 const DeviceInfo& device_info() {
-    static thread_local DeviceInfo info;
-    static thread_local bool init = false;
-    if (!init) {
-        int dev = 0;
-        FDS_CUDA(cudaGetDevice(&dev));
-        cudaDeviceProp p;
-        FDS_CUDA(cudaGetDeviceProperties(&p, dev));
-        if (p.major != 10) throw CudaError("fdsweep_b200 is built for sm_100a (B200); found sm_" +
-                                           std::to_string(p.major) + std::to_string(p.minor));
-        info.device = dev;
-        info.sms = p.multiProcessorCount;
-        info.smem_optin = p.sharedMemPerBlockOptin;
-        init = true;
-    }
-    return info;
+    // per device (fds_set_device may switch the calling thread's device)
+    int dev = 0;
+    FDS_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<int, DeviceInfo> infos;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = infos.find(dev);
+    if (it != infos.end()) return it->second;
+    cudaDeviceProp p;
+    FDS_CUDA(cudaGetDeviceProperties(&p, dev));
+    if (p.major != 10) throw CudaError("fdsweep_b200 is built for sm_100a (B200); found sm_" +
+                                       std::to_string(p.major) + std::to_string(p.minor));
+    DeviceInfo info;
+    info.device = dev;
+    info.sms = p.multiProcessorCount;
+    info.smem_optin = p.sharedMemPerBlockOptin;
+    return infos.emplace(dev, info).first->second;
 }
 
 thread_local std::string g_error;
@@ -188,15 +190,18 @@ struct fds_bem {
         cap = B;
     }
 
-    int chunk_limit() const {
+    int auto_batch = 0;  // max_batch == 0: fixed at the first evaluate (deterministic chunking)
+    int chunk_limit() {
         if (max_batch > 0) return max_batch;
+        if (auto_batch > 0) return auto_batch;
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         // matrix + b-partials + the 3M update's operand planes (LuWorkspace::g3_planes) + slack
         const size_t per = mstride * sizeof(double) + dev.pstride * sizeof(cplx) +
                            static_cast<size_t>(ld) * (2 * 128 + 136) * sizeof(double) + 4096 * 64;
         const size_t budget = static_cast<size_t>(0.85 * (fr + static_cast<size_t>(cap) * per));
-        return std::max<int>(1, static_cast<int>(budget / std::max<size_t>(per, 1)));
+        auto_batch = std::max<int>(1, static_cast<int>(budget / std::max<size_t>(per, 1)));
+        return auto_batch;
     }
 
     // Solves B frequencies already in svec_host; result (B x K) left in `out` on device.
@@ -211,6 +216,7 @@ struct fds_bem {
         launches = 0;
         t_asm = t_lu = t_solve = 0;
         const int64_t l0 = g_launches.load();
+        const auto gate = lu_device_gate();  // held until the stream synchronises below
         ensure(B);
         FDS_CUDA(cudaMemcpyAsync(svec, s_host, B * sizeof(cplx), cudaMemcpyHostToDevice, st));
         FDS_CUDA(cudaEventRecord(ev[0], st));
@@ -601,9 +607,12 @@ int fds_zgesv_batch(int n, int B, const fds_c64* A, const fds_c64* rhs, fds_c64*
         pb.ipiv = dp.p;
         pb.info = di.p;
         LuWorkspace ws;
-        lu_factor(pb, ws, st);
-        lu_solve(pb, dr.p, ld, ws, st);
-        FDS_CUDA(cudaStreamSynchronize(st));
+        {
+            const auto gate = lu_device_gate();
+            lu_factor(pb, ws, st);
+            lu_solve(pb, dr.p, ld, ws, st);
+            FDS_CUDA(cudaStreamSynchronize(st));
+        }
         ws.release();
         std::vector<int> info(B);
         FDS_CUDA(cudaMemcpy(info.data(), di.p, B * sizeof(int), cudaMemcpyDeviceToHost));
@@ -630,6 +639,7 @@ int fds_lu_factor_device(int n, int B, double* A_planar, int* ipiv, int* info, d
         cudaEvent_t e0, e1;
         FDS_CUDA(cudaEventCreate(&e0));
         FDS_CUDA(cudaEventCreate(&e1));
+        const auto gate = lu_device_gate();
         FDS_CUDA(cudaEventRecord(e0, nullptr));
         lu_factor(pb, ws, nullptr);
         FDS_CUDA(cudaEventRecord(e1, nullptr));

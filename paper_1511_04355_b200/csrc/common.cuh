@@ -1,6 +1,8 @@
 // Shared device/host helpers for the fdsweep_b200 sm_100a library.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -9,6 +11,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "fdsweep_b200.h"
@@ -32,18 +35,35 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define FDS_CUDA(x) ::fdsb::cuda_check((x), #x)
 
 // Opt a kernel into `bytes` of dynamic shared memory (> 48 KB needs the
-// attribute), tracked per kernel — several template instances launched from
-// one generic lambda must not share one "already set" flag.
+// attribute), tracked per (device, kernel) — several template instances
+// launched from one generic lambda must not share one "already set" flag, and
+// the attribute is per device context.
 inline void ensure_dynamic_smem(const void* fn, size_t bytes) {
     if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     static std::mutex mu;
-    static std::map<const void*, size_t> done;
+    static std::map<std::pair<int, const void*>, size_t> done;
     std::lock_guard<std::mutex> lk(mu);
-    size_t& have = done[fn];
+    size_t& have = done[{dev, fn}];
     if (bytes <= have) return;
     cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
                "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
     have = bytes;
+}
+// Once-per-(device, key) initialisation (constant-memory tables, occupancy queries).
+template <class F>
+inline void once_per_device(const void* key, F init) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, bool> done;
+    std::lock_guard<std::mutex> lk(mu);
+    bool& d = done[{dev, key}];
+    if (!d) {
+        init();
+        d = true;
+    }
 }
 // Every kernel launch of the library goes through this (launch accounting +
 // immediate launch-error check).
@@ -88,6 +108,67 @@ __device__ __forceinline__ cplx cexpd(cplx z) {
 }
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    return encode;
+}
+
+// ---------------------------------------------------------------- mbarrier / TMA (sm_90+ async proxy)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0),
+        "r"(c1), "r"(c2), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0),
+        "r"(c1), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n"
+                 ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))) : "memory");
+}
+// 1-D bulk copy global -> shared (16 B aligned addresses, size a multiple of 16),
+// completion counted on the mbarrier's transaction bytes.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(src), "r"(bytes),
+        "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
 
 // Optional per-kernel timing (bench roofline): when enabled, selected launches
 // are bracketed by CUDA events on their stream; totals are read back with

@@ -31,6 +31,7 @@
 #include <math.h>
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "vf.cuh"
 
@@ -358,8 +359,13 @@ struct Fsm256Lane {
 
 // One DOF: X = its staged half spectrum (N_s/2 + 1 values, buffer of kFsmBuf),
 // reused in place as the exchange buffer; o = its N_s output samples.
-__device__ __forceinline__ void fsm256_dof(cplx* X, const cplx* __restrict__ pst, int hanning, int lane,
-                                           const Fsm256Lane& c, double2* __restrict__ o) {
+// rd(n) returns spectrum value n of the DOF; X is the DOF's exchange buffer
+// (kFsmBuf cplx, may alias the spectrum: every rd() happens before the first
+// write); released() runs once the spectrum has been read.
+template <class Rd, class Rel>
+__device__ __forceinline__ void fsm256_dof_rd(Rd rd, Rel released, cplx* X, const cplx* __restrict__ pst,
+                                              int hanning, int lane, const Fsm256Lane& c,
+                                              double2* __restrict__ o) {
     constexpr int L = kFsmL;
     // pack Z_n = (x_n + conj x_{L-n}) + i e^{2πi n/N_s} (x_n - conj x_{L-n}), windowed,
     // k = 0 and N_s/2 forced real (laplace.cpp:80-81)
@@ -367,7 +373,7 @@ __device__ __forceinline__ void fsm256_dof(cplx* X, const cplx* __restrict__ pst
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
         const int n = lane + 32 * m;
-        cplx xk = X[n], xm = X[L - n];
+        cplx xk = rd(n), xm = rd(L - n);
         if (m == 0 && lane == 0) { xk.im = 0.0; xm.im = 0.0; }
         const cplx pm = pst[n];
         if (hanning) {
@@ -381,6 +387,7 @@ __device__ __forceinline__ void fsm256_dof(cplx* X, const cplx* __restrict__ pst
     // pass 1 (radix 8, no twiddle): inputs n = lane + 32 t, outputs 8 lane + t
     dft8_inv<1>(y);
     __syncwarp();
+    released();
 #pragma unroll
     for (int t = 0; t < 8; ++t) X[fpad(8 * lane + t)] = y[t];
     __syncwarp();
@@ -418,6 +425,11 @@ __device__ __forceinline__ void fsm256_dof(cplx* X, const cplx* __restrict__ pst
             __stcs(&o[lane + 32 * h + 64 * t], make_double2(z.re * (w.x * gt), z.im * (w.y * gt)));
         }
     __syncwarp();
+}
+
+__device__ __forceinline__ void fsm256_dof(cplx* X, const cplx* __restrict__ pst, int hanning, int lane,
+                                           const Fsm256Lane& c, double2* __restrict__ o) {
+    fsm256_dof_rd([X](int n) { return X[n]; }, [] {}, X, pst, hanning, lane, c, o);
 }
 
 // Warp-private pipeline: each warp streams groups of D adjacent DOFs through a
@@ -525,6 +537,80 @@ fsm_stockham256_tile_kernel(int K, const cplx* __restrict__ half, size_t sk, siz
         slot = (slot + 1) % P;
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// TMA variant for frequency-major spectra (default): groups of 8 adjacent DOFs.
+// A producer warp loads each group's 257 x 128 B block with two
+// cp.async.bulk.tensor.2d boxes (rows 0-255, row 256) under the 128 B swizzle
+// into an ST-deep ring (no per-element copy instructions, ST - 1 groups in
+// flight per SM); each of 8 consumer warps transforms one DOF, reading its
+// spectrum through the swizzle (element (n, d) at n*128 + 16 (d ^ (n & 7)): the
+// 32 lanes' reads of one spectrum row set fill every bank once per 8 lanes)
+// and exchanging its Stockham passes in a private buffer, then releases the
+// stage as soon as the spectrum is consumed.
+constexpr int kFtDofs = 8;
+constexpr unsigned kFtStageBytes = 33 * 1024;  // 257 rows x 128 B, 1 KB aligned
+template <int ST>
+__global__ void __launch_bounds__(32 * (1 + kFtDofs), 1)
+fsm256_tma_kernel(const __grid_constant__ CUtensorMap tm_lo, const __grid_constant__ CUtensorMap tm_hi, int K,
+                  int hanning, double edt, const cplx* __restrict__ gpost, const cplx* __restrict__ gtw,
+                  const double* __restrict__ gwout, double* __restrict__ out) {
+    extern __shared__ unsigned char ft_raw[];
+    const unsigned raw = static_cast<unsigned>(__cvta_generic_to_shared(ft_raw));
+    unsigned char* base = ft_raw + ((1024u - (raw & 1023u)) & 1023u);
+    cplx* xbuf = reinterpret_cast<cplx*>(base + ST * kFtStageBytes);  // kFtDofs x kFsmBuf
+    cplx* pst = xbuf + kFtDofs * kFsmBuf;
+    uint64_t* full = reinterpret_cast<uint64_t*>(pst + kFsmL);
+    uint64_t* empty = full + ST;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int groups = (K + kFtDofs - 1) / kFtDofs;
+    for (int j = threadIdx.x; j < kFsmL; j += blockDim.x) pst[j] = gpost[j];
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < ST; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kFtDofs);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            int i = 0;
+            for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
+                const int q = i % ST;
+                if (i >= ST) mbar_wait(&empty[q], ((i / ST) - 1) & 1);
+                unsigned char* stg = base + q * kFtStageBytes;
+                mbar_expect_tx(&full[q], 257u * 128u);
+                tma_load_2d(stg, &tm_lo, &full[q], 2 * kFtDofs * g, 0);
+                tma_load_2d(stg + 256 * 128, &tm_hi, &full[q], 2 * kFtDofs * g, 256);
+            }
+        }
+        return;
+    }
+    const int d = warp - 1;
+    Fsm256Lane c;
+    c.load(lane, edt, gtw, gwout);
+    cplx* X = xbuf + d * kFsmBuf;
+    int i = 0;
+    for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
+        const int q = i % ST;
+        mbar_wait(&full[q], (i / ST) & 1);
+        const unsigned char* stg = base + q * kFtStageBytes;
+        const int k = g * kFtDofs + d;
+        auto rd = [stg, d](int n) {
+            return *reinterpret_cast<const cplx*>(stg + n * 128 + 16 * (d ^ (n & 7)));
+        };
+        auto rel = [&] {
+            if (lane == 0) mbar_arrive(&empty[q]);
+        };
+        if (k < K) {
+            fsm256_dof_rd(rd, rel, X, pst, hanning, lane, c,
+                          reinterpret_cast<double2*>(out + static_cast<size_t>(k) * (2 * kFsmL)));
+        } else {
+            __syncwarp();
+            rel();
+        }
+    }
 }
 
 __global__ void fsm_dft_kernel(int Ns, double eta, double dt, double invT, int K, const cplx* __restrict__ half,
@@ -717,11 +803,7 @@ void rat_invert_device(const std::vector<Cx>& poles, const cplx* res_mk_dev, int
     const size_t smem = 3 * static_cast<size_t>(Q) * RS * sizeof(double);
     if (smem > device_info().smem_optin - 1024) throw ValidationError("rational_invert: model order too large");
     auto go = [&](auto kern) {
-        static size_t attr = 0;
-        if (smem > 48 * 1024 && smem > attr) {
-            FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            attr = smem;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
         return kern;
     };
     dim3 g(ceil_div(K, RBM));
@@ -869,6 +951,15 @@ static bool fsm_stockham() {
     return on;
 }
 
+// Frequency-major N_s = 512 spectra take the TMA kernel unless FDSWEEP_FSM=cpasync.
+static bool fsm_tma() {
+    static const bool on = [] {
+        const char* e = std::getenv("FDSWEEP_FSM");
+        return !(e && std::string(e) == "cpasync");
+    }();
+    return on;
+}
+
 void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* half_dev, size_t sk, size_t si,
                        bool hanning, double* out_dev, cudaStream_t st) {
     if (!(period > 0.0)) throw ValidationError("FsmGrid: period must be positive");
@@ -884,12 +975,7 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
     cudaEvent_t pe;
     profiler().begin(st, kProfFsm, 0.0, pe);
     if (pow2 && L >= 2 && smem <= device_info().smem_optin - 1024) {
-        static size_t attr = 0;
-        if (smem > 48 * 1024 && smem > attr) {
-            FDS_CUDA(cudaFuncSetAttribute(fsm_c2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-            attr = smem;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(fsm_c2r_kernel), smem);
         auto& cx = VfContext::get();
         double* tab = static_cast<double*>(cx.tab2.get(sizeof(double) * (5 * static_cast<size_t>(L) + 4 + Ns)));
         double* win = tab;
@@ -899,7 +985,29 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
         FDS_LAUNCH(fsm_tables_kernel, ceil_div(Ns + 1, 256), 256, 0, st, Ns, eta, dt, invT, hanning ? 1 : 0, win, post,
                    tw, wout);
         const int R = L / 32;
-        if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1) {
+        if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1 && fsm_tma()) {
+            constexpr int ST = 5;
+            auto kern = fsm256_tma_kernel<ST>;
+            const size_t ssm = 1024 + ST * kFtStageBytes + (kFtDofs * kFsmBuf + kFsmL) * sizeof(cplx) +
+                               2 * ST * sizeof(uint64_t);
+            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), ssm);
+            CUtensorMap lo, hi;
+            PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+            const cuuint64_t dims[2] = {2 * static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(L + 1)};
+            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(si) * sizeof(cplx)};
+            const cuuint32_t estr[2] = {1, 1};
+            const cuuint32_t box_lo[2] = {2 * kFtDofs, 256}, box_hi[2] = {2 * kFtDofs, 1};
+            for (auto [t, box] : {std::pair<CUtensorMap*, const cuuint32_t*>{&lo, box_lo}, {&hi, box_hi}}) {
+                const CUresult r = encode(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<cplx*>(half_dev), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (fsm) failed (" + std::to_string(r) + ")");
+            }
+            const int ctas = std::min(ceil_div(K, kFtDofs), device_info().sms);
+            FDS_LAUNCH(kern, ctas, 32 * (1 + kFtDofs), ssm, st, lo, hi, K, hanning ? 1 : 0, eta * dt, post, tw, wout,
+                       out_dev);
+        } else if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1) {
             // frequency-major spectra: CTA-cooperative groups of adjacent DOFs.
             // 8 warps x 16-DOF groups x 2-deep ring (148 KB smem, 1 CTA/SM). Measured on the
             // 300k-DOF cfg5 spectra: 0.69 ms vs 0.77 ms for warp-private DOF pairs; 8-DOF
@@ -907,11 +1015,9 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
             constexpr int W = 8, P = 2, D = 16;
             auto kern = fsm_stockham256_tile_kernel<W, P, D>;
             const size_t ssm = (static_cast<size_t>(P) * D * kFsmStride + kFsmL) * sizeof(cplx);
-            static int per_sm = 0;
-            if (per_sm == 0) {
-                ensure_dynamic_smem(reinterpret_cast<const void*>(kern), ssm);
-                FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
-            }
+            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), ssm);
+            int per_sm = 0;
+            FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
             const int ctas = std::min(ceil_div(K, D), std::max(1, per_sm) * device_info().sms);
             FDS_LAUNCH(kern, ctas, W * 32, ssm, st, K, half_dev, sk, si, hanning ? 1 : 0, eta * dt, post, tw, wout,
                        out_dev);
@@ -920,24 +1026,18 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
             constexpr int W = 4, P = 2, D = 2;
             auto kern = fsm_stockham256_kernel<W, P, 2, D>;
             const size_t ssm = (static_cast<size_t>(W) * P * D * kFsmBuf + kFsmL) * sizeof(cplx);
-            static bool attr = false;
-            if (!attr) {
-                FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm)));
-                attr = true;
-            }
-            static int per_sm = 0;
-            if (per_sm == 0) FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
+            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), ssm);
+            int per_sm = 0;
+            FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
             const int ctas = std::min(ceil_div(ceil_div(K, D), W), std::max(1, per_sm) * device_info().sms);
             FDS_LAUNCH(kern, ctas, W * 32, ssm, st, K, half_dev, sk, si, hanning ? 1 : 0, eta * dt, post, tw, wout,
                        out_dev);
         } else if (L % 32 == 0 && (R == 1 || R == 2 || R == 4 || R == 8 || R == 16)) {
-            static bool w16 = false;
-            if (!w16) {
+            once_per_device(&c_w16, [] {
                 double h[16][2];
                 for (int j = 0; j < 16; ++j) { h[j][0] = std::cos(2.0 * M_PI * j / 16); h[j][1] = std::sin(2.0 * M_PI * j / 16); }
                 FDS_CUDA(cudaMemcpyToSymbol(c_w16, h, sizeof(h)));
-                w16 = true;
-            }
+            });
             const int OP = L + L / 32;
             const size_t wsm = (static_cast<size_t>(L + 2) + 2 * OP + 2 * L) * sizeof(double) +
                                4 * (4 * static_cast<size_t>(L + 1) + OP + 2) * sizeof(cplx);

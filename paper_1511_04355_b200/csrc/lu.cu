@@ -32,6 +32,7 @@
 
 #include <climits>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <tuple>
 #include <cstdlib>
@@ -604,32 +605,6 @@ lu_gemm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, in
 constexpr int kTmaABox0 = GAS, kTmaBBox0 = GBS;
 constexpr unsigned kTmaStageBytes = 2u * (GBK * GAS + GBN * GBS) * sizeof(double);
 constexpr size_t kTmaSmemPad = 128 + GSTAGES * sizeof(uint64_t);
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-                 "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-                 ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(a), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-        ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0),
-        "r"(c1), "r"(c2), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
-        : "memory");
-}
 
 template <int W>
 __global__ void __launch_bounds__(kGemmThreads, 2)
@@ -1872,7 +1847,6 @@ void LuWorkspace::ensure_side() {
     int lo = 0, hi = 0;
     FDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     FDS_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
-    FDS_CUDA(cudaStreamCreateWithPriority(&side_lo, cudaStreamNonBlocking, lo));
     for (auto& e : ev) FDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
@@ -1907,13 +1881,6 @@ void LuWorkspace::release() {
     if (linv_buf) cudaFree(linv_buf);
     linv_buf = nullptr;
     linv_cap = 0;
-    calu.release();
-    if (calu.top) cudaFree(calu.top);
-    if (calu.disp) cudaFree(calu.disp);
-    if (calu.moves) cudaFree(calu.moves);
-    calu.top = calu.disp = nullptr;
-    calu.moves = nullptr;
-    calu.batch_cap = 0;
     if (slots) cudaFree(slots);
     if (counters) cudaFree(counters);
     slots = nullptr;
@@ -1922,10 +1889,9 @@ void LuWorkspace::release() {
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);
     }
-    if (side_lo) cudaStreamDestroy(side_lo);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
-    side = side_lo = nullptr;
+    side = nullptr;
     for (auto& e : ev) e = nullptr;
     slot_bytes = 0;
     counter_count = 0;
@@ -1955,12 +1921,10 @@ bool use_cluster_panel() {
 template <int NB>
 void panel_step_cluster(const LuProblem& pb, int k, int w, int P, int R, size_t smem, cudaStream_t st) {
     auto kern = lu_panel_cluster_kernel<NB>;
-    static size_t attr_smem = 0;
-    if (smem > attr_smem) {
-        FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+    once_per_device(reinterpret_cast<const void*>(kern), [&] {
         FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_smem = smem;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1994,12 +1958,7 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
     if (P > sms) throw NumericError("lu: panel does not fit in on-chip memory");
     const int R = ceil_div(rows, P);
     const size_t smem = panel_smem(NB, R);
-    static size_t attr_smem = 0;
-    if (smem > attr_smem) {
-        FDS_CUDA(cudaFuncSetAttribute(lu_panel_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        attr_smem = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(lu_panel_kernel<NB>), smem);
     if (NB == kSub && P <= 16 && use_cluster_panel()) {
         panel_step_cluster<NB>(pb, k, w, P, R, smem, st);
         return;
@@ -2041,12 +2000,7 @@ constexpr size_t kInvSmem = (4 * 64 * 65 + 2 * 48 * 17) * sizeof(double);
 
 // L11^{-1} and the swap map of the 64-wide panel at k (lu_l11_inverse_kernel)
 void l11_inverse_step(const LuProblem& pb, int k, cudaStream_t st, double* linv) {
-    static bool iset = false;
-    if (!iset) {
-        FDS_CUDA(cudaFuncSetAttribute(lu_l11_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kInvSmem)));
-        iset = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(lu_l11_inverse_kernel), kInvSmem);
     FDS_LAUNCH(lu_l11_inverse_kernel, pb.batch, kInvThreads, kInvSmem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
                pb.ipiv, linv);
 }
@@ -2056,23 +2010,13 @@ template <int NB>
 void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv, bool inverse_ready = false) {
     const int rest = pb.n - k - w;
     if (rest <= 0) return;
-    static bool attr_set = false;
     const size_t smem = (2 * NB * NB + 2 * kTrsmCols * NB) * sizeof(double);
-    if (!attr_set) {
-        FDS_CUDA(cudaFuncSetAttribute(lu_swap_trsm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        attr_set = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(lu_swap_trsm_kernel<NB>), smem);
     cudaEvent_t te;
     profiler().begin(st, kProfLuTrsm, 0.0, te);
     if (NB == 64 && w == 64) {
         const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
-        static bool aset = false;
-        if (!aset) {
-            FDS_CUDA(cudaFuncSetAttribute(lu_swap_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(asmem)));
-            aset = true;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(lu_swap_apply_kernel), asmem);
         if (!inverse_ready) l11_inverse_step(pb, k, st, linv);
         FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
                    pb.mstride, pb.plane, pb.n, pb.ld, k, linv, k + 64, pb.n, 0, 0);
@@ -2090,39 +2034,17 @@ struct TmaMaps {
     CUtensorMap a, b, b32;  // b32: 32-column U12 boxes of the 3M kernel's narrow tiles
 };
 
-// Trailing-update kernel: 1 = 3M with 64x32 tiles, 2 CTAs/SM (default); 0 = the
+// Trailing-update kernel: 3M with 64x32 tiles, 2 CTAs/SM (default), or the
 // four-product kernel (FDSWEEP_GEMM=4m: bit-identical results across batch
-// sizes / schedules); 2 = 3M 64x64 at 1 CTA/SM, 3 = 3M 64x64 with 16 warps
-// (FDSWEEP_GEMM=3m64 / 3m64w16, measured slower: 524 / 541 vs 480 ms on cfg2).
-int gemm_variant() {
-    static const int v = [] {
+// sizes / schedules). 64x64 3M tiles at 1 CTA/SM, with 16 warps, or at 2
+// CTAs/SM with spills, and a cp.async (non-TMA) operand feed were measured
+// slower on B200 and removed.
+bool gemm_3m() {
+    static const bool v = [] {
         const char* e = std::getenv("FDSWEEP_GEMM");
-        if (e && std::string(e) == "4m") return 0;
-        if (e && std::string(e) == "3m64") return 2;
-        if (e && std::string(e) == "3m64w16") return 3;
-        if (e && std::string(e) == "3m64x2") return 4;
-        return 1;
+        return !(e && std::string(e) == "4m");
     }();
     return v;
-}
-
-bool use_tma_gemm() {
-    static const bool on = [] {
-        const char* e = std::getenv("FDSWEEP_GEMM");
-        return !(e && std::string(e) == "cpasync");
-    }();
-    return on;
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        FDS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }();
-    return encode;
 }
 
 const TmaMaps& tma_maps(const LuProblem& pb) {
@@ -2159,7 +2081,7 @@ const TmaMaps& tma_maps(const LuProblem& pb) {
 // (boxes 20 x BN like tmB).
 struct G3Maps {
     double* base = nullptr;
-    CUtensorMap l, u32, u64;
+    CUtensorMap l, u32;
 };
 
 // set by lu_factor for the schedules whose updates run in stream order on one
@@ -2192,9 +2114,7 @@ const G3Maps& g3_maps(const LuProblem& pb, LuWorkspace& ws) {
     const cuuint64_t udims[3] = {kG3Rows, static_cast<cuuint64_t>(pb.ld), static_cast<cuuint64_t>(pb.batch)};
     const cuuint64_t ustr[2] = {kG3Rows * sizeof(double), static_cast<cuuint64_t>(pb.ld) * kG3Rows * sizeof(double)};
     const cuuint32_t ubox32[3] = {static_cast<cuuint32_t>(kTmaBBox0), 32, 1};
-    const cuuint32_t ubox64[3] = {static_cast<cuuint32_t>(kTmaBBox0), 64, 1};
     enc(&m.u32, ubase, udims, ustr, ubox32);
-    enc(&m.u64, ubase, udims, ustr, ubox64);
     return cache.emplace(key, m).first->second;
 }
 
@@ -2208,27 +2128,17 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
     if (c0 < 0) c0 = k + w;
     if (c1 < 0) c1 = pb.n;
     if (c1 <= c0) return;
-    static bool gset = false;
-    if (!gset) {
-        FDS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kGemmSmemDoubles * sizeof(double))));
-        gset = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_kernel), kGemmSmemDoubles * sizeof(double));
     dim3 gg(ceil_div(rest, GBM), ceil_div(c1 - c0, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
-    if ((w == 64 || w == 128) && use_tma_gemm()) {
-        static bool tset = false;
-        if (!tset) {
-            FDS_CUDA(cudaFuncSetAttribute(lu_gemm_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kGemmSmemDoubles * sizeof(double) + kTmaSmemPad)));
-            FDS_CUDA(cudaFuncSetAttribute(lu_gemm_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kGemmSmemDoubles * sizeof(double) + kTmaSmemPad)));
-            tset = true;
-        }
+    if (w == 64 || w == 128) {
+        ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_tma_kernel<64>),
+                            kGemmSmemDoubles * sizeof(double) + kTmaSmemPad);
+        ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_tma_kernel<128>),
+                            kGemmSmemDoubles * sizeof(double) + kTmaSmemPad);
         const TmaMaps& tm = tma_maps(pb);
-        const int gv = gemm_variant();
-        if (gv != 0 && t_g3_ws) {
+        if (gemm_3m() && t_g3_ws) {
             const G3Maps& gm = g3_maps(pb, *t_g3_ws);
             // operand planes: L21 once per (A, k, w) (the look-ahead window and the rest
             // share it; both run on this stream), U12 for this call's columns
@@ -2240,33 +2150,28 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                                    static_cast<long long>(c1 - c0) * w;
             FDS_LAUNCH(lu_g3_prep_kernel, dim3(static_cast<unsigned>(std::min<long long>(ceil_div(work, 256LL), 64)), pb.batch),
                        256, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? 1 : 0);
-            auto go = [&](auto kern, int bn, const CUtensorMap& mu, int nt = kGemmThreads) {
-                const size_t sm = (bn == 32 ? g3_smem_doubles<32>() : g3_smem_doubles<64>()) * sizeof(double) +
-                                  kTmaSmemPad + GSTAGES * sizeof(unsigned);
-                static bool set[8] = {};
-                const int slot = (bn == 32 ? 0 : (nt == kGemmThreads ? 2 : nt == 512 ? 4 : 6)) + (w == 128 ? 1 : 0);
-                if (nt == kGemmThreads + 1) nt = kGemmThreads;
-                if (!set[slot]) {
-                    FDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-                    set[slot] = true;
-                }
-                dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, bn), pb.batch);
-                FDS_LAUNCH(kern, g3, nt, sm, st, tm.a, bn == 32 ? tm.b32 : tm.b, gm.l, mu, pb.A, pb.mstride, pb.plane,
+            constexpr size_t sm = g3_smem_doubles<32>() * sizeof(double) + kTmaSmemPad + GSTAGES * sizeof(unsigned);
+            auto go = [&](auto kern) {
+                ensure_dynamic_smem(reinterpret_cast<const void*>(kern), sm);
+                dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, 32), pb.batch);
+                FDS_LAUNCH(kern, g3, kGemmThreads, sm, st, tm.a, tm.b32, gm.l, gm.u32, pb.A, pb.mstride, pb.plane,
                            pb.n, pb.ld, k, c0);
             };
-            if (gv == 1) {
-                if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>, 32, gm.u32);
-                else go(lu_gemm3m_tma_kernel<64, 32, 4, 2>, 32, gm.u32);
-            } else if (gv == 4) {
-                if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 2, 2>, 64, gm.u64, kGemmThreads + 1);
-                else go(lu_gemm3m_tma_kernel<64, 64, 2, 2>, 64, gm.u64, kGemmThreads + 1);
-            } else if (gv == 3) {
-                if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 4, 1, 512>, 64, gm.u64, 512);
-                else go(lu_gemm3m_tma_kernel<64, 64, 4, 1, 512>, 64, gm.u64, 512);
-            } else {
-                if (w == 128) go(lu_gemm3m_tma_kernel<128, 64, 2, 1>, 64, gm.u64);
-                else go(lu_gemm3m_tma_kernel<64, 64, 2, 1>, 64, gm.u64);
-            }
+            static const int v3 = [] {
+                const char* e = std::getenv("FDSWEEP_G3");
+                return e ? std::atoi(e) : 0;
+            }();
+            if (v3 == 1) {  // experiment: 4 warps of 32x16 per 64x32 tile
+                auto go4 = [&](auto kern) {
+                    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), sm);
+                    dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, 32), pb.batch);
+                    FDS_LAUNCH(kern, g3, 128, sm, st, tm.a, tm.b32, gm.l, gm.u32, pb.A, pb.mstride, pb.plane, pb.n,
+                               pb.ld, k, c0);
+                };
+                if (w == 128) go4(lu_gemm3m_tma_kernel<128, 32, 2, 2, 128>);
+                else go4(lu_gemm3m_tma_kernel<64, 32, 2, 2, 128>);
+            } else if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>);
+            else go(lu_gemm3m_tma_kernel<64, 32, 4, 2>);
         } else if (w == 128)
             FDS_LAUNCH(lu_gemm_tma_kernel<128>, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st,
                        tm.a, tm.b, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
@@ -2291,17 +2196,6 @@ void trailing_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* l
 
 namespace {
 
-// Panel algorithm: barrier-per-column partial pivoting (default; measured
-// faster on B200 for both the 129-matrix N=3840 batch and the single N=15360
-// matrix) or tournament pivoting (FDSWEEP_PANEL=calu, lu_calu.cu).
-bool use_calu() {
-    static const bool v = [] {
-        const char* e = std::getenv("FDSWEEP_PANEL");
-        return e && std::string(e) == "calu";
-    }();
-    return v;
-}
-
 // 16-wide sub-panels: for batches ~4x more matrices fit on chip at once
 // (cfg2 panel 225 -> 77 ms); for a single matrix the narrower rank-1 updates
 // still win (N=15360 panel 107 -> 97 ms). FDSWEEP_SUBPANEL=0/1 overrides.
@@ -2320,7 +2214,6 @@ bool use_subpanels(const LuProblem&) { return subpanels_enabled(); }
 int lu_panel_width(int n) {
     // NB = 64; the panel must fit one matrix's rows in the SMs' shared memory:
     // as 16-wide sub-panels (default) or as one 64-wide GEPP panel; otherwise 32.
-    if (use_calu()) return 64;
     const int sms = device_info().sms;
     if (ceil_div(n, panel_rows_max<64>()) <= sms) return 64;
     if (subpanels_enabled() && ceil_div(n, panel_rows_max<kSub>()) <= sms) return 64;
@@ -2360,58 +2253,6 @@ void subpanel_block(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStre
     }
     profiler().enabled = keep;
     profiler().end(st, pe, kProfLuPanel, 8.0 * (pb.n - k) * w * w / 2.0 * pb.batch);
-}
-
-bool use_pipeline(const LuProblem& pb) {
-    static const int env = [] {
-        const char* e = std::getenv("FDSWEEP_PIPELINE");
-        return e ? std::atoi(e) : -1;
-    }();
-    if (env >= 0) return env != 0 && pb.batch >= 2;
-    // Off by default: measured on B200 the co-scheduled panels slow the GEMM
-    // half (RF/smem sharing) more than they hide (cfg2 LU 745 -> 789 ms).
-    return false;
-}
-
-// Opt-in (FDSWEEP_PIPELINE=1). Batched factorization as two half-batches in flight: the panels and
-// swap+TRSM of one half run on a high-priority stream while the other half's
-// trailing GEMM occupies the tensor pipes on a low-priority stream, so the
-// latency-bound panel work hides behind the compute-bound GEMM.
-void lu_factor_pipelined(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
-    ws.ensure_side();
-    cudaStream_t s_hi = ws.side, s_lo = ws.side_lo;
-    cudaEvent_t* ev = ws.ev;
-    cudaEvent_t ev_start = ev[0], ev_hi_end = ev[1], ev_lo_end = ev[2];
-    cudaEvent_t ev_trsm[2] = {ev[3], ev[4]}, ev_gemm[2] = {ev[5], ev[6]};
-    const int b0 = pb.batch / 2;
-    LuProblem ph[2] = {pb, pb};
-    ph[0].batch = b0;
-    ph[1].batch = pb.batch - b0;
-    ph[1].A = pb.A + static_cast<size_t>(b0) * pb.mstride;
-    ph[1].ipiv = pb.ipiv + static_cast<size_t>(b0) * pb.n;
-    ph[1].info = pb.info + b0;
-    double* linv_all = ws.linv(pb.batch);
-    double* linv[2] = {linv_all, linv_all + static_cast<size_t>(b0) * kLinvStride};
-    FDS_CUDA(cudaEventRecord(ev_start, st));
-    FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_start, 0));
-    FDS_CUDA(cudaStreamWaitEvent(s_lo, ev_start, 0));
-    for (int k = 0; k < pb.n; k += 64) {
-        const int w = std::min(64, pb.n - k);
-        for (int h = 0; h < 2; ++h) {
-            if (k > 0) FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_gemm[h], 0));
-            if (w == 64) subpanel_block(ph[h], ws, k, w, s_hi, false);
-            else panel_step<64>(ph[h], ws, k, w, s_hi, false);
-            trsm_step<64>(ph[h], k, w, s_hi, linv[h]);
-            FDS_CUDA(cudaEventRecord(ev_trsm[h], s_hi));
-            FDS_CUDA(cudaStreamWaitEvent(s_lo, ev_trsm[h], 0));
-            gemm_step(ph[h], k, w, s_lo);
-            FDS_CUDA(cudaEventRecord(ev_gemm[h], s_lo));
-        }
-    }
-    FDS_CUDA(cudaEventRecord(ev_hi_end, s_hi));
-    FDS_CUDA(cudaEventRecord(ev_lo_end, s_lo));
-    FDS_CUDA(cudaStreamWaitEvent(st, ev_hi_end, 0));
-    FDS_CUDA(cudaStreamWaitEvent(st, ev_lo_end, 0));
 }
 
 int lookahead_mode() {
@@ -2531,13 +2372,24 @@ void super_panel_step(const LuProblem& pb, LuWorkspace& ws, int k, cudaStream_t 
 
 }  // namespace
 
+std::unique_lock<std::mutex> lu_device_gate() {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<std::mutex>> gates;
+    int dev = 0;
+    FDS_CUDA(cudaGetDevice(&dev));
+    std::mutex* g;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& p = gates[dev];
+        if (!p) p = std::make_unique<std::mutex>();
+        g = p.get();
+    }
+    return std::unique_lock<std::mutex>(*g);
+}
+
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     FDS_CUDA(cudaMemsetAsync(pb.info, 0, pb.batch * sizeof(int), st));
     ws.super_end = 0;
-    if (!use_calu() && lu_panel_width(pb.n) == 64 && use_pipeline(pb)) {
-        lu_factor_pipelined(pb, ws, st);
-        return;
-    }
     struct G3Scope {  // the 3M update's operand planes live in this workspace
         explicit G3Scope(LuWorkspace* w) {
             w->g3_key_A = nullptr;
@@ -2546,17 +2398,14 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
         }
         ~G3Scope() { t_g3_ws = nullptr; }
     } g3scope(&ws);
-    if (!use_calu() && lu_panel_width(pb.n) == 64 && subpanels_enabled() && pb.n >= 128 && use_lookahead(pb)) {
+    if (lu_panel_width(pb.n) == 64 && subpanels_enabled() && pb.n >= 128 && use_lookahead(pb)) {
         lu_factor_lookahead(pb, ws, st);
         return;
     }
     const int nb = lu_panel_width(pb.n);
     for (int k = 0; k < pb.n; k += nb) {
         const int w = std::min(nb, pb.n - k);
-        if (use_calu()) {
-            calu_panel_step(pb, ws.calu, k, w, st);
-            trailing_step<64>(pb, k, w, st, ws.linv(pb.batch));
-        } else if (nb == 64 && w == 64 && use_subpanels(pb) && super_panels() && k + 128 <= pb.n) {
+        if (nb == 64 && w == 64 && use_subpanels(pb) && super_panels() && k + 128 <= pb.n) {
             super_panel_step(pb, ws, k, st);
             ws.super_end = k + 128;
             k += 64;  // two panels
@@ -2625,12 +2474,8 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
     FDS_LAUNCH(lu_pivflag_kernel, dim3(groups, pb.batch), 128, 0, st, sg, pb.ipiv, pflag);
     const int ctas = nblk * pb.batch;
     auto go = [&](auto fwd, auto bwd) {
-        static bool attr = false;
-        if (!attr) {
-            FDS_CUDA(cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            FDS_CUDA(cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            attr = true;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(fwd), smem);
+        ensure_dynamic_smem(reinterpret_cast<const void*>(bwd), smem);
         FDS_LAUNCH(fwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ks, pb.ipiv, pflag, rhs,
                    rstride, ws.ybuf, ffl, tk);
         FDS_LAUNCH(bwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ws.ybuf, rhs, rstride, bfl,

@@ -1,6 +1,8 @@
 // Batched / blocked complex LU with partial pivoting on sm_100a.
 #pragma once
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace fdsb {
@@ -18,26 +20,10 @@ struct LuProblem {
     int* info = nullptr;  // [batch], 0 = ok, c+1 = first zero pivot
 };
 
-// Tournament-pivoting panel buffers (lu_calu.cu).
-struct CaluWorkspace {
-    int* cand_idx = nullptr;
-    int* cand_cnt = nullptr;
-    double* cand_val = nullptr;
-    unsigned* counters = nullptr;
-    size_t node_cap = 0;
-    double* top = nullptr;
-    double* disp = nullptr;
-    int* moves = nullptr;
-    int batch_cap = 0;
-    void ensure(int batch, int nodes);
-    void release();
-};
-
 struct LuWorkspace {
-    CaluWorkspace calu;
-    // side stream + events of the look-ahead / pipelined schedules (per
-    // workspace, so concurrent handles never share them)
-    cudaStream_t side = nullptr, side_lo = nullptr;
+    // side stream + events of the look-ahead schedule (per workspace, so
+    // concurrent handles never share them)
+    cudaStream_t side = nullptr;
     cudaEvent_t ev[8] = {};
     void ensure_side();
     double* linv_buf = nullptr;  // [batch][2][64][64] L11^{-1} per panel
@@ -75,12 +61,22 @@ struct LuWorkspace {
 inline int lu_ld(int n) { return (n + 63) / 64 * 64; }
 inline size_t lu_plane(int n) { return static_cast<size_t>(lu_ld(n)) * lu_ld(n); }
 
+// Process-wide, per-device gate held by every caller of lu_factor from the
+// enqueue until the factorization has completed on the device. The
+// single-matrix look-ahead schedule launches its software-barrier panel kernel
+// (lu_panel_kernel, CTAs spin on a global counter) next to its own trailing
+// GEMM on a second stream; that is safe because the GEMM's CTAs retire, but
+// panels of two handles running at once could fill the SMs with spinning CTAs.
+// Holding the gate serialises factorizations of different handles/threads in
+// one process. (Other processes on the same GPU — MPS — are not covered: run
+// one process per GPU, as the bench and the driver do.)
+std::unique_lock<std::mutex> lu_device_gate();
+
 // Per-step timings are not taken here; the caller brackets with events.
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st);
 // rhs[b*rstride + i], complex interleaved, overwritten with the solution
 // (dataflow substitution; FDSWEEP_SOLVE=blocked selects the per-panel launches).
 void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, cudaStream_t st);
 int lu_panel_width(int n);
-void calu_panel_step(const LuProblem& pb, CaluWorkspace& ws, int k, int w, cudaStream_t st);
 
 }  // namespace fdsb

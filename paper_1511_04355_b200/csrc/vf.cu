@@ -26,6 +26,9 @@
 #include <limits>
 
 #include "eig_host.h"
+
+#include <cstdlib>
+#include <type_traits>
 #include "vf.cuh"
 
 namespace fdsb {
@@ -571,6 +574,107 @@ __global__ void vf_gather_channels_kernel(int K, int M, int KT, const cplx* __re
     dst[idx] = src[static_cast<size_t>(m) * K + pos[q]];
 }
 
+// identify_residues apply, bulk-copy fed (default for J <= 64, M <= 64 per
+// slice): X (M x K) = W (M x 2J) B (2J x K). One persistent CTA per SM walks
+// 64-channel tiles; a producer warp streams each tile's J value rows (1 KB
+// contiguous runs of values[j][k0..k0+63]) into a ST-deep shared-memory ring
+// with cp.async.bulk (mbarrier transaction counts, no registers spent on the
+// copy); 2*MT consumer warps each own one 8-pole m-tile of W — its A fragments
+// for all steps live in registers for the whole kernel — and one 32-channel
+// half of the tile, reading B fragments from the ring (row stride 136 doubles:
+// the two value rows a fragment spans land 16 banks apart).
+constexpr int kRtTile = 64;        // channels per tile
+constexpr int kRtRow = 2 * kRtTile + 8;  // doubles per staged value row
+template <int MT, int SP, int ST>
+__global__ void __launch_bounds__(32 + 64 * MT, 1)
+vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
+                      cplx* __restrict__ res) {
+    extern __shared__ double rtm_raw[];
+    double* ring = rtm_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(ST) * J * kRtRow);
+    uint64_t* empty = full + ST;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m0 = blockIdx.y * 64;
+    const int ntiles = (K + kRtTile - 1) / kRtTile;
+    const int Q = 2 * J;
+    constexpr int kConsumers = 2 * MT;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {  // producer
+        int i = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int s = i % ST;
+            if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
+            const int k0 = t * kRtTile;
+            const unsigned bytes = static_cast<unsigned>(min(kRtTile, K - k0)) * 16u;
+            if (lane == 0) mbar_expect_tx(&full[s], bytes * J);
+            __syncwarp();
+            double* st = ring + static_cast<size_t>(s) * J * kRtRow;
+            for (int j = lane; j < J; j += 32)
+                bulk_load(st + j * kRtRow, vals + static_cast<size_t>(j) * K + k0, bytes, &full[s]);
+        }
+        return;
+    }
+    const int cw = warp - 1, mt = cw >> 1, half = cw & 1;
+    const int q_l = lane & 3, n_l = lane >> 2;
+    const int j0 = q_l >> 1, part = q_l & 1;
+    // A fragments of this warp's m-tile for every step: W[m][4 st + q_l] (zero padded)
+    double fa[SP];
+    const int mrow = m0 + mt * 8 + n_l;
+#pragma unroll
+    for (int st = 0; st < SP; ++st) {
+        const int q = 4 * st + q_l;
+        fa[st] = (mrow < M && q < Q) ? W[static_cast<size_t>(mrow) * Q + q] : 0.0;
+    }
+    const int steps = (J + 1) / 2;
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int s = i % ST;
+        mbar_wait(&full[s], (i / ST) & 1);
+        const double* st_base = ring + static_cast<size_t>(s) * J * kRtRow + (half * 32 + n_l) * 2 + part;
+        double acc[4][2];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+        for (int st = 0; st < SP; ++st) {
+            if (st < steps) {
+                // value row 2 st + j0 (the odd-J tail row meets zero A columns; clamp the read)
+                const int row = min(2 * st + j0, J - 1);
+                const double* b = st_base + row * kRtRow;
+                double fb[4];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) fb[nt] = b[nt * 16];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) dmma_v(acc[nt][0], acc[nt][1], fa[st], fb[nt]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
+        // the partner row sits 4 lanes away in the accumulator fragment
+        const int k0 = t * kRtTile + half * 32;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double x = acc[nt][e];
+                const double y = __shfl_xor_sync(0xffffffffu, x, 4);
+                const int k = k0 + nt * 8 + 2 * q_l + e;
+                if (mrow >= M || k >= K) continue;
+                cplx r;
+                if (mrow < 2 * P) r = (mrow % 2 == 0) ? mk(x, y) : mk(y, -x);
+                else r = mk(x, 0.0);
+                __stcs(reinterpret_cast<double2*>(res) + static_cast<size_t>(mrow) * K + k, make_double2(r.re, r.im));
+            }
+    }
+}
+
 // ------------------------------------------------------------------ host drivers
 namespace {
 
@@ -723,17 +827,47 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
     if (hst.rank < M) throw NumericError("identify_residues: rank-deficient least-squares system");
     const int P = pair_count(poles);
     const size_t smem = static_cast<size_t>(kResChunk) * 2 * J * sizeof(double);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        FDS_CUDA(cudaFuncSetAttribute(vf_residue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        attr = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(vf_residue_kernel), smem);
     const int PF = (((J + 1) / 2) % 5 == 0) ? 5 : 4;  // prefetch depth dividing the step count when possible
     const size_t msmem = static_cast<size_t>(4 * res_steps(J, PF)) * kRmS * sizeof(double);
     cudaEvent_t pe;
     profiler().begin(st, kProfVfResidue, 0.0, pe);
-    if (msmem <= device_info().smem_optin - 1024) {
+    const int mt_all = std::min(8, ceil_div(M, 8));
+    const size_t row_bytes = static_cast<size_t>(J) * kRtRow * sizeof(double);
+    const int rt_st = std::min<int>(4, static_cast<int>((device_info().smem_optin - 1024) / std::max<size_t>(row_bytes, 1)));
+    if (J <= 64 && rt_st >= 2 && !std::getenv("FDSWEEP_RESIDUE_LEGACY")) {
+        const size_t tsmem = rt_st * row_bytes + 2 * 4 * sizeof(uint64_t);
+        const int ctas = std::min(ceil_div(K, kRtTile), device_info().sms);
+        auto go = [&](auto kern) {
+            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), tsmem);
+            FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 32 + 64 * mt_all, tsmem, st, J, K, M, P, values_dev, dW,
+                       res_dev);
+        };
+        auto by_sp = [&](auto mtc) {
+            constexpr int MTc = decltype(mtc)::value;
+            const int sp = (J + 1) / 2;
+            auto by_st = [&](auto spc) {
+                constexpr int SPc = decltype(spc)::value;
+                if (rt_st >= 4) go(vf_residue_tma_kernel<MTc, SPc, 4>);
+                else if (rt_st == 3) go(vf_residue_tma_kernel<MTc, SPc, 3>);
+                else go(vf_residue_tma_kernel<MTc, SPc, 2>);
+            };
+            if (sp <= 8) by_st(std::integral_constant<int, 8>{});
+            else if (sp <= 16) by_st(std::integral_constant<int, 16>{});
+            else if (sp <= 24) by_st(std::integral_constant<int, 24>{});
+            else by_st(std::integral_constant<int, 32>{});
+        };
+        switch (mt_all) {
+            case 1: by_sp(std::integral_constant<int, 1>{}); break;
+            case 2: by_sp(std::integral_constant<int, 2>{}); break;
+            case 3: by_sp(std::integral_constant<int, 3>{}); break;
+            case 4: by_sp(std::integral_constant<int, 4>{}); break;
+            case 5: by_sp(std::integral_constant<int, 5>{}); break;
+            case 6: by_sp(std::integral_constant<int, 6>{}); break;
+            case 7: by_sp(std::integral_constant<int, 7>{}); break;
+            default: by_sp(std::integral_constant<int, 8>{}); break;
+        }
+    } else if (msmem <= device_info().smem_optin - 1024) {
         const int ctas = std::min(ceil_div(K, 4 * 8 * kResNI), 8 * device_info().sms);
         const int mt = std::min(8, ceil_div(M, 8));  // m-tiles of the first (largest) slice
         auto go = [&](auto kern) {

@@ -46,11 +46,12 @@ __device__ void lsq_solve_warp(const double* a, int m, int n, int np, const doub
         for (int i = 1 + lane; i < m - k; i += 32) b[k + i] -= d * ess[i];
         __syncwarp();
     }
-    for (int i = np - 1; i >= 0; --i) {  // R11 z = (Q^T b)[0:np]
-        double s = 0.0;
-        for (int j = i + 1 + lane; j < np; j += 32) s += a[static_cast<size_t>(j) * m + i] * b[j];
-        s = warp_sum(s);
-        if (lane == 0) b[i] = (b[i] - s) / a[static_cast<size_t>(i) * m + i];
+    for (int i = np - 1; i >= 0; --i) {  // R11 z = (Q^T b)[0:np], column-oriented (no reductions)
+        const double* col = a + static_cast<size_t>(i) * m;
+        const double zi = b[i] / col[i];
+        __syncwarp();
+        if (lane == 0) b[i] = zi;
+        for (int j = lane; j < i; j += 32) b[j] -= zi * col[j];
         __syncwarp();
     }
     for (int i = lane; i < n; i += 32) x[i] = 0.0;
@@ -70,7 +71,7 @@ vf_lsq_kernel(int m, int n, const double* __restrict__ in, long long rs, long lo
               double* gwork, double* __restrict__ x_out, double* __restrict__ w_out,
               const double* __restrict__ wscale, VfLsqStatus* __restrict__ status) {
     extern __shared__ double lsm[];
-    __shared__ int s_big, s_nonzero, s_rank;
+    __shared__ int s_nonzero, s_rank;
     __shared__ double s_maxpivot, s_thr;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int size = min(m, n);
@@ -106,29 +107,34 @@ vf_lsq_kernel(int m, int n, const double* __restrict__ in, long long rs, long lo
     }
     for (int k = 0; k < size; ++k) {
         __syncthreads();
-        if (tid == 0) {  // pivot: largest remaining norm, first maximum
-            int big = k;
-            for (int j = k + 1; j < n; ++j)
-                if (upd[j] > upd[big]) big = j;
-            if (s_nonzero == size && upd[big] * upd[big] < s_thr * (m - k)) s_nonzero = k;
-            s_big = big;
-        }
-        __syncthreads();
-        const int big = s_big;
-        if (big != k) {
-            for (int i = tid; i < m; i += kLsqThreads) {
-                const double t = a[static_cast<size_t>(k) * m + i];
-                a[static_cast<size_t>(k) * m + i] = a[static_cast<size_t>(big) * m + i];
-                a[static_cast<size_t>(big) * m + i] = t;
+        if (warp == 0) {
+            // pivot: largest remaining norm, first maximum (warp argmax)
+            double bv = -1.0;
+            int bj = n;
+            for (int j = k + lane; j < n; j += 32)
+                if (upd[j] > bv) { bv = upd[j]; bj = j; }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                if (ov > bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
             }
-            if (tid == 0) {
-                double t = upd[k]; upd[k] = upd[big]; upd[big] = t;
-                t = dir[k]; dir[k] = dir[big]; dir[big] = t;
-                const int p = perm[k]; perm[k] = perm[big]; perm[big] = p;
+            const int big = bj;
+            if (lane == 0 && s_nonzero == size && upd[big] * upd[big] < s_thr * (m - k)) s_nonzero = k;
+            if (big != k) {
+                for (int i = lane; i < m; i += 32) {
+                    const double t = a[static_cast<size_t>(k) * m + i];
+                    a[static_cast<size_t>(k) * m + i] = a[static_cast<size_t>(big) * m + i];
+                    a[static_cast<size_t>(big) * m + i] = t;
+                }
+                if (lane == 0) {
+                    double t = upd[k]; upd[k] = upd[big]; upd[big] = t;
+                    t = dir[k]; dir[k] = dir[big]; dir[big] = t;
+                    const int p = perm[k]; perm[k] = perm[big]; perm[big] = p;
+                }
+                __syncwarp();
             }
-            __syncthreads();
-        }
-        if (warp == 0) {  // Householder vector of column k, rows k..m-1
+            // Householder vector of column k, rows k..m-1
             double* x = a + static_cast<size_t>(k) * m + k;
             const int len = m - k;
             double tail = 0.0;

@@ -326,3 +326,27 @@ def test_identify_residues_kernel_tiers_in_one_process():
             ro, rmso = O.identify_residues(s, v[:, k], pl)
             assert rel_l2(res[k], ro) < 1e-10
             assert rms[k] == pytest.approx(rmso, rel=1e-8)
+
+
+@pytest.mark.parametrize("J,pairs,reals,K", [(7, 2, 0, 100), (40, 24, 0, 1000), (41, 23, 1, 333), (64, 32, 0, 129),
+                                             (40, 35, 0, 200), (80, 48, 0, 65), (33, 3, 2, 64)])
+def test_identify_residues_shapes(J, pairs, reals, K):
+    """The bulk-copy-fed residue kernel (J <= 64) and the legacy register-ring
+    kernel (J > 64) over odd J, unpaired real poles, M > 64 (two 64-pole
+    slices) and channel counts that leave a ragged last 64-channel tile:
+    every sampled channel against the oracle's per-channel identify_residues
+    (vecfit.cpp:356-408)."""
+    rng = np.random.default_rng(J * 1000 + K)
+    p = []
+    for m in range(pairs):
+        a = complex(-0.05 - 0.02 * m, 0.4 + 1.1 * m)
+        p += [a, a.conjugate()]
+    p += [complex(-0.3 - 0.2 * r, 0.0) for r in range(reals)]
+    p = np.array(p)
+    s = 0.3 + 1j * np.linspace(0.1, 1.1 * abs(p.imag).max() + 1.0, J)
+    v = rng.normal(size=(J, K)) + 1j * rng.normal(size=(J, K))
+    res, rms = P.identify_residues(s, v, p)
+    for k in sorted({0, 1, K // 2, K - 2, K - 1}):
+        ro, rmso = O.identify_residues(s, v[:, k], p)
+        assert rel_l2(res[k], ro) < 1e-10, (k, rel_l2(res[k], ro))
+        assert rms[k] == pytest.approx(rmso, rel=1e-8)
