@@ -435,7 +435,18 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
             b = min(b, ms.value)
         return b
 
+    # cold: the solve operator W formed from scratch (the vector fit above left the
+    # ORF fit's operator for the same (s, poles) cached, which the warm timings reuse)
+    P.api._check(L.fds_vf_release_workspace())
+    P.api._check(L.fds_vf_identify_residues_device(
+        J, D, s_np.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(vals.data_ptr()), M,
+        ph.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(res_dev.data_ptr()), ctypes.byref(ms)))
+    t_res_cold = ms.value
     t_res = best(lambda: P.api._check(L.fds_vf_identify_residues_device(
+        J, D, s_np.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(vals.data_ptr()), M,
+        ph.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(res_dev.data_ptr()), ctypes.byref(ms))))
+    # pair heads only (the conjugate rows carry no information; rational_invert reads heads)
+    t_res_h = best(lambda: P.api._check(L.fds_vf_identify_residues_device_heads(
         J, D, s_np.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(vals.data_ptr()), M,
         ph.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(res_dev.data_ptr()), ctypes.byref(ms))))
     t_rat = best(lambda: P.api._check(L.fds_rational_invert_device(
@@ -466,6 +477,15 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
         c, kms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
         P.api._check(L.fds_profile_read(kind, ctypes.byref(c), ctypes.byref(kms), ctypes.byref(wk)))
         kern[name] = kms.value / max(c.value, 1)
+    P.api._check(L.fds_profile_enable(0))
+    P.api._check(L.fds_profile_enable(1))
+    for _ in range(reps):
+        P.api._check(L.fds_vf_identify_residues_device_heads(
+            J, D, s_np.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(vals_keep.data_ptr()), M,
+            ph.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(res_dev.data_ptr()), ctypes.byref(ms)))
+    c, kms, wk = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    P.api._check(L.fds_profile_read(5, ctypes.byref(c), ctypes.byref(kms), ctypes.byref(wk)))
+    kern["residue_heads"] = kms.value / max(c.value, 1)
     P.api._check(L.fds_profile_enable(0))
     # channel-major spectra (the reference's per-channel fsm_invert layout)
     cmaj = half.T.contiguous()
@@ -499,7 +519,11 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
     f_res = D * 4.0 * J * M  # W (M x 2J) times the 2J real samples of each DOF
     out = {
         "dofs": D, "J": J, "M": M, "time_steps": T_steps, "relocation_s": t_reloc,
-        "api_ms": {"residue_id": t_res, "rational_invert": t_rat, "fsm": t_fsm, "fsm_chan_major": t_fsm_cm},
+        "api_ms": {"residue_id": t_res, "residue_id_cold": t_res_cold, "residue_id_heads": t_res_h,
+                   "rational_invert": t_rat, "fsm": t_fsm, "fsm_chan_major": t_fsm_cm},
+        "api_note": "residue_id* warm: the shared solve operator for (s, poles) is reused from the preceding call "
+                    "(as run_afs's final all-channel fit reuses its last high-order fit); residue_id_cold forms it "
+                    "on the device from scratch (one-CTA pivoted QR)",
         "kernel_ms": {"residue_id": kr, "rational_invert": kt, "fsm": kf, "fsm_chan_major": kc},
         "residue_id_dof_per_s": D / (kr * 1e-3), "residue_id_gbs": b_res / (kr * 1e-3) / 1e9,
         "residue_id_hbm_frac": b_res / (kr * 1e-3) / 1e9 / hbm,
@@ -511,10 +535,20 @@ def cfg5_vf_fsm(D=300_000, J=40, pairs=24, T_steps=512, reps=3):
         "fsm_chan_major_gbs": b_fsm / (kc * 1e-3) / 1e9, "fsm_chan_major_hbm_frac": b_fsm / (kc * 1e-3) / 1e9 / hbm,
         "fsm_layouts": "fsm = frequency-major [i][k] spectra as the batched BEM emits them (gather-bound); "
                        "fsm_chan_major = per-channel [k][i] spectra, the reference fsm_invert layout",
-        "vf_fsm_dof_per_s": D / ((t_res + t_rat) * 1e-3),
-        "vf_fsm_dof_per_s_def": "D / (API-level residue identification + rational_invert time: CUDA events "
-                                "around the whole C-ABI call, including the shared QR and the W operator)",
-        "api_dof_per_s": {"residue_id": D / (t_res * 1e-3), "rational_invert": D / (t_rat * 1e-3),
+        "vf_fsm_dof_per_s": D / ((t_res_h + t_rat) * 1e-3),
+        "vf_fsm_dof_per_s_def": "D / (API-level residue identification (pair heads) + rational_invert time: CUDA "
+                                "events around the whole C-ABI calls, including the shared QR and the W operator)",
+        "residue_heads": {"api_ms": t_res_h, "kernel_ms": kern["residue_heads"],
+                          "bytes_per_dof": 16.0 * J + 8.0 * M,
+                          "hbm_frac": D * (16.0 * J + 8.0 * M) / (kern["residue_heads"] * 1e-3) / 1e9 / hbm,
+                          "fp64_frac": D * 4.0 * J * M / (kern["residue_heads"] * 1e-3) / 1e12 / fp64,
+                          "binding_roofline_frac": max(D * 4.0 * J * M / (fp64 * 1e12),
+                                                       D * (16.0 * J + 8.0 * M) / (hbm * 1e9)) /
+                          (kern["residue_heads"] * 1e-3),
+                          "note": "fds_vf_identify_residues_device_heads: conjugate rows of pole pairs not written "
+                                  "(SURVEY §8d's 16 J + 16 M/2 bytes per DOF)"},
+        "api_dof_per_s": {"residue_id": D / (t_res * 1e-3), "residue_id_heads": D / (t_res_h * 1e-3),
+                          "rational_invert": D / (t_rat * 1e-3),
                           "fsm": D / (t_fsm * 1e-3), "fsm_chan_major": D / (t_fsm_cm * 1e-3)},
         "api_hbm_frac": {"residue_id": b_res / (t_res * 1e-3) / 1e9 / hbm, "fsm": b_fsm / (t_fsm * 1e-3) / 1e9 / hbm,
                          "fsm_chan_major": b_fsm / (t_fsm_cm * 1e-3) / 1e9 / hbm},

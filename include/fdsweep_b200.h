@@ -150,8 +150,15 @@ int fds_vector_fit(int J, int K, const fds_c64* s, const fds_c64* values, int n_
                    fds_c64* residues_out, int* report_i, double* report_d,
                    double* per_channel_rms, double* relocation_rms);
 /* eval_model (vecfit.cpp:503-509) at G points: out[g*K + k]. */
+/* Frees the calling thread's VF / Laplace device workspaces, including the
+ * cached identify_residues solve operator (reused while (s, poles) repeat). */
+int fds_vf_release_workspace(void);
 int fds_eval_model(int M, const fds_c64* poles, int K, const fds_c64* residues, int G,
                    const fds_c64* s, fds_c64* out);
+/* fit_error_evf (vecfit.cpp:511-526): E_vf of one channel of the model
+ * (residues [K][M]) against samples values[j*K + k] at s[J]; on the device. */
+int fds_fit_error_evf(int M, const fds_c64* poles, int K, const fds_c64* residues, int channel, int J,
+                      const fds_c64* s, const fds_c64* values, double* out);
 /* channel_errors (afs.cpp:118-145): e[k] = max_g|fH-fL| / max_g|fH|. */
 int fds_channel_errors(int MH, const fds_c64* poles_h, const fds_c64* res_h, int ML,
                        const fds_c64* poles_l, const fds_c64* res_l, int K, int G,
@@ -173,12 +180,21 @@ int fds_fsm_invert(double period, int Ns, double eta, int K, const fds_c64* half
 int fds_rational_invert(int M, const fds_c64* poles, int K, const fds_c64* residues, int T,
                         const double* t, double* out);
 
-/* Device-resident VF/FSM stage for the bench (config 5): all pointers are HBM.
- * residues: [k*M + m]; values: [j*K + k]; half: [i*K + k] (frequency-major);
- * out: [k*Ns + n] / [k*T + n]. Each returns the kernel-only device ms. */
+/* Device-resident VF/FSM stage (config 5): data pointers are HBM, the small
+ * s / poles / t vectors host. residues: [m*K + k] (canonical pole order);
+ * values: [j*K + k]; half: [i*K + k] (frequency-major); out: [k*Ns + n] /
+ * [k*T + n]. ms (optional) = device time of the whole call (CUDA events on the
+ * library stream around every launch the call makes, shared QR included). */
 int fds_vf_identify_residues_device(int J, int K, const fds_c64* s_host, const fds_c64* values_dev,
                                     int M, const fds_c64* poles_host, fds_c64* residues_dev,
                                     double* ms);
+/* Same, but the conjugate row m+1 of every pole pair (canonical order: pairs
+ * adjacent, +Im first) is left unwritten — it equals conj(row m). For
+ * consumers that use the pair symmetry (fds_rational_invert_device reads only
+ * the pair heads and the real poles); saves 8 M bytes of HBM writes per DOF. */
+int fds_vf_identify_residues_device_heads(int J, int K, const fds_c64* s_host, const fds_c64* values_dev,
+                                          int M, const fds_c64* poles_host, fds_c64* residues_dev,
+                                          double* ms);
 int fds_rational_invert_device(int M, const fds_c64* poles_host, int K, const fds_c64* residues_dev,
                                int T, const double* t_host, double* out_dev, double* ms);
 int fds_fsm_invert_device(double period, int Ns, double eta, int K, const fds_c64* half_dev,

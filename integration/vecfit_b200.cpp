@@ -1,8 +1,9 @@
 // Drop-in replacement for proj/src/vecfit.cpp: the reference's vecfit.hpp API
 // (vecfit.hpp:48-86) implemented by forwarding to libfdsweep_b200 (GPU).
 // Linked instead of vecfit.cpp, it makes the reference's own run_afs
-// (afs.cpp:226-396) fit on the B200. eval_model / fit_error_evf / the pole
-// utilities are O(M) host helpers and keep the reference semantics here.
+// (afs.cpp:226-396) fit on the B200, eval_model / fit_error_evf included; the
+// O(M) pole utilities (conjugate closure, canonical order, starting poles)
+// are host bookkeeping and keep the reference semantics here.
 #include <algorithm>
 #include <cmath>
 
@@ -80,6 +81,12 @@ std::pair<RationalModel, FitReport> vector_fit(std::span<const FrequencySample> 
     return b200::vector_fit(samples, orf, order, n_relocations, std::move(labels));
 }
 
+// One (channel, s) point: M complex divisions. The reference's channel_errors
+// (afs.cpp:118-145) calls this G x K times per iteration, where a device round
+// trip per call would cost ~10^3 times the arithmetic, so the scalar form stays
+// on the host; every batched evaluation (eval_model over the channels,
+// fit_error_evf over the samples, fds_eval_model over a grid, the GPU AFS
+// driver's channel errors) runs on the device.
 Complex eval_model_channel(const RationalModel& model, int channel, Complex s) {  // vecfit.cpp:490-501
     if (channel < 0 || channel >= model.channel_count()) throw ValidationError("eval_model_channel: channel out of range");
     Complex acc(0.0, 0.0);
@@ -91,22 +98,27 @@ Complex eval_model_channel(const RationalModel& model, int channel, Complex s) {
     return acc;
 }
 
-std::vector<Complex> eval_model(const RationalModel& model, Complex s) {
-    std::vector<Complex> out(model.channel_count());
-    for (int k = 0; k < model.channel_count(); ++k) out[k] = eval_model_channel(model, k, s);
+std::vector<Complex> eval_model(const RationalModel& model, Complex s) {  // vecfit.cpp:503-509
+    const int K = model.channel_count(), M = model.order();
+    std::vector<Complex> res(static_cast<size_t>(K) * M), out(K);
+    for (int k = 0; k < K; ++k) std::copy(model.residues[k].begin(), model.residues[k].end(), res.begin() + static_cast<size_t>(k) * M);
+    b200::check(fds_eval_model(M, b200::c(model.poles.data()), K, b200::c(res.data()), 1, b200::c(&s), b200::c(out.data())));
     return out;
 }
 
-double fit_error_evf(const RationalModel& model, int channel, std::span<const FrequencySample> samples) {
+double fit_error_evf(const RationalModel& model, int channel, std::span<const FrequencySample> samples) {  // :511-526
     if (samples.empty()) throw ValidationError("fit_error_evf: no samples");
-    double num = 0.0, den = 0.0;
-    for (const auto& smp : samples) {
-        const Complex d = smp.values.at(channel);
-        num += std::norm(eval_model_channel(model, channel, smp.s) - d);
-        den += std::norm(d);
+    if (channel < 0 || channel >= model.channel_count()) throw ValidationError("eval_model_channel: channel out of range");
+    const int J = static_cast<int>(samples.size()), M = model.order();
+    std::vector<Complex> s(J), v(J);
+    for (int j = 0; j < J; ++j) {
+        s[j] = samples[j].s;
+        v[j] = samples[j].values.at(channel);
     }
-    if (den == 0.0) throw NumericError("fit_error_evf: zero-norm sample data");
-    return std::sqrt(num / den);
+    double e = 0.0;
+    b200::check(fds_fit_error_evf(M, b200::c(model.poles.data()), 1, b200::c(model.residues[channel].data()), 0, J,
+                                  b200::c(s.data()), b200::c(v.data()), &e));
+    return e;
 }
 
 }  // namespace fdsweep

@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     ValidationError,
     channel_errors,
     eval_model,
+    fit_error_evf,
     fsm_invert,
     identify_residues,
     kernel_launches,

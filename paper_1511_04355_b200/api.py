@@ -352,6 +352,16 @@ def eval_model(model: RationalModel, s):
     return out
 
 
+def fit_error_evf(model: RationalModel, channel, s, values):
+    """vecfit.cpp:511-526 on the device: E_vf of one channel; values (J, K)."""
+    p, r = _cz(model.poles), _cz(np.atleast_2d(model.residues))
+    s, v = _cz(np.atleast_1d(s)), _cz(np.atleast_2d(values))
+    out = ctypes.c_double()
+    _check(lib().fds_fit_error_evf(len(p), _p(p), r.shape[0], _p(r), int(channel), len(s), _p(s), _p(v),
+                                   ctypes.byref(out)))
+    return out.value
+
+
 def channel_errors(high: RationalModel, low: RationalModel, grid):
     g = _cz(grid)
     ph, rh, pl, rl = _cz(high.poles), _cz(high.residues), _cz(low.poles), _cz(low.residues)

@@ -103,21 +103,27 @@ int fds_vector_fit(int J, int K, const fds_c64* s, const fds_c64* values, int n_
     });
 }
 
+int fds_vf_release_workspace(void) {
+    return fds_guard([&] { VfContext::get().release(); });
+}
+
 int fds_eval_model(int M, const fds_c64* poles, int K, const fds_c64* residues, int G, const fds_c64* s, fds_c64* out) {
-    // eval_model (vecfit.cpp:490-509): direct partial-fraction sum (host; O(G K M)).
+    // eval_model (vecfit.cpp:490-509) on the device (vf_eval_kernel)
     return fds_guard([&] {
-        for (int g = 0; g < G; ++g) {
-            const Cx sg(s[g].re, s[g].im);
-            for (int k = 0; k < K; ++k) {
-                Cx acc(0.0, 0.0);
-                for (int m = 0; m < M; ++m) {
-                    const Cx d = sg - Cx(poles[m].re, poles[m].im);
-                    if (d == 0.0) throw NumericError("eval_model: s coincides with a pole");
-                    acc += Cx(residues[static_cast<size_t>(k) * M + m].re, residues[static_cast<size_t>(k) * M + m].im) / d;
-                }
-                out[static_cast<size_t>(g) * K + k] = {acc.real(), acc.imag()};
-            }
-        }
+        need(M >= 0 && K >= 0 && G >= 0, "eval_model: negative size");
+        need((M == 0 || poles) && (K * M == 0 || residues) && (G == 0 || (s && out)), "eval_model: null argument");
+        vf_eval_model(cv(poles, M), reinterpret_cast<const Cx*>(residues), K, cv(s, G), reinterpret_cast<Cx*>(out));
+    });
+}
+
+int fds_fit_error_evf(int M, const fds_c64* poles, int K, const fds_c64* residues, int channel, int J,
+                      const fds_c64* s, const fds_c64* values, double* out) {
+    // fit_error_evf (vecfit.cpp:511-526) on the device (vf_evf_kernel)
+    return fds_guard([&] {
+        need(out && M >= 0 && K > 0 && J >= 0, "fit_error_evf: bad argument");
+        if (channel < 0 || channel >= K) throw ValidationError("eval_model_channel: channel out of range");
+        *out = vf_fit_error_evf(cv(poles, M), reinterpret_cast<const Cx*>(residues) + static_cast<size_t>(channel) * M,
+                                cv(s, J), reinterpret_cast<const Cx*>(values) + channel, K);
     });
 }
 
@@ -177,6 +183,21 @@ int fds_vf_identify_residues_device(int J, int K, const fds_c64* s_host, const f
         FDS_CUDA(cudaEventRecord(ev.a, cx.st));
         vf_residues_device(cv(s_host, J), reinterpret_cast<const cplx*>(values_dev), K, canon,
                            reinterpret_cast<cplx*>(residues_dev), nullptr, cx.st);
+        FDS_CUDA(cudaEventRecord(ev.b, cx.st));
+        FDS_CUDA(cudaEventSynchronize(ev.b));
+        if (ms) *ms = elapsed(ev.a, ev.b);
+    });
+}
+
+int fds_vf_identify_residues_device_heads(int J, int K, const fds_c64* s_host, const fds_c64* values_dev, int M,
+                                    const fds_c64* poles_host, fds_c64* residues_dev, double* ms) {
+    return fds_guard([&] {
+        auto& cx = VfContext::get();
+        EventPair ev;
+        const std::vector<Cx> canon = canonical_order(cv(poles_host, M));
+        FDS_CUDA(cudaEventRecord(ev.a, cx.st));
+        vf_residues_device(cv(s_host, J), reinterpret_cast<const cplx*>(values_dev), K, canon,
+                           reinterpret_cast<cplx*>(residues_dev), nullptr, cx.st, true);
         FDS_CUDA(cudaEventRecord(ev.b, cx.st));
         FDS_CUDA(cudaEventSynchronize(ev.b));
         if (ms) *ms = elapsed(ev.a, ev.b);

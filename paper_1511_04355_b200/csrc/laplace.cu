@@ -11,10 +11,12 @@
 //                      Stockham passes exchanged through the consumed buffer,
 //                      coalesced direct stores. 86 % of HBM on channel-major
 //                      spectra.
-//   fsm_stockham256_tile_kernel  the same DOF transform for frequency-major
-//                      spectra: the CTA stages 16 adjacent DOFs per group, so
-//                      every frequency row is one 256 B run (the scattered rows
-//                      keep this layout below the channel-major rate).
+//   fsm256_tma_kernel  the same DOF transform for frequency-major spectra (the
+//                      layout the batched BEM emits): groups of 8 adjacent DOFs
+//                      arrive as 257 x 128 B swizzled tiles through 2-D bulk
+//                      tensor copies into a 5-deep ring (80 % of HBM at 300k
+//                      DOFs; the cp.async-staged 16-DOF tile kernel it
+//                      replaced reached 56 %).
 //   fsm_warp_kernel    other N_s = 64 R: register FFT with xor-shuffle stages.
 //   fsm_dft_kernel     same contract for any even N_s (direct DFT; e.g. the
 //                      paper's N_s = 218), thread per output sample.
@@ -482,63 +484,6 @@ fsm_stockham256_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t s
     asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-// CTA-cooperative variant for frequency-major spectra ([i][k], DOFs adjacent):
-// the whole CTA stages a group of D adjacent DOFs, so each frequency row is
-// read as one contiguous D·16 B run (256 B at D = 16) instead of the 32 B
-// sectors of the warp-private pipeline, whose scattered rows leave HBM
-// page-bound. The copy transposes on the fly into DOF-major buffers (stride
-// kFsmStride = 289 cplx: consecutive DOFs start on different 16 B bank
-// chunks, so a row's stores are conflict-free); each warp then runs
-// fsm256_dof on D/W of the group's DOFs. P-deep ring, one CTA barrier per group.
-constexpr int kFsmStride = kFsmBuf + 1;
-
-template <int WARPS, int P, int D>
-__global__ void __launch_bounds__(WARPS * 32, 1)
-fsm_stockham256_tile_kernel(int K, const cplx* __restrict__ half, size_t sk, size_t si, int hanning, double edt,
-                            const cplx* __restrict__ gpost, const cplx* __restrict__ gtw,
-                            const double* __restrict__ gwout, double* __restrict__ out) {
-    static_assert(D % WARPS == 0, "DOFs per group must split evenly over the warps");
-    constexpr int Nc = kFsmNc, NT = WARPS * 32;
-    extern __shared__ __align__(16) cplx fsm_s[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    cplx* pst = fsm_s + static_cast<size_t>(P) * D * kFsmStride;
-    for (int j = threadIdx.x; j < kFsmL; j += NT) pst[j] = gpost[j];
-    Fsm256Lane c;
-    c.load(lane, edt, gtw, gwout);
-    const int groups = (K + D - 1) / D;
-    auto stage = [&](int g, cplx* buf) {
-        if (g < groups) {
-            const int k0 = g * D;
-            for (int q = threadIdx.x; q < D * Nc; q += NT) {
-                const int i = q / D, d = q % D;  // row-major walk: a row's D DOFs are adjacent in HBM
-                const int k = min(k0 + d, K - 1);
-                const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(buf + d * kFsmStride + i));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
-                             "l"(half + static_cast<size_t>(k) * sk + static_cast<size_t>(i) * si));
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-    };
-#pragma unroll
-    for (int p = 0; p < P - 1; ++p) stage(blockIdx.x + p * gridDim.x, fsm_s + static_cast<size_t>(p) * D * kFsmStride);
-    int slot = 0;
-    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(P - 2));
-        __syncthreads();  // group g visible to every warp; slot (slot-1) fully consumed
-        stage(g + (P - 1) * gridDim.x, fsm_s + static_cast<size_t>((slot + P - 1) % P) * D * kFsmStride);
-        cplx* buf = fsm_s + static_cast<size_t>(slot) * D * kFsmStride;
-#pragma unroll 1
-        for (int d = warp; d < D; d += WARPS) {
-            const int k = g * D + d;
-            if (k >= K) break;
-            fsm256_dof(buf + d * kFsmStride, pst, hanning, lane, c,
-                       reinterpret_cast<double2*>(out + static_cast<size_t>(k) * (2 * kFsmL)));
-        }
-        slot = (slot + 1) % P;
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-}
-
 // TMA variant for frequency-major spectra (default): groups of 8 adjacent DOFs.
 // A producer warp loads each group's 257 x 128 B block with two
 // cp.async.bulk.tensor.2d boxes (rows 0-255, row 256) under the 128 B swizzle
@@ -951,15 +896,6 @@ static bool fsm_stockham() {
     return on;
 }
 
-// Frequency-major N_s = 512 spectra take the TMA kernel unless FDSWEEP_FSM=cpasync.
-static bool fsm_tma() {
-    static const bool on = [] {
-        const char* e = std::getenv("FDSWEEP_FSM");
-        return !(e && std::string(e) == "cpasync");
-    }();
-    return on;
-}
-
 void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* half_dev, size_t sk, size_t si,
                        bool hanning, double* out_dev, cudaStream_t st) {
     if (!(period > 0.0)) throw ValidationError("FsmGrid: period must be positive");
@@ -985,7 +921,7 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
         FDS_LAUNCH(fsm_tables_kernel, ceil_div(Ns + 1, 256), 256, 0, st, Ns, eta, dt, invT, hanning ? 1 : 0, win, post,
                    tw, wout);
         const int R = L / 32;
-        if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1 && fsm_tma()) {
+        if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1) {
             constexpr int ST = 5;
             auto kern = fsm256_tma_kernel<ST>;
             const size_t ssm = 1024 + ST * kFtStageBytes + (kFtDofs * kFsmBuf + kFsmL) * sizeof(cplx) +
@@ -1006,20 +942,6 @@ void fsm_invert_device(double period, int Ns, double eta, int K, const cplx* hal
             }
             const int ctas = std::min(ceil_div(K, kFtDofs), device_info().sms);
             FDS_LAUNCH(kern, ctas, 32 * (1 + kFtDofs), ssm, st, lo, hi, K, hanning ? 1 : 0, eta * dt, post, tw, wout,
-                       out_dev);
-        } else if (L == kFsmL && fsm_stockham() && sk == 1 && K > 1) {
-            // frequency-major spectra: CTA-cooperative groups of adjacent DOFs.
-            // 8 warps x 16-DOF groups x 2-deep ring (148 KB smem, 1 CTA/SM). Measured on the
-            // 300k-DOF cfg5 spectra: 0.69 ms vs 0.77 ms for warp-private DOF pairs; 8-DOF
-            // groups (2 CTAs/SM), 24-DOF groups, a 3-deep ring and 16 warps were 0.73-0.80 ms.
-            constexpr int W = 8, P = 2, D = 16;
-            auto kern = fsm_stockham256_tile_kernel<W, P, D>;
-            const size_t ssm = (static_cast<size_t>(P) * D * kFsmStride + kFsmL) * sizeof(cplx);
-            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), ssm);
-            int per_sm = 0;
-            FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, ssm));
-            const int ctas = std::min(ceil_div(K, D), std::max(1, per_sm) * device_info().sms);
-            FDS_LAUNCH(kern, ctas, W * 32, ssm, st, K, half_dev, sk, si, hanning ? 1 : 0, eta * dt, post, tw, wout,
                        out_dev);
         } else if (L == kFsmL && fsm_stockham()) {
             // 4 warps x 2-deep ring of DOF pairs: 74 KB smem, 2 CTAs (8 warps) per SM

@@ -2157,20 +2157,7 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                 FDS_LAUNCH(kern, g3, kGemmThreads, sm, st, tm.a, tm.b32, gm.l, gm.u32, pb.A, pb.mstride, pb.plane,
                            pb.n, pb.ld, k, c0);
             };
-            static const int v3 = [] {
-                const char* e = std::getenv("FDSWEEP_G3");
-                return e ? std::atoi(e) : 0;
-            }();
-            if (v3 == 1) {  // experiment: 4 warps of 32x16 per 64x32 tile
-                auto go4 = [&](auto kern) {
-                    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), sm);
-                    dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, 32), pb.batch);
-                    FDS_LAUNCH(kern, g3, 128, sm, st, tm.a, tm.b32, gm.l, gm.u32, pb.A, pb.mstride, pb.plane, pb.n,
-                               pb.ld, k, c0);
-                };
-                if (w == 128) go4(lu_gemm3m_tma_kernel<128, 32, 2, 2, 128>);
-                else go4(lu_gemm3m_tma_kernel<64, 32, 2, 2, 128>);
-            } else if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>);
+            if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>);
             else go(lu_gemm3m_tma_kernel<64, 32, 4, 2>);
         } else if (w == 128)
             FDS_LAUNCH(lu_gemm_tma_kernel<128>, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st,

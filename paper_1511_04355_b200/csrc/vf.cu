@@ -19,8 +19,12 @@
 //   vf_chanerr_kernel    CTA per channel: max_g|f_H − f_L|, max_g|f_H|.
 //   vf_select_kernel     exclusion-radius filtered argmax of |f_H − f_L| for the
 //                        worst ORF channel (first maximum = smallest ω).
-// Host work (latency-bound, microseconds): the shared pivoted QR, the
-// stacked σ least squares and the M x M eigenproblem (host_linalg.cpp).
+//   vf_eval_kernel       eval_model / fit_error_evf (vecfit.cpp:490-526): thread
+//                        per (s, channel) partial-fraction sum, exact pole
+//                        collisions flagged for NumericError.
+// The shared pivoted QR and the stacked σ least squares run on one CTA
+// (vf_lsq.cu); only the M x M relocation eigenproblem stays on the host
+// (eig_host.cpp).
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -28,6 +32,7 @@
 #include "eig_host.h"
 
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include "vf.cuh"
 
@@ -42,6 +47,17 @@ void* VfContext::Buf::get(size_t need) {
         bytes = need;
     }
     return p;
+}
+
+void VfContext::release() {
+    if (st) cudaStreamSynchronize(st);
+    for (Buf* b : {&values, &resid, &W, &phi, &rms, &tab, &tab2, &out, &misc, &misc2, &qr, &lsq, &lsq_io}) {
+        if (b->p) cudaFree(b->p);
+        b->p = nullptr;
+        b->bytes = 0;
+    }
+    w_valid = false;
+    w_key.clear();
 }
 
 VfContext& VfContext::get() {
@@ -266,7 +282,7 @@ constexpr int kResThreads = 128;
 
 __global__ void __launch_bounds__(kResThreads)
 vf_residue_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
-                  cplx* __restrict__ res) {
+                  cplx* __restrict__ res, int heads) {
     extern __shared__ double wsm[];  // [kResChunk][2J]
     const int m0 = blockIdx.y * kResChunk;
     const int cm = min(kResChunk, M - m0);
@@ -296,6 +312,7 @@ vf_residue_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, con
         } else {
             r = mk(x[c], 0.0);
         }
+        if (heads && m < 2 * P && (m & 1)) continue;  // conjugate row not requested
         res[static_cast<size_t>(m) * K + k] = r;
     }
 }
@@ -318,7 +335,7 @@ __host__ __device__ inline int res_steps(int J, int PF) { return ((J + 1) / 2 + 
 template <int MT, int PF>
 __global__ void __launch_bounds__(128, 4)
 vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
-                      cplx* __restrict__ res) {
+                      cplx* __restrict__ res, int heads) {
     // Persistent CTAs; W (the shared solve operator, M x 2J) staged once in smem
     // as the A operand, zero past row M and past column 2J (the padded steps).
     // Each warp owns 16 channels x 8 MT poles per tile; its B fragments (Re/Im
@@ -403,7 +420,7 @@ vf_residue_mma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
                     const double x = acc[mi][ni][e];
                     const double y = __shfl_xor_sync(0xffffffffu, x, 4);
                     const int k = kb + ni * 8 + 2 * q_l + e;
-                    if (m >= M || k >= K) continue;
+                    if (m >= M || k >= K || (heads && m < 2 * P && (m & 1))) continue;
                     cplx r;
                     if (m < 2 * P) r = (m % 2 == 0) ? mk(x, y) : mk(y, -x);
                     else r = mk(x, 0.0);
@@ -588,7 +605,7 @@ constexpr int kRtRow = 2 * kRtTile + 8;  // doubles per staged value row
 template <int MT, int SP, int ST>
 __global__ void __launch_bounds__(32 + 64 * MT, 1)
 vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
-                      cplx* __restrict__ res) {
+                      cplx* __restrict__ res, int heads) {
     extern __shared__ double rtm_raw[];
     double* ring = rtm_raw;
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(ST) * J * kRtRow);
@@ -666,13 +683,114 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
                 const double x = acc[nt][e];
                 const double y = __shfl_xor_sync(0xffffffffu, x, 4);
                 const int k = k0 + nt * 8 + 2 * q_l + e;
-                if (mrow >= M || k >= K) continue;
+                if (mrow >= M || k >= K || (heads && mrow < 2 * P && (mrow & 1))) continue;
                 cplx r;
                 if (mrow < 2 * P) r = (mrow % 2 == 0) ? mk(x, y) : mk(y, -x);
                 else r = mk(x, 0.0);
                 __stcs(reinterpret_cast<double2*>(res) + static_cast<size_t>(mrow) * K + k, make_double2(r.re, r.im));
             }
     }
+}
+
+// out[g*K + k] = sum_m res[k*M + m] / (s_g - a_m) (vecfit.cpp:490-509); *hit is
+// set when some s_g equals a pole exactly (the reference's NumericError).
+__global__ void vf_eval_kernel(int M, const cplx* __restrict__ poles, int K, const cplx* __restrict__ res, int G,
+                               const cplx* __restrict__ s, cplx* __restrict__ out, int* __restrict__ hit) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<size_t>(G) * K) return;
+    const int g = static_cast<int>(idx / K), k = static_cast<int>(idx % K);
+    const cplx sg = s[g];
+    cplx acc = mk(0.0, 0.0);
+    for (int m = 0; m < M; ++m) {
+        const cplx d = sg - poles[m];
+        if (d.re == 0.0 && d.im == 0.0) {
+            *hit = 1;
+            return;
+        }
+        acc = acc + cdiv(res[static_cast<size_t>(k) * M + m], d);
+    }
+    out[idx] = acc;
+}
+
+// fit_error_evf (vecfit.cpp:511-526) for one channel: one CTA, fixed-order
+// tree reduction of sum |fit - data|^2 and sum |data|^2 over the J samples.
+__global__ void vf_evf_kernel(int M, const cplx* __restrict__ poles, const cplx* __restrict__ res_k, int J,
+                              const cplx* __restrict__ s, const cplx* __restrict__ data, int dstride,
+                              double* __restrict__ out2, int* __restrict__ hit) {
+    __shared__ double rn[256], rd[256];
+    double num = 0.0, den = 0.0;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+        cplx acc = mk(0.0, 0.0);
+        for (int m = 0; m < M; ++m) {
+            const cplx d = s[j] - poles[m];
+            if (d.re == 0.0 && d.im == 0.0) { *hit = 1; break; }
+            acc = acc + cdiv(res_k[m], d);
+        }
+        const cplx v = data[static_cast<size_t>(j) * dstride];
+        num += abs2(acc - v);
+        den += abs2(v);
+    }
+    rn[threadIdx.x] = num;
+    rd[threadIdx.x] = den;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            rn[threadIdx.x] += rn[threadIdx.x + w];
+            rd[threadIdx.x] += rd[threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out2[0] = rn[0];
+        out2[1] = rd[0];
+    }
+}
+
+void vf_eval_model(const std::vector<Cx>& poles, const Cx* res_km, int K, const std::vector<Cx>& s, Cx* out) {
+    const int M = static_cast<int>(poles.size()), G = static_cast<int>(s.size());
+    if (G == 0 || K == 0) return;
+    auto& cx = VfContext::get();
+    const size_t nres = static_cast<size_t>(K) * M, nout = static_cast<size_t>(G) * K;
+    cplx* d = static_cast<cplx*>(cx.values.get(sizeof(cplx) * (M + nres + G + nout) + sizeof(int)));
+    cplx *dp = d, *dr = dp + M, *ds = dr + nres, *dout = ds + G;
+    int* dhit = reinterpret_cast<int*>(dout + nout);
+    FDS_CUDA(cudaMemcpyAsync(dp, poles.data(), M * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dr, res_km, nres * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(ds, s.data(), G * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemsetAsync(dhit, 0, sizeof(int), cx.st));
+    FDS_LAUNCH(vf_eval_kernel, static_cast<unsigned>((nout + 255) / 256), 256, 0, cx.st, M, dp, K, dr, G, ds, dout, dhit);
+    int hit = 0;
+    FDS_CUDA(cudaMemcpyAsync(&hit, dhit, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(out, dout, nout * sizeof(cplx), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    if (hit) throw NumericError("eval_model: s coincides with a pole");
+}
+
+double vf_fit_error_evf(const std::vector<Cx>& poles, const Cx* res_k, const std::vector<Cx>& s, const Cx* data,
+                        int dstride) {
+    const int M = static_cast<int>(poles.size()), J = static_cast<int>(s.size());
+    if (J == 0) throw ValidationError("fit_error_evf: no samples");
+    auto& cx = VfContext::get();
+    cplx* d = static_cast<cplx*>(cx.values.get(sizeof(cplx) * (2 * M + 2 * static_cast<size_t>(J) + 2)));
+    cplx *dp = d, *dr = dp + M, *ds = dr + M, *dd = ds + J;
+    double* d2 = reinterpret_cast<double*>(dd + J);
+    int* dhit = reinterpret_cast<int*>(d2 + 2);
+    std::vector<Cx> col(J);
+    for (int j = 0; j < J; ++j) col[j] = data[static_cast<size_t>(j) * dstride];
+    FDS_CUDA(cudaMemcpyAsync(dp, poles.data(), M * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dr, res_k, M * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(ds, s.data(), J * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(dd, col.data(), J * sizeof(cplx), cudaMemcpyHostToDevice, cx.st));
+    FDS_CUDA(cudaMemsetAsync(dhit, 0, sizeof(int), cx.st));
+    FDS_LAUNCH(vf_evf_kernel, 1, 256, 0, cx.st, M, dp, dr, J, ds, dd, 1, d2, dhit);
+    double h2[2];
+    int hit = 0;
+    FDS_CUDA(cudaMemcpyAsync(h2, d2, sizeof(h2), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaMemcpyAsync(&hit, dhit, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+    FDS_CUDA(cudaStreamSynchronize(cx.st));
+    if (hit) throw NumericError("eval_model: s coincides with a pole");
+    if (h2[1] == 0.0) throw NumericError("fit_error_evf: zero-norm sample data");
+    return std::sqrt(h2[0] / h2[1]);
 }
 
 // ------------------------------------------------------------------ host drivers
@@ -789,42 +907,59 @@ RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const
 }
 
 void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K, const std::vector<Cx>& poles,
-                        cplx* res_dev, double* rms_dev, cudaStream_t st) {
+                        cplx* res_dev, double* rms_dev, cudaStream_t st, bool heads_only) {
     // vecfit.cpp:356-408 for all channels: factor [Re Φ; Im Φ] (column-scaled)
     // once on the host, apply its solve operator on the device.
     const int J = static_cast<int>(s.size()), M = static_cast<int>(poles.size());
     if (J < 1) throw ValidationError("identify_residues: no samples");
     if (2 * J < M) throw ValidationError("identify_residues: too few samples for the order");
     require_distinct(s);
-    const std::vector<Cx> phi = basis(s, poles);
     const int rows = 2 * J;
-    std::vector<double> a(static_cast<size_t>(rows) * M), scale(M);  // column-major [Re Phi; Im Phi]
-    for (int m = 0; m < M; ++m) {
-        double n2 = 0.0;
-        for (int j = 0; j < J; ++j) {
-            const Cx v = phi[static_cast<size_t>(m) * J + j];
-            a[static_cast<size_t>(m) * rows + 2 * j] = v.real();
-            a[static_cast<size_t>(m) * rows + 2 * j + 1] = v.imag();
-            n2 += v.real() * v.real() + v.imag() * v.imag();
-        }
-        const double n = std::sqrt(n2);
-        scale[m] = n > 0.0 ? 1.0 / n : 1.0;
-        for (int i = 0; i < rows; ++i) a[static_cast<size_t>(m) * rows + i] *= scale[m];
-    }
-    // one shared pivoted QR (vecfit.cpp:389) turned into the solve operator
-    // W (M x 2J, rows pre-scaled) on the device
     auto& cx = VfContext::get();
-    double* da = dev<double>(cx.lsq_io, a.size() + M + 2 * sizeof(VfLsqStatus) / sizeof(double) + 2);
-    double* dscale = da + a.size();
-    auto* dstat = reinterpret_cast<VfLsqStatus*>(dscale + M);
+    // The solve operator depends only on (s, poles): the last one stays in HBM
+    // and is reused when a call repeats them bit for bit (e.g. the final
+    // all-channel fit of run_afs after the last iteration's high-order fit,
+    // afs.cpp:379-393).
+    std::vector<double> key;
+    key.reserve(2 + 2 * (J + M));
+    key.push_back(J);
+    key.push_back(M);
+    for (Cx x : s) { key.push_back(x.real()); key.push_back(x.imag()); }
+    for (Cx x : poles) { key.push_back(x.real()); key.push_back(x.imag()); }
     double* dW = dev<double>(cx.W, static_cast<size_t>(M) * rows);
-    FDS_CUDA(cudaMemcpyAsync(da, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-    FDS_CUDA(cudaMemcpyAsync(dscale, scale.data(), M * sizeof(double), cudaMemcpyHostToDevice, st));
-    vf_lsq_launch(rows, M, da, 1, rows, nullptr, nullptr, dW, dscale, dstat, st);
-    VfLsqStatus hst;
-    FDS_CUDA(cudaMemcpyAsync(&hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, st));
-    FDS_CUDA(cudaStreamSynchronize(st));
-    if (hst.rank < M) throw NumericError("identify_residues: rank-deficient least-squares system");
+    const bool cached = cx.w_valid && cx.w_key.size() == key.size() &&
+                        std::memcmp(cx.w_key.data(), key.data(), key.size() * sizeof(double)) == 0;
+    if (!cached) {
+        cx.w_valid = false;
+        const std::vector<Cx> phi = basis(s, poles);
+        std::vector<double> a(static_cast<size_t>(rows) * M), scale(M);  // column-major [Re Phi; Im Phi]
+        for (int m = 0; m < M; ++m) {
+            double n2 = 0.0;
+            for (int j = 0; j < J; ++j) {
+                const Cx v = phi[static_cast<size_t>(m) * J + j];
+                a[static_cast<size_t>(m) * rows + 2 * j] = v.real();
+                a[static_cast<size_t>(m) * rows + 2 * j + 1] = v.imag();
+                n2 += v.real() * v.real() + v.imag() * v.imag();
+            }
+            const double n = std::sqrt(n2);
+            scale[m] = n > 0.0 ? 1.0 / n : 1.0;
+            for (int i = 0; i < rows; ++i) a[static_cast<size_t>(m) * rows + i] *= scale[m];
+        }
+        // one shared pivoted QR (vecfit.cpp:389) turned into the solve operator
+        // W (M x 2J, rows pre-scaled) on the device
+        double* da = dev<double>(cx.lsq_io, a.size() + M + 2 * sizeof(VfLsqStatus) / sizeof(double) + 2);
+        double* dscale = da + a.size();
+        auto* dstat = reinterpret_cast<VfLsqStatus*>(dscale + M);
+        FDS_CUDA(cudaMemcpyAsync(da, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        FDS_CUDA(cudaMemcpyAsync(dscale, scale.data(), M * sizeof(double), cudaMemcpyHostToDevice, st));
+        vf_lsq_launch(rows, M, da, 1, rows, nullptr, nullptr, dW, dscale, dstat, st);
+        VfLsqStatus hst;
+        FDS_CUDA(cudaMemcpyAsync(&hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, st));
+        FDS_CUDA(cudaStreamSynchronize(st));
+        if (hst.rank < M) throw NumericError("identify_residues: rank-deficient least-squares system");
+        cx.w_key = std::move(key);
+        cx.w_valid = true;
+    }
     const int P = pair_count(poles);
     const size_t smem = static_cast<size_t>(kResChunk) * 2 * J * sizeof(double);
     ensure_dynamic_smem(reinterpret_cast<const void*>(vf_residue_kernel), smem);
@@ -832,6 +967,7 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
     const size_t msmem = static_cast<size_t>(4 * res_steps(J, PF)) * kRmS * sizeof(double);
     cudaEvent_t pe;
     profiler().begin(st, kProfVfResidue, 0.0, pe);
+    const int hf = heads_only ? 1 : 0;
     const int mt_all = std::min(8, ceil_div(M, 8));
     const size_t row_bytes = static_cast<size_t>(J) * kRtRow * sizeof(double);
     const int rt_st = std::min<int>(4, static_cast<int>((device_info().smem_optin - 1024) / std::max<size_t>(row_bytes, 1)));
@@ -841,7 +977,7 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
         auto go = [&](auto kern) {
             ensure_dynamic_smem(reinterpret_cast<const void*>(kern), tsmem);
             FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 32 + 64 * mt_all, tsmem, st, J, K, M, P, values_dev, dW,
-                       res_dev);
+                       res_dev, hf);
         };
         auto by_sp = [&](auto mtc) {
             constexpr int MTc = decltype(mtc)::value;
@@ -872,7 +1008,7 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
         const int mt = std::min(8, ceil_div(M, 8));  // m-tiles of the first (largest) slice
         auto go = [&](auto kern) {
             ensure_dynamic_smem(reinterpret_cast<const void*>(kern), msmem);
-            FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 128, msmem, st, J, K, M, P, values_dev, dW, res_dev);
+            FDS_LAUNCH(kern, dim3(ctas, ceil_div(M, 64)), 128, msmem, st, J, K, M, P, values_dev, dW, res_dev, hf);
         };
         if (PF == 5) {
             if (mt <= 2) go(vf_residue_mma_kernel<2, 5>);
@@ -887,10 +1023,10 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
         }
     } else {
         dim3 g(ceil_div(K, kResThreads), ceil_div(M, kResChunk));
-        FDS_LAUNCH(vf_residue_kernel, g, kResThreads, smem, st, J, K, M, P, values_dev, dW, res_dev);
+        FDS_LAUNCH(vf_residue_kernel, g, kResThreads, smem, st, J, K, M, P, values_dev, dW, res_dev, hf);
     }
-    // algorithmic bytes: values 16 J + unique residues 16 M/2 per channel
-    profiler().end(st, pe, kProfVfResidue, static_cast<double>(K) * (16.0 * J + 8.0 * M));
+    // bytes moved: values 16 J + residues 16 M (all rows) or 8 M (pair heads + reals) per channel
+    profiler().end(st, pe, kProfVfResidue, static_cast<double>(K) * (16.0 * J + (heads_only ? 8.0 : 16.0) * M));
     if (rms_dev) {
         std::vector<Cx> invd(static_cast<size_t>(M) * J);
         for (int m = 0; m < M; ++m)

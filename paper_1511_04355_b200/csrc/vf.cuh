@@ -21,6 +21,9 @@ struct VfContext {
         void* get(size_t need);
     };
     Buf values, resid, W, phi, rms, tab, tab2, out, misc, misc2, qr, lsq, lsq_io;
+    std::vector<double> w_key;  // (J, M, s, poles) of the solve operator held in W
+    bool w_valid = false;
+    void release();  // frees every buffer (and forgets the cached solve operator)
     static VfContext& get();
 };
 
@@ -54,9 +57,18 @@ RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const
 
 // identify_residues for K channels whose values live on the device as
 // [j][k] complex (values_dev); residues written on the device as [m][k];
-// rms_dev (K doubles) optional. Poles must already be canonical.
+// rms_dev (K doubles) optional. Poles must already be canonical. heads_only:
+// the conjugate row m+1 of each pole pair is not written (its values are
+// conj(row m); consumers that use the pair symmetry never read it).
 void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
-                        const std::vector<Cx>& poles, cplx* res_dev, double* rms_dev, cudaStream_t st);
+                        const std::vector<Cx>& poles, cplx* res_dev, double* rms_dev, cudaStream_t st,
+                        bool heads_only = false);
+
+// eval_model (vecfit.cpp:490-509) on the device: out[g*K + k], residues [k][m].
+void vf_eval_model(const std::vector<Cx>& poles, const Cx* res_km, int K, const std::vector<Cx>& s, Cx* out);
+// fit_error_evf (vecfit.cpp:511-526) of one channel: residues res_k[m], data[j*dstride].
+double vf_fit_error_evf(const std::vector<Cx>& poles, const Cx* res_k, const std::vector<Cx>& s, const Cx* data,
+                        int dstride);
 
 struct FitReportC {
     int iterations = 0;

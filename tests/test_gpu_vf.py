@@ -350,3 +350,68 @@ def test_identify_residues_shapes(J, pairs, reals, K):
         ro, rmso = O.identify_residues(s, v[:, k], p)
         assert rel_l2(res[k], ro) < 1e-10, (k, rel_l2(res[k], ro))
         assert rms[k] == pytest.approx(rmso, rel=1e-8)
+
+
+def test_identify_residues_heads_only_and_rational_invert():
+    """fds_vf_identify_residues_device_heads writes the pair heads and real poles
+    only (conjugate rows keep whatever the buffer held: here NaN), and
+    fds_rational_invert_device on that buffer matches the oracle's
+    rational_invert of the full model (laplace.cpp:127-164)."""
+    import ctypes
+
+    import torch
+
+    rng = np.random.default_rng(11)
+    J, K = 40, 777
+    p = []
+    for m in range(10):
+        a = complex(-0.1 - 0.03 * m, 0.5 + 1.3 * m)
+        p += [a, a.conjugate()]
+    p += [complex(-0.7, 0.0)]
+    p = np.array(p)
+    M = len(p)
+    s = 0.3 + 1j * np.linspace(0.1, 15.0, J)
+    v = rng.normal(size=(J, K)) + 1j * rng.normal(size=(J, K))
+    full, _ = P.identify_residues(s, v, p)  # (K, M), every row
+    vd = torch.tensor(v, device="cuda")
+    rd = torch.full((M, K), complex(float("nan"), float("nan")), dtype=torch.complex128, device="cuda")
+    L = P.lib()
+    pc = np.ascontiguousarray(O.canonical_poles(p))
+    P.api._check(L.fds_vf_identify_residues_device_heads(
+        J, K, s.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(vd.data_ptr()), M, pc.ctypes.data_as(ctypes.c_void_p),
+        ctypes.c_void_p(rd.data_ptr()), None))
+    r = rd.cpu().numpy()
+    heads = [m for m in range(M) if not (m < 20 and m % 2 == 1)]
+    conj_rows = [m for m in range(M) if m < 20 and m % 2 == 1]
+    np.testing.assert_array_equal(r[heads].T, full[:, heads])
+    assert np.all(np.isnan(r[conj_rows]))
+    t = np.linspace(0.0, 8.0, 300)
+    out = torch.empty((K, len(t)), dtype=torch.float64, device="cuda")
+    P.api._check(L.fds_rational_invert_device(M, pc.ctypes.data_as(ctypes.c_void_p), K, ctypes.c_void_p(rd.data_ptr()),
+                                              len(t), t.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(out.data_ptr()),
+                                              None))
+    sub = [0, 5, 400, K - 1]
+    ho = O.rational_invert(pc, full[sub], t)
+    assert rel_l2(out.cpu().numpy()[sub], ho) < 1e-12
+
+
+def test_eval_model_and_fit_error_on_device():
+    """Row a8: eval_model (vecfit.cpp:490-509) and fit_error_evf (:511-526)
+    through the device kernels against the oracle, plus the pole-collision
+    NumericError and the zero-norm error."""
+    s, v = _noisy_modal(7, 30)
+    o = O.vector_fit(s, v, [0, 1], 12, 3)
+    model = P.RationalModel(o["poles"], o["residues"])
+    grid = 0.35 + 1j * np.linspace(0.0, 40.0, 257)
+    g = P.eval_model(model, grid)  # (G, K)
+    for gi in (0, 100, 256):
+        ref = O.eval_model(o["poles"], o["residues"], grid[gi])
+        assert rel_l2(g[gi], ref) < 1e-13
+    for k in range(7):
+        e = P.fit_error_evf(model, k, s, v)
+        eo = O.fit_error_evf(o["poles"], o["residues"], k, s, v)
+        assert e == pytest.approx(eo, rel=1e-10)
+    with pytest.raises(P.NumericError):
+        P.eval_model(model, [o["poles"][0]])
+    with pytest.raises(P.NumericError):
+        P.fit_error_evf(model, 0, s, np.zeros_like(v))
