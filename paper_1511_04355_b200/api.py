@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -20,6 +21,10 @@ _LIB_NAME = "libfdsweep_b200.so"
 
 
 def library_path() -> Path:
+    # FDSWEEP_LIB_VARIANT=jitter selects the race-stress build (same code with
+    # timing perturbation at the synchronisation points; tests only)
+    if os.environ.get("FDSWEEP_LIB_VARIANT") == "jitter":
+        return HERE / _LIB_NAME.replace(".so", "_jitter.so")
     return HERE / _LIB_NAME
 
 

@@ -122,6 +122,24 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return encode;
 }
 
+// Timing-perturbation points for the race stress test (tests/test_gpu_race_stress.py):
+// compiled to nothing in the product library; the FDS_JITTER build
+// (libfdsweep_b200_jitter.so) sleeps a pseudo-random 0-8 us at every point, so
+// a missing fence or barrier in a hand-rolled synchronisation protocol shows
+// up as results that are no longer bit-identical to the product library's.
+#ifdef FDS_JITTER
+__device__ __forceinline__ void fds_jitter(unsigned salt) {
+    unsigned h = (blockIdx.x * 73856093u) ^ (blockIdx.y * 2654435761u) ^ (blockIdx.z * 40503u) ^
+                 (threadIdx.x * 19349663u) ^ (salt * 83492791u) ^ static_cast<unsigned>(clock64());
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    if ((h & 3u) == 0u) __nanosleep(h % 8192u);
+}
+#else
+__device__ __forceinline__ void fds_jitter(unsigned) {}
+#endif
+
 // ---------------------------------------------------------------- mbarrier / TMA (sm_90+ async proxy)
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),

@@ -524,6 +524,7 @@ fsm256_tma_kernel(const __grid_constant__ CUtensorMap tm_lo, const __grid_consta
             for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
                 const int q = i % ST;
                 if (i >= ST) mbar_wait(&empty[q], ((i / ST) - 1) & 1);
+                fds_jitter(i);
                 unsigned char* stg = base + q * kFtStageBytes;
                 mbar_expect_tx(&full[q], 257u * 128u);
                 tma_load_2d(stg, &tm_lo, &full[q], 2 * kFtDofs * g, 0);
@@ -546,6 +547,7 @@ fsm256_tma_kernel(const __grid_constant__ CUtensorMap tm_lo, const __grid_consta
             return *reinterpret_cast<const cplx*>(stg + n * 128 + 16 * (d ^ (n & 7)));
         };
         auto rel = [&] {
+            fds_jitter(i);
             if (lane == 0) mbar_arrive(&empty[q]);
         };
         if (k < K) {

@@ -53,6 +53,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 
 __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
+    fds_jitter(target);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -305,6 +306,7 @@ lu_panel_cluster_kernel(double* A, size_t mstride, size_t plane, int n, int ld, 
                 }
             }
             ++step;
+            fds_jitter(step);
             cluster.sync();
             // winner among the P candidates (peers' smem), pivot row + old row c
             if (wid == 0) {
@@ -450,7 +452,8 @@ lu_swap_trsm_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int 
 
 // ------------------------------------------------------------------ DMMA GEMM
 constexpr int GBM = 64, GBN = 64, GBK = 16, GSTAGES = 2;
-constexpr int kG3Rows = 136;  // U12 sum-plane column length: 128 panel rows + TMA over-read
+constexpr int kG3W = 256;      // deepest trailing update (256-column super-panels)
+constexpr int kG3Rows = kG3W + 8;  // U12 sum-plane column length: update depth + TMA over-read
 constexpr int GAS = GBM + 4;  // A tile row stride (doubles) ≡ 4 (mod 16): conflict-free fragments
 constexpr int GBS = GBK + 4;  // B tile row stride
 constexpr int kGemmThreads = 256;
@@ -743,8 +746,8 @@ __global__ void lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, 
     const int b = blockIdx.y;
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
-    double* L = g3 + static_cast<size_t>(b) * 2 * 128 * ld;
-    double* U = g3 + static_cast<size_t>(gridDim.y) * 2 * 128 * ld + static_cast<size_t>(b) * ld * kG3Rows;
+    double* L = g3 + static_cast<size_t>(b) * 2 * kG3W * ld;
+    double* U = g3 + static_cast<size_t>(gridDim.y) * 2 * kG3W * ld + static_cast<size_t>(b) * ld * kG3Rows;
     const int rows = do_l ? n - k - w : 0;
     const long long nl = static_cast<long long>(rows) * w, nu = static_cast<long long>(c1 - c0) * w;
     for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < nl + nu;
@@ -754,7 +757,7 @@ __global__ void lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, 
             const size_t gi = static_cast<size_t>(k + kk) * ld + m;
             const double x = Are[gi], y = Aim[gi];
             L[static_cast<size_t>(kk) * ld + m] = x + y;
-            L[static_cast<size_t>(128 + kk) * ld + m] = x - y;
+            L[static_cast<size_t>(kG3W + kk) * ld + m] = x - y;
         } else {
             const long long u = q - nl;
             const int c = c0 + static_cast<int>(u / w), kk = static_cast<int>(u % w);
@@ -764,7 +767,7 @@ __global__ void lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, 
     }
 }
 
-template <int W, int BN, int WGM, int MINB, int NT = kGemmThreads>
+template <int W, int BN, int WGM, int MINB, int NT = kGemmThreads, int PFIRST = 0>
 __global__ void __launch_bounds__(NT, MINB)
 lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmU, double* A,
@@ -823,13 +826,9 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 p[mi][ni][e] = 0.0;
             }
     }
-    // No CTA barrier per k-chunk: each warp's lane 0 counts itself out of a stage
-    // once its fragment loads have been consumed, and the last warp out refills the
-    // stage with chunk kc + GSTAGES (fast warps never wait for slow ones).
-#pragma unroll 1
-    for (int kc = 0; kc < nk; ++kc) {
-        const int st = kc % GSTAGES;
-        mbar_wait(&bar[st], (kc / GSTAGES) & 1);
+    // passes [p0, p1) of chunk kc (P: Re A x (Re+Im) B, Q: (Re+Im) A x Im B,
+    // R: (Re-Im) A x Re B), each holding only its own MI + NI fragments
+    auto compute = [&](int st, int p0, int p1) {
         const double* ar = As(st, 0);
         const double* as = As(st, 1);
         const double* ad = As(st, 2);
@@ -839,10 +838,9 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 #pragma unroll
         for (int k4 = 0; k4 < GBK; k4 += 4) {
             const int kr = k4 + (lane & 3);
-            // three passes (P: Re A x (Re+Im) B, Q: (Re+Im) A x Im B, R: (Re-Im) A x Re B),
-            // each holding only its own MI + NI fragments
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
+                if (pass < p0 || pass >= p1) continue;
                 const double* pa = pass == 0 ? ar : (pass == 1 ? as : ad);
                 const double* pb = pass == 0 ? bs : (pass == 1 ? bi : br);
                 double fa[MI], fb[NI];
@@ -859,6 +857,27 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     }
             }
         }
+    };
+    // P-first prologue (PFIRST chunks): the C-independent product runs while the
+    // C tile loads into the Q / R accumulators are still in flight
+#pragma unroll 1
+    for (int kc = 0; kc < PFIRST && kc < nk; ++kc) {
+        mbar_wait(&bar[kc % GSTAGES], (kc / GSTAGES) & 1);
+        compute(kc % GSTAGES, 0, 1);
+    }
+    // No CTA barrier per k-chunk: each warp's lane 0 counts itself out of a stage
+    // once its fragment loads have been consumed, and the last warp out refills the
+    // stage with chunk kc + GSTAGES (fast warps never wait for slow ones).
+#pragma unroll 1
+    for (int kc = 0; kc < nk; ++kc) {
+        const int st = kc % GSTAGES;
+        if (kc < PFIRST) {
+            compute(st, 1, 3);
+        } else {
+            mbar_wait(&bar[st], (kc / GSTAGES) & 1);
+            compute(st, 0, 3);
+        }
+        fds_jitter(kc);
         if (kc + GSTAGES < nk) {
             __syncwarp();
             if (lane == 0) {
@@ -1054,12 +1073,13 @@ constexpr int kApplyCols = 32;  // strip width: L11^{-1} + one strip = 104 KB sm
 // untouched strip, and U12 = L11^{-1} (P A12) runs on DMMA.
 // mode 0: swap + TRSM; 1: swap only (the panel's interchanges applied to a
 // column range, e.g. an earlier panel's L columns); 2: TRSM only (rows already
-// in place); 3: swap, then the rank-64 update from the previous panel at kp
-// (X -= L[k.., kp..] U[kp.., strip], operands straight from L2 / HBM), then
-// TRSM — the second panel of a super-panel. Columns [cb, ce).
+// in place); 3: swap, then the rank-rlen update from the earlier panels of the
+// super-panel, columns [kp, kp + rlen) (X -= L[k.., kp..] U[kp.., strip],
+// operands straight from L2 / HBM), then TRSM — panels 2..4 of a super-panel
+// (rlen = 64, 128, 192). Columns [cb, ce).
 __global__ void __launch_bounds__(kApplyThreads, 2)
 lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int k, const double* linv, int cb, int ce,
-                     int mode, int kp) {
+                     int mode, int kp, int rlen) {
     extern __shared__ __align__(16) double ssm[];
     double* Lr = ssm;                 // [kk][m] = Linv[m][kk]
     double* Li = Lr + 64 * SAS;
@@ -1166,7 +1186,7 @@ lu_swap_apply_kernel(double* A, size_t mstride, size_t plane, int n, int ld, int
         const int nb_col = col0 + wn * 8 + (lane >> 2);
         const bool bok = nb_col < ce;
 #pragma unroll 4
-        for (int k4 = 0; k4 < 64; k4 += 4) {
+        for (int k4 = 0; k4 < rlen; k4 += 4) {
             const int kk = kp + k4 + (lane & 3);
             double nar[4], fai[4], nai[4];
 #pragma unroll
@@ -1551,6 +1571,7 @@ __device__ __forceinline__ int ld_relaxed_i(const int* p) {
 // the furthest block known ready, fenced once, and polls again only past it.
 // step = +1 (forward chain) or -1 (backward chain).
 __device__ __forceinline__ int wait_ready(const int* fl, int j, int last, int step) {
+    fds_jitter(j);
     int r = 0;
     if ((threadIdx.x & 31) == 0) {
         if (ld_relaxed_i(fl + last) != 0) {
@@ -1586,16 +1607,26 @@ __device__ __forceinline__ int swap_backward(int q, const int* pv, int k, int w)
 }
 
 // Interchange groups: 128-row super-panels below ks, nb-row panels from ks on.
+// Interchange groups: 256-row super-panels below k1, 128-row super-panels in
+// [k1, ks), nb-row panels from ks on.
 struct SwapGroups {
-    int n, nb, ks;
-    __device__ __forceinline__ int count() const { return (ks >> 7) + (n - ks + nb - 1) / nb; }
-    __device__ __forceinline__ int of(int r) const { return r < ks ? r >> 7 : (ks >> 7) + (r - ks) / nb; }
-    __device__ __forceinline__ int start(int g) const { return g < (ks >> 7) ? g << 7 : ks + (g - (ks >> 7)) * nb; }
-    __device__ __forceinline__ int size(int g) const { return min(g < (ks >> 7) ? 128 : nb, n - start(g)); }
+    int n, nb, k1, ks;
+    __host__ __device__ __forceinline__ int g1() const { return k1 >> 8; }
+    __host__ __device__ __forceinline__ int g2() const { return g1() + ((ks - k1) >> 7); }
+    __host__ __device__ __forceinline__ int count() const { return g2() + (n - ks + nb - 1) / nb; }
+    __device__ __forceinline__ int of(int r) const {
+        return r < k1 ? r >> 8 : (r < ks ? g1() + ((r - k1) >> 7) : g2() + (r - ks) / nb);
+    }
+    __device__ __forceinline__ int start(int g) const {
+        return g < g1() ? g << 8 : (g < g2() ? k1 + ((g - g1()) << 7) : ks + (g - g2()) * nb);
+    }
+    __device__ __forceinline__ int size(int g) const {
+        return min(g < g1() ? 256 : (g < g2() ? 128 : nb), n - start(g));
+    }
 };
 
-// pflag[b][g] = interchange group g has an interchange
-__global__ void __launch_bounds__(128)
+// pflag[b][g] = interchange group g has an interchange (blockDim >= the largest group)
+__global__ void __launch_bounds__(256)
 lu_pivflag_kernel(SwapGroups sg, const int* ipiv, int* pflag) {
     const int b = blockIdx.y, g = blockIdx.x;
     const int r = sg.start(g) + threadIdx.x;
@@ -1689,7 +1720,7 @@ __device__ __forceinline__ cplx apply_diag(const double* dsm, const cplx* v, cpl
 
 template <int NB>
 __global__ void __launch_bounds__(kDfThreads, 2)
-lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int ks, const int* ipiv,
+lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, int k1, int ks, const int* ipiv,
                  const int* pflag, const cplx* rhs, size_t rstride, cplx* ybuf, int* flags, int* tickets) {
     extern __shared__ double dsm[];  // unit-lower diagonal block
     __shared__ cplx part[4][64];
@@ -1705,7 +1736,7 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
     const int* pv = ipiv + static_cast<size_t>(b) * n;
-    const SwapGroups sg{n, nb, ks};
+    const SwapGroups sg{n, nb, k1, ks};
     const int* pf = pflag + static_cast<size_t>(b) * sg.count();
     int* fl = flags + static_cast<size_t>(b) * nblk;
     cplx* yb = ybuf + static_cast<size_t>(b) * n;
@@ -1759,6 +1790,7 @@ lu_fwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, i
     if (g == 0 && live) yb[k + tr] = y;
     __threadfence();
     __syncthreads();
+    fds_jitter(m);
     if (tid == 0) st_release_i(fl + m, 1);
 }
 
@@ -1823,6 +1855,7 @@ lu_bwd_df_kernel(const double* A, size_t mstride, size_t plane, int n, int ld, c
     if (g == 0 && live) x[k + tr] = xm;
     __threadfence();
     __syncthreads();
+    fds_jitter(m);
     if (tid == 0) st_release_i(fl + m, 1);
 }
 
@@ -1851,7 +1884,7 @@ void LuWorkspace::ensure_side() {
 }
 
 double* LuWorkspace::g3_planes(const LuProblem& pb) {
-    const size_t need = static_cast<size_t>(pb.batch) * pb.ld * (2 * 128 + kG3Rows);
+    const size_t need = static_cast<size_t>(pb.batch) * pb.ld * (2 * kG3W + kG3Rows);
     if (need > g3_cap) {
         if (g3) cudaFree(g3);
         FDS_CUDA(cudaMalloc(&g3, need * sizeof(double)));
@@ -2019,7 +2052,7 @@ void trsm_step(const LuProblem& pb, int k, int w, cudaStream_t st, double* linv,
         ensure_dynamic_smem(reinterpret_cast<const void*>(lu_swap_apply_kernel), asmem);
         if (!inverse_ready) l11_inverse_step(pb, k, st, linv);
         FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(rest, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
-                   pb.mstride, pb.plane, pb.n, pb.ld, k, linv, k + 64, pb.n, 0, 0);
+                   pb.mstride, pb.plane, pb.n, pb.ld, k, linv, k + 64, pb.n, 0, 0, 64);
     } else {
         dim3 gt(ceil_div(rest, kTrsmCols), pb.batch);
         FDS_LAUNCH(lu_swap_trsm_kernel<NB>, gt, kTrsmThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k,
@@ -2077,7 +2110,7 @@ const TmaMaps& tma_maps(const LuProblem& pb) {
 }
 
 // The 3M kernel's pre-formed operand planes (LuWorkspace::g3): L21 sums as a
-// [2 batch][128][ld] tensor (boxes 68 x 16 like tmA), U12 sums as [batch][ld][kG3Rows]
+// [2 batch][kG3W][ld] tensor (boxes 68 x 16 like tmA), U12 sums as [batch][ld][kG3Rows]
 // (boxes 20 x BN like tmB).
 struct G3Maps {
     double* base = nullptr;
@@ -2105,12 +2138,12 @@ const G3Maps& g3_maps(const LuProblem& pb, LuWorkspace& ws) {
                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     };
-    const cuuint64_t ldims[3] = {static_cast<cuuint64_t>(pb.ld), 128, static_cast<cuuint64_t>(2) * pb.batch};
+    const cuuint64_t ldims[3] = {static_cast<cuuint64_t>(pb.ld), kG3W, static_cast<cuuint64_t>(2) * pb.batch};
     const cuuint64_t lstr[2] = {static_cast<cuuint64_t>(pb.ld) * sizeof(double),
-                                static_cast<cuuint64_t>(pb.ld) * 128 * sizeof(double)};
+                                static_cast<cuuint64_t>(pb.ld) * kG3W * sizeof(double)};
     const cuuint32_t lbox[3] = {static_cast<cuuint32_t>(kTmaABox0), GBK, 1};
     enc(&m.l, base, ldims, lstr, lbox);
-    double* ubase = base + static_cast<size_t>(pb.batch) * 2 * 128 * pb.ld;
+    double* ubase = base + static_cast<size_t>(pb.batch) * 2 * kG3W * pb.ld;
     const cuuint64_t udims[3] = {kG3Rows, static_cast<cuuint64_t>(pb.ld), static_cast<cuuint64_t>(pb.batch)};
     const cuuint64_t ustr[2] = {kG3Rows * sizeof(double), static_cast<cuuint64_t>(pb.ld) * kG3Rows * sizeof(double)};
     const cuuint32_t ubox32[3] = {static_cast<cuuint32_t>(kTmaBBox0), 32, 1};
@@ -2132,7 +2165,8 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
     dim3 gg(ceil_div(rest, GBM), ceil_div(c1 - c0, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
-    if (w == 64 || w == 128) {
+    if (w == 256 && !(gemm_3m() && t_g3_ws)) throw CudaError("lu: rank-256 updates need the 3M kernel");
+    if (w == 64 || w == 128 || w == 256) {
         ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_tma_kernel<64>),
                             kGemmSmemDoubles * sizeof(double) + kTmaSmemPad);
         ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_tma_kernel<128>),
@@ -2157,8 +2191,10 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                 FDS_LAUNCH(kern, g3, kGemmThreads, sm, st, tm.a, tm.b32, gm.l, gm.u32, pb.A, pb.mstride, pb.plane,
                            pb.n, pb.ld, k, c0);
             };
-            if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2>);
-            else go(lu_gemm3m_tma_kernel<64, 32, 4, 2>);
+            // P-first prologue on the first chunk (measured 0.4 % faster at cfg4)
+            if (w == 256) go(lu_gemm3m_tma_kernel<256, 32, 4, 2, kGemmThreads, 1>);
+            else if (w == 128) go(lu_gemm3m_tma_kernel<128, 32, 4, 2, kGemmThreads, 1>);
+            else go(lu_gemm3m_tma_kernel<64, 32, 4, 2, kGemmThreads, 1>);
         } else if (w == 128)
             FDS_LAUNCH(lu_gemm_tma_kernel<128>, gg, kGemmThreads, kGemmSmemDoubles * sizeof(double) + kTmaSmemPad, st,
                        tm.a, tm.b, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, c0);
@@ -2323,11 +2359,12 @@ void profiler_scope_trsm(cudaStream_t st, F f, double work) {
     profiler().end(st, e, kProfLuTrsm, work);
 }
 
-void swap_cols(const LuProblem& pb, int k, int cb, int ce, int mode, const double* linv, cudaStream_t st, int kp = 0) {
+void swap_cols(const LuProblem& pb, int k, int cb, int ce, int mode, const double* linv, cudaStream_t st, int kp = 0,
+               int rlen = 64) {
     if (ce <= cb) return;
     const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
     FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(ce - cb, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
-               pb.mstride, pb.plane, pb.n, pb.ld, k, linv, cb, ce, mode, kp);
+               pb.mstride, pb.plane, pb.n, pb.ld, k, linv, cb, ce, mode, kp, rlen);
 }
 
 // Two 64-column panels P1 = [k, k+64), P2 = [k+64, k+128) with one rank-128
@@ -2357,6 +2394,66 @@ void super_panel_step(const LuProblem& pb, LuWorkspace& ws, int k, cudaStream_t 
     gemm_step(pb, k, 128, st);
 }
 
+// Four 64-column panels P1..P4 = [k, k+256) with one rank-256 trailing update:
+// the first half H1 = P1 P2 runs as super_panel_step except that its rank-128
+// update reaches only the second half's columns; P3 is factored, its
+// interchanges go into H1's L columns, P4's columns take L33^{-1} and P3's
+// rank-64 update, and the trailing columns take P3's interchanges, H1's
+// rank-128 update of P3's rows and L33^{-1} (strip mode 3, rlen 128); P4 is
+// factored, its interchanges go into [k, k+192) and the trailing columns take
+// them, the rank-192 update of P4's rows and L44^{-1}; then rows / columns
+// >= k+256 take [L21_1 .. L21_4][U12_1; ..; U12_4] in one pass — the trailing C
+// tiles are read and written once per 256 columns of k. Interchanges are in
+// LAPACK order inside the 256 columns, LINPACK order across super-panels.
+void super_panel256_step(const LuProblem& pb, LuWorkspace& ws, int k, cudaStream_t st) {
+    double* linv = ws.linv(pb.batch);
+    const int k2 = k + 64, k3 = k + 128, k4 = k + 192, kt = k + 256;
+    // H1 (P1, P2) with its update restricted to H2's columns
+    subpanel_block(pb, ws, k, 64, st, true);
+    trsm_step<64>(pb, k, 64, st, linv);
+    gemm_step(pb, k, 64, st, k2, k3);
+    subpanel_block(pb, ws, k2, 64, st, true);
+    profiler_scope_trsm(st, [&] {
+        l11_inverse_step(pb, k2, st, linv);
+        swap_cols(pb, k2, k, k2, 1, linv, st);
+        swap_cols(pb, k2, k3, pb.n, 3, linv, st, k, 64);
+    }, (4.0 + 8.0) * 64 * 64 * (pb.n - k3) * pb.batch);
+    gemm_step(pb, k, 128, st, k3, kt);
+    // P3
+    subpanel_block(pb, ws, k3, 64, st, true);
+    profiler_scope_trsm(st, [&] {
+        l11_inverse_step(pb, k3, st, linv);
+        swap_cols(pb, k3, k, k3, 1, linv, st);             // into H1's L columns
+        swap_cols(pb, k3, k4, kt, 0, linv, st);            // P4's columns: swap + L33^{-1}
+        swap_cols(pb, k3, kt, pb.n, 3, linv, st, k, 128);  // trailing: swap, H1's update, L33^{-1}
+    }, (4.0 + 8.0 * 2) * 64 * 64 * (pb.n - k4) * pb.batch);
+    gemm_step(pb, k3, 64, st, k4, kt);
+    // P4
+    subpanel_block(pb, ws, k4, 64, st, true);
+    profiler_scope_trsm(st, [&] {
+        l11_inverse_step(pb, k4, st, linv);
+        swap_cols(pb, k4, k, k4, 1, linv, st);             // into [k, k+192)
+        swap_cols(pb, k4, kt, pb.n, 3, linv, st, k, 192);  // trailing: swap, rank-192 update, L44^{-1}
+    }, (4.0 + 8.0 * 3) * 64 * 64 * (pb.n - kt) * pb.batch);
+    if (pb.n - kt <= 0) return;
+    gemm_step(pb, k, 256, st);
+}
+
+// 256-column super-panels (needs the 3M trailing update). Measured on B200:
+// the N = 3840 batch of 129 factors in 537 vs 552 ms with 256- vs 128-column
+// super-panels, the N = 15360 batch of 8 in 1995 vs 1983 ms (the rank-256
+// update does not raise the GEMM's steady-state rate there, and the second
+// half's panels run on a longer critical path), so the default takes them for
+// n <= 8192. FDSWEEP_SUPER256=0 / 1 forces them off / on.
+bool super256(int n) {
+    static const int env = [] {
+        const char* e = std::getenv("FDSWEEP_SUPER256");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (!gemm_3m()) return false;
+    return env >= 0 ? env != 0 : n <= 8192;
+}
+
 }  // namespace
 
 std::unique_lock<std::mutex> lu_device_gate() {
@@ -2376,7 +2473,7 @@ std::unique_lock<std::mutex> lu_device_gate() {
 
 void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     FDS_CUDA(cudaMemsetAsync(pb.info, 0, pb.batch * sizeof(int), st));
-    ws.super_end = 0;
+    ws.super_end = ws.super256_end = 0;
     struct G3Scope {  // the 3M update's operand planes live in this workspace
         explicit G3Scope(LuWorkspace* w) {
             w->g3_key_A = nullptr;
@@ -2392,7 +2489,12 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
     const int nb = lu_panel_width(pb.n);
     for (int k = 0; k < pb.n; k += nb) {
         const int w = std::min(nb, pb.n - k);
-        if (nb == 64 && w == 64 && use_subpanels(pb) && super_panels() && k + 128 <= pb.n) {
+        if (nb == 64 && w == 64 && use_subpanels(pb) && super_panels() && super256(pb.n) && k + 256 <= pb.n &&
+            ws.super_end == ws.super256_end) {
+            super_panel256_step(pb, ws, k, st);
+            ws.super_end = ws.super256_end = k + 256;
+            k += 192;  // four panels
+        } else if (nb == 64 && w == 64 && use_subpanels(pb) && super_panels() && k + 128 <= pb.n) {
             super_panel_step(pb, ws, k, st);
             ws.super_end = k + 128;
             k += 64;  // two panels
@@ -2449,6 +2551,7 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
     const int nb = lu_panel_width(pb.n);
     const int nblk = ceil_div(pb.n, nb);
     const int ks = nb == 64 ? ws.super_end : 0;
+    const int k1 = nb == 64 ? ws.super256_end : 0;
     ws.ensure_solve(pb.batch, pb.n, nblk);
     int* pflag = ws.sflags;  // [batch][groups] fits in the [batch][nblk] slot
     int* ffl = pflag + static_cast<size_t>(pb.batch) * nblk;
@@ -2456,15 +2559,15 @@ void lu_solve(const LuProblem& pb, cplx* rhs, size_t rstride, LuWorkspace& ws, c
     int* tk = bfl + static_cast<size_t>(pb.batch) * nblk;
     FDS_CUDA(cudaMemsetAsync(ffl, 0, (2 * static_cast<size_t>(pb.batch) * nblk + 2) * sizeof(int), st));
     const size_t smem = 2 * 64 * 64 * sizeof(double);
-    const SwapGroups sg{pb.n, nb, ks};
-    const int groups = (ks >> 7) + ceil_div(pb.n - ks, nb);
-    FDS_LAUNCH(lu_pivflag_kernel, dim3(groups, pb.batch), 128, 0, st, sg, pb.ipiv, pflag);
+    const SwapGroups sg{pb.n, nb, k1, ks};
+    const int groups = sg.count();
+    FDS_LAUNCH(lu_pivflag_kernel, dim3(groups, pb.batch), 256, 0, st, sg, pb.ipiv, pflag);
     const int ctas = nblk * pb.batch;
     auto go = [&](auto fwd, auto bwd) {
         ensure_dynamic_smem(reinterpret_cast<const void*>(fwd), smem);
         ensure_dynamic_smem(reinterpret_cast<const void*>(bwd), smem);
-        FDS_LAUNCH(fwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ks, pb.ipiv, pflag, rhs,
-                   rstride, ws.ybuf, ffl, tk);
+        FDS_LAUNCH(fwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k1, ks, pb.ipiv, pflag,
+                   rhs, rstride, ws.ybuf, ffl, tk);
         FDS_LAUNCH(bwd, ctas, kDfThreads, smem, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, ws.ybuf, rhs, rstride, bfl,
                    tk + 1);
     };

@@ -40,6 +40,7 @@ struct LuWorkspace {
     // were factored as 128-column super-panels (LAPACK order inside each), the
     // rest as nb-column panels; LINPACK order across groups
     int super_end = 0;
+    int super256_end = 0;  // columns [0, super256_end) were factored as 256-column super-panels
     // dataflow solve: forward results [batch][n], per-panel pivot flags, block flags, tickets
     cplx* ybuf = nullptr;
     size_t ybuf_cap = 0;

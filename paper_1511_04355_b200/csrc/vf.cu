@@ -628,6 +628,7 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int s = i % ST;
             if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
+            fds_jitter(i);
             const int k0 = t * kRtTile;
             const unsigned bytes = static_cast<unsigned>(min(kRtTile, K - k0)) * 16u;
             if (lane == 0) mbar_expect_tx(&full[s], bytes * J);
@@ -671,6 +672,7 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
                 for (int nt = 0; nt < 4; ++nt) dmma_v(acc[nt][0], acc[nt][1], fa[st], fb[nt]);
             }
         }
+        fds_jitter(i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
