@@ -150,13 +150,15 @@ def test_bem_create_validates_on_the_host(case):
 
 
 def test_default_3m_gemm_kernel_is_tma_fed_dmma():
-    """The default trailing update (lu_gemm3m_tma_kernel<128, 32, 4, 2>) issues
-    only DMMA for its products (no FP64 adds in the k-loop: the operand sums come
-    from lu_g3_prep_kernel) and is fed by TMA tensor loads."""
-    fn = "_ZN4fdsb20lu_gemm3m_tma_kernelILi128ELi32ELi4ELi2ELi256EEEv14CUtensorMap_stS1_S1_S1_Pdmmiiii"
+    """The default trailing update (lu_gemm3m_tma_kernel<128, 32, 4, 2, 256, 1>)
+    issues only DMMA for its products (no FP64 adds in the k-loop: the operand
+    sums come from lu_g3_prep_kernel) and is fed by TMA tensor loads."""
+    fn = "_ZN4fdsb20lu_gemm3m_tma_kernelILi128ELi32ELi4ELi2ELi256ELi1EEEv14CUtensorMap_stS1_S1_S1_Pdmmiiii"
     out = subprocess.run(["cuobjdump", "-sass", "-fun", fn, str(P.library_path())], capture_output=True,
                          text=True).stdout
     assert "UTMALDG" in out
     n_dmma = out.count("DMMA.8x8x4")
-    assert n_dmma == 3 * 4 * 2 * 2  # 3 products x 4 k-steps x (MI = 2) x (NI = 2) per unrolled k-chunk
+    # 3 products x 4 k-steps x (MI = 2) x (NI = 2) per unrolled k-chunk, twice: the
+    # steady-state chunk and the P-first first chunk (P alone, then Q and R)
+    assert n_dmma == 2 * 3 * 4 * 2 * 2
     assert out.count("DADD") <= 2 * 2 * 2 * 2  # epilogue only: Q - P, R - P per accumulator pair
