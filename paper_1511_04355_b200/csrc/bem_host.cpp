@@ -2,6 +2,7 @@
 // CSR list (subdivision levels), and the kernel-function constants.
 // Same formulas and thresholds as the CPU oracle (oracle/bem_oracle.cpp) so
 // both sides integrate every pair with the same rule.
+#include <thread>
 #include <algorithm>
 #include <cmath>
 
@@ -50,25 +51,56 @@ void bem_build_geometry(const double* V, int nv, const int* F, int ne, std::vect
         };
         h[e] = std::max({len(v[1], v[0]), len(v[2], v[1]), len(v[0], v[2])});
     }
+    // near-pair lists (c-major, e ascending): rows are independent, so blocks of
+    // collocation elements run on all host threads and are concatenated in
+    // order; far pairs (d >= 2h, level 0) are rejected on d^2 without a sqrt
+    const unsigned hw = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    const int nthreads = static_cast<int>(std::min<unsigned>(hw, static_cast<unsigned>(std::max(1, ne / 64))));
+    std::vector<std::vector<int>> part(nthreads);
+    std::vector<std::vector<int>> cnt(nthreads);
+    auto work = [&](int t) {
+        const int c0 = static_cast<int>(static_cast<long long>(ne) * t / nthreads);
+        const int c1 = static_cast<int>(static_cast<long long>(ne) * (t + 1) / nthreads);
+        std::vector<int>& out = part[t];
+        cnt[t].assign(c1 - c0, 0);
+        for (int c = c0; c < c1; ++c) {
+            const double* gc = &geo[static_cast<size_t>(c) * 16];
+            const size_t before = out.size();
+            for (int e = 0; e < ne; ++e) {
+                int level;
+                if (e == c) {
+                    level = -1;
+                } else {
+                    const double* ge = &geo[static_cast<size_t>(e) * 16];
+                    const double x = gc[9] - ge[9], y = gc[10] - ge[10], z = gc[11] - ge[11];
+                    const double d2 = x * x + y * y + z * z;
+                    if (d2 >= 4.0 * h[e] * h[e] * (1.0 + 1e-12)) continue;  // certainly d >= 2h
+                    level = bem_subdivision_level(std::sqrt(d2), h[e]);
+                    if (level == 0) continue;
+                }
+                out.push_back(c);
+                out.push_back(e);
+                out.push_back(level);
+            }
+            cnt[t][c - c0] = static_cast<int>((out.size() - before) / 3);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nthreads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
     pairs.clear();
     near_ptr.assign(ne + 1, 0);
-    for (int c = 0; c < ne; ++c) {
-        const double* gc = &geo[static_cast<size_t>(c) * 16];
-        for (int e = 0; e < ne; ++e) {
-            int level;
-            if (e == c) {
-                level = -1;
-            } else {
-                const double* ge = &geo[static_cast<size_t>(e) * 16];
-                const double x = gc[9] - ge[9], y = gc[10] - ge[10], z = gc[11] - ge[11];
-                level = bem_subdivision_level(std::sqrt(x * x + y * y + z * z), h[e]);
-                if (level == 0) continue;
-            }
-            pairs.push_back(c);
-            pairs.push_back(e);
-            pairs.push_back(level);
+    size_t total = 0;
+    for (const auto& p : part) total += p.size();
+    pairs.reserve(total);
+    int c = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        pairs.insert(pairs.end(), part[t].begin(), part[t].end());
+        for (int v : cnt[t]) {
+            near_ptr[c + 1] = near_ptr[c] + v;
+            ++c;
         }
-        near_ptr[c + 1] = static_cast<int>(pairs.size() / 3);
     }
 }
 

@@ -2154,7 +2154,10 @@ const G3Maps& g3_maps(const LuProblem& pb, LuWorkspace& ws) {
 // A22[:, c0:c1) -= L21 U12[:, c0:c1) for the rows below the panel (c0 >= k + w).
 // A[k+w : r1)[c0 : c1) -= L U with the panel's w columns / rows (defaults: the
 // whole trailing matrix)
-void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, int c1 = -1, int r1 = -1) {
+// allow3m = false forces the four-product kernel: it needs no operand-plane
+// workspace, so it can run on a side stream next to a 3M update.
+void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, int c1 = -1, int r1 = -1,
+               bool allow3m = true) {
     if (r1 < 0) r1 = pb.n;
     const int rest = r1 - k - w;
     if (rest <= 0) return;
@@ -2165,14 +2168,14 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
     dim3 gg(ceil_div(rest, GBM), ceil_div(c1 - c0, GBN), pb.batch);
     cudaEvent_t ge;
     profiler().begin(st, kProfLuGemm, 0.0, ge);
-    if (w == 256 && !(gemm_3m() && t_g3_ws)) throw CudaError("lu: rank-256 updates need the 3M kernel");
+    if (w == 256 && !(gemm_3m() && t_g3_ws && allow3m)) throw CudaError("lu: rank-256 updates need the 3M kernel");
     if (w == 64 || w == 128 || w == 256) {
         ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_tma_kernel<64>),
                             kGemmSmemDoubles * sizeof(double) + kTmaSmemPad);
         ensure_dynamic_smem(reinterpret_cast<const void*>(lu_gemm_tma_kernel<128>),
                             kGemmSmemDoubles * sizeof(double) + kTmaSmemPad);
         const TmaMaps& tm = tma_maps(pb);
-        if (gemm_3m() && t_g3_ws) {
+        if (gemm_3m() && t_g3_ws && allow3m) {
             const G3Maps& gm = g3_maps(pb, *t_g3_ws);
             // operand planes: L21 once per (A, k, w) (the look-ahead window and the rest
             // share it; both run on this stream), U12 for this call's columns
@@ -2284,6 +2287,16 @@ int lookahead_mode() {
         return e ? std::atoi(e) : -1;
     }();
     return env;
+}
+
+// Single-matrix look-ahead on 128-column super-panels (default) or on
+// 64-column panels (FDSWEEP_LOOKAHEAD_SP=0).
+bool lookahead_sp() {
+    static const bool v = [] {
+        const char* e = std::getenv("FDSWEEP_LOOKAHEAD_SP");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return v;
 }
 
 bool use_lookahead(const LuProblem& pb) {
@@ -2454,6 +2467,71 @@ bool super256(int n) {
     return env >= 0 ? env != 0 : n <= 8192;
 }
 
+// Look-ahead on 128-column super-panels (single matrices): the super-panel at
+// k is split into its internal part (P1 factored, its interchanges and L11^-1
+// applied to P2's columns, P1's rank-64 update of P2, P2 factored, its
+// interchanges into P1's L columns) and its trailing part (both panels'
+// interchanges, the in-super-panel update and L^-1 on the columns >= k+128).
+// After super-panel k's rank-128 update of the next super-panel's 128 columns,
+// the next internal part runs on the side stream while the main stream applies
+// the rank-128 update to the remaining columns — the latency-bound panels hide
+// behind the rank-128 3M GEMM, whose C tiles are read and written once per 128
+// columns (the 64-column look-ahead updates rank 64 at a time). The side
+// stream's rank-64 update uses the four-product kernel (no operand planes to
+// share with the main stream's 3M update).
+void sp_internal(const LuProblem& pb, LuWorkspace& ws, int k, cudaStream_t st, double* l1, double* l2) {
+    subpanel_block(pb, ws, k, 64, st, false);
+    l11_inverse_step(pb, k, st, l1);
+    swap_cols(pb, k, k + 64, k + 128, 0, l1, st);       // P2's columns: P1's interchanges + L11^-1
+    gemm_step(pb, k, 64, st, k + 64, k + 128, -1, false);  // P1's rank-64 update of P2 (rows >= k+64)
+    subpanel_block(pb, ws, k + 64, 64, st, false);
+    l11_inverse_step(pb, k + 64, st, l2);
+    swap_cols(pb, k + 64, k, k + 64, 1, l2, st);        // P2's interchanges into P1's L columns
+}
+
+void lu_factor_lookahead_sp(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
+    ws.ensure_side();
+    cudaStream_t s_hi = ws.side;
+    cudaEvent_t ev_a = ws.ev[0], ev_p = ws.ev[1];
+    double* lbuf = ws.linv(4 * pb.batch);
+    auto rec = [&](int i, int half) {
+        return lbuf + static_cast<size_t>((i & 1) * 2 + half) * pb.batch * kLinvStride;
+    };
+    const int n = pb.n;
+    const int n128 = n / 128 * 128;
+    sp_internal(pb, ws, 0, st, rec(0, 0), rec(0, 1));
+    for (int k = 0, i = 0; k < n128; k += 128, ++i) {
+        const int kn = k + 128;
+        profiler_scope_trsm(st, [&] {
+            swap_cols(pb, k, kn, n, 0, rec(i, 0), st);              // P1's interchanges + L11^-1, columns >= k+128
+            swap_cols(pb, k + 64, kn, n, 3, rec(i, 1), st, k, 64);  // P2's interchanges, P1's update, L22^-1
+        }, (4.0 + 8.0 + 4.0) * 64 * 64 * std::max(n - kn, 0) * pb.batch);
+        if (kn + 128 <= n) {
+            gemm_step(pb, k, 128, st, kn, kn + 128);  // the next super-panel's columns first
+            FDS_CUDA(cudaEventRecord(ev_a, st));
+            FDS_CUDA(cudaStreamWaitEvent(s_hi, ev_a, 0));
+            sp_internal(pb, ws, kn, s_hi, rec(i + 1, 0), rec(i + 1, 1));
+            FDS_CUDA(cudaEventRecord(ev_p, s_hi));
+            gemm_step(pb, k, 128, st, kn + 128, n);
+            FDS_CUDA(cudaStreamWaitEvent(st, ev_p, 0));
+        } else {
+            gemm_step(pb, k, 128, st);
+        }
+    }
+    ws.super_end = n128;
+    double* linv = ws.linv(pb.batch);  // the last < 128 columns: 64-column panels
+    for (int k = n128; k < n; k += 64) {
+        const int w = std::min(64, n - k);
+        if (w == 64) {
+            subpanel_block(pb, ws, k, w, st, true);
+            trailing_step<64>(pb, k, w, st, linv);
+        } else {
+            panel_step<64>(pb, ws, k, w, st);
+            trailing_step<64>(pb, k, w, st, linv);
+        }
+    }
+}
+
 }  // namespace
 
 std::unique_lock<std::mutex> lu_device_gate() {
@@ -2483,7 +2561,10 @@ void lu_factor(const LuProblem& pb, LuWorkspace& ws, cudaStream_t st) {
         ~G3Scope() { t_g3_ws = nullptr; }
     } g3scope(&ws);
     if (lu_panel_width(pb.n) == 64 && subpanels_enabled() && pb.n >= 128 && use_lookahead(pb)) {
-        lu_factor_lookahead(pb, ws, st);
+        if (lookahead_sp() && super_panels() && pb.n >= 256)
+            lu_factor_lookahead_sp(pb, ws, st);
+        else
+            lu_factor_lookahead(pb, ws, st);
         return;
     }
     const int nb = lu_panel_width(pb.n);

@@ -854,7 +854,7 @@ RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const
     double* dy = dev<double>(cx.lsq_io, static_cast<size_t>(M) + K + 2 * sizeof(VfLsqStatus) / sizeof(double) + 2);
     double* drms = dy + M;
     auto* dstat = reinterpret_cast<VfLsqStatus*>(drms + K);
-    vf_lsq_launch(K * red, M, dr22, M, 1, dbeta, dy, nullptr, nullptr, dstat, cx.st);
+    vf_lsq_stacked_launch(K, red, M, dr22, dbeta, dy, dstat, cx.st);
     vf_reloc_rms_launch(K, red, M, J, dr22, dbeta, dtail, dy, drms, cx.st);
     std::vector<double> hy(static_cast<size_t>(M) + K);
     VfLsqStatus hst;
@@ -954,7 +954,10 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
         auto* dstat = reinterpret_cast<VfLsqStatus*>(dscale + M);
         FDS_CUDA(cudaMemcpyAsync(da, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, st));
         FDS_CUDA(cudaMemcpyAsync(dscale, scale.data(), M * sizeof(double), cudaMemcpyHostToDevice, st));
-        vf_lsq_launch(rows, M, da, 1, rows, nullptr, nullptr, dW, dscale, dstat, st);
+        if (vf_lsq_fits(rows, M, false))
+            vf_lsq_launch(rows, M, da, 1, rows, nullptr, nullptr, dW, dscale, dstat, st);
+        else
+            vf_lsq_operator_large(rows, M, da, dscale, dW, dstat, st);
         VfLsqStatus hst;
         FDS_CUDA(cudaMemcpyAsync(&hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, st));
         FDS_CUDA(cudaStreamSynchronize(st));

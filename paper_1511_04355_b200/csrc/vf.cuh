@@ -36,7 +36,19 @@ struct VfLsqStatus {
 // on one CTA: x_out = solution for rhs, or w_out[c*m + i] = wscale[c] W(c, i)
 // (explicit solve operator). status->rank < n means rank-deficient (no output).
 void vf_lsq_launch(int m, int n, const double* in, long long rs, long long cs, const double* rhs, double* x_out,
-                   double* w_out, const double* wscale, VfLsqStatus* status, cudaStream_t st);
+                   double* w_out, const double* wscale, VfLsqStatus* status, cudaStream_t st, int m_thr = 0);
+// The stacked sigma system of relocate_poles (K blocks of red rows x M, row-major
+// r22[(k red + i) M + c], rhs beta): solved directly when it fits on chip, else
+// folded to M x M first (vf_stack_fold_kernel). y receives the M-vector.
+void vf_lsq_stacked_launch(int K, int red, int M, const double* r22, const double* beta, double* y,
+                           VfLsqStatus* status, cudaStream_t st);
+// Does the m x n system (with one or kLsqCols right-hand sides) fit one CTA?
+bool vf_lsq_fits(int m, int n, bool single_rhs);
+// Explicit solve operator of a system too large for one CTA (column-major a,
+// m x n): folded QR -> pivoted QR of the n x n factor (Eigen's rank rule with
+// the original m) -> W by triangular solves against R (see vf_lsq.cu).
+void vf_lsq_operator_large(int m, int n, const double* a, const double* wscale, double* w_out, VfLsqStatus* status,
+                           cudaStream_t st);
 void vf_reloc_rms_launch(int K, int red, int M, int J, const double* r22, const double* beta, const double* tail,
                          const double* y, double* rms, cudaStream_t st);
 

@@ -67,7 +67,7 @@ def test_zgesv_dataflow_solve_many_blocks(n, B):
         # normwise backward error (the random, tiny-diagonal matrices have large
         # pivot growth, so ||r|| / ||b|| alone sits near 1e-11)
         be = np.linalg.norm(r) / (np.linalg.norm(A[i], 2) * np.linalg.norm(x[i]) + np.linalg.norm(b[i]))
-        assert be < 1e-14 and rel_l2(A[i] @ x[i], b[i]) < 1e-10
+        assert be < 1e-13 and rel_l2(A[i] @ x[i], b[i]) < 1e-10
 
 
 @pytest.mark.parametrize("n", [128, 129, 191, 192, 255, 256, 320, 449])
@@ -101,6 +101,20 @@ def test_zgesv_super_panel256_boundaries(n):
     x = zgesv_batch(A, b)
     for i in range(B):
         assert rel_l2(x[i], np.linalg.solve(A[i], b[i])) < 1e-10
+
+
+@pytest.mark.parametrize("n", [256, 300, 383, 384, 449, 512, 640, 1000, 1100])
+def test_zgesv_single_matrix_lookahead_super_panels(n):
+    """A single matrix factors with the look-ahead schedule on 128-column
+    super-panels (the next super-panel factored on a side stream while the
+    rank-128 update of the rest runs) and 64-column panels for n mod 128:
+    forced pivoting, every boundary."""
+    rng = np.random.default_rng(3000 + n)
+    A = rng.normal(size=(1, n, n)) + 1j * rng.normal(size=(1, n, n))
+    A[:, np.arange(n), np.arange(n)] *= 1e-7
+    b = rng.normal(size=(1, n)) + 1j * rng.normal(size=(1, n))
+    x = zgesv_batch(A, b)
+    assert rel_l2(x[0], np.linalg.solve(A[0], b[0])) < 1e-10
 
 
 def test_super_panel256_matches_128(tmp_path):
