@@ -2302,11 +2302,12 @@ bool lookahead_sp() {
 bool use_lookahead(const LuProblem& pb) {
     const int env = lookahead_mode();
     if (env >= 0) return env != 0;
-    // measured: single N = 15360 399 -> 368 ms; N = 36864 4.33 -> 4.45 s (the
-    // panel share is small there and the co-running panel costs GEMM slots);
-    // batched N = 3840 x 129 697 -> 731 ms. With the 3M update: N = 15360
-    // 326 -> 306 ms with look-ahead, N = 36864 3.88 -> 4.07 s (kept off)
-    return pb.batch == 1 && pb.n <= 24576;
+    // single matrices. Measured: 64-column look-ahead, N = 15360 399 -> 368 ms
+    // (326 -> 306 ms with the 3M update) but N = 36864 3.88 -> 4.07 s, so it
+    // stopped at N <= 24576; the super-panel look-ahead (lookahead_sp) takes
+    // N = 15360 from 305 to 278 ms and N = 36864 from 3.88 to 3.80 s.
+    if (pb.batch != 1) return false;
+    return lookahead_sp() || pb.n <= 24576;
 }
 
 // Look-ahead: the trailing update of step k is split into the next panel's
@@ -2376,6 +2377,7 @@ void swap_cols(const LuProblem& pb, int k, int cb, int ce, int mode, const doubl
                int rlen = 64) {
     if (ce <= cb) return;
     const size_t asmem = (2 * 64 * SAS + 2 * kApplyCols * SAS) * sizeof(double);
+    ensure_dynamic_smem(reinterpret_cast<const void*>(lu_swap_apply_kernel), asmem);
     FDS_LAUNCH(lu_swap_apply_kernel, dim3(ceil_div(ce - cb, kApplyCols), pb.batch), kApplyThreads, asmem, st, pb.A,
                pb.mstride, pb.plane, pb.n, pb.ld, k, linv, cb, ce, mode, kp, rlen);
 }
