@@ -651,27 +651,6 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
         fa[st] = (mrow < M && q < Q) ? W[static_cast<size_t>(mrow) * Q + q] : 0.0;
     }
     const int steps = (J + 1) / 2;
-    // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
-    // the partner row sits 4 lanes away in the accumulator fragment
-    auto store = [&](const double (&v)[4][2], int k0) {
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double x = v[nt][e];
-                const double y = __shfl_xor_sync(0xffffffffu, x, 4);
-                const int k = k0 + nt * 8 + 2 * q_l + e;
-                if (mrow >= M || k >= K || (heads && mrow < 2 * P && (mrow & 1))) continue;
-                cplx r;
-                if (mrow < 2 * P) r = (mrow % 2 == 0) ? mk(x, y) : mk(y, -x);
-                else r = mk(x, 0.0);
-                __stcs(reinterpret_cast<double2*>(res) + static_cast<size_t>(mrow) * K + k, make_double2(r.re, r.im));
-            }
-    };
-    // the previous tile's stores are issued in the middle of the current tile's
-    // DMMA chain, so the warps' epilogues no longer idle the tensor pipe together
-    double prev[4][2];
-    int prev_k0 = -1;
     int i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int s = i % ST;
@@ -692,19 +671,27 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) dmma_v(acc[nt][0], acc[nt][1], fa[st], fb[nt]);
             }
-            if (st == 2 && prev_k0 >= 0) store(prev, prev_k0);
         }
         fds_jitter(i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+        // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
+        // the partner row sits 4 lanes away in the accumulator fragment
+        const int k0 = t * kRtTile + half * 32;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-            prev[nt][0] = acc[nt][0];
-            prev[nt][1] = acc[nt][1];
-        }
-        prev_k0 = t * kRtTile + half * 32;
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double x = acc[nt][e];
+                const double y = __shfl_xor_sync(0xffffffffu, x, 4);
+                const int k = k0 + nt * 8 + 2 * q_l + e;
+                if (mrow >= M || k >= K || (heads && mrow < 2 * P && (mrow & 1))) continue;
+                cplx r;
+                if (mrow < 2 * P) r = (mrow % 2 == 0) ? mk(x, y) : mk(y, -x);
+                else r = mk(x, 0.0);
+                __stcs(reinterpret_cast<double2*>(res) + static_cast<size_t>(mrow) * K + k, make_double2(r.re, r.im));
+            }
     }
-    if (prev_k0 >= 0) store(prev, prev_k0);
 }
 
 // out[g*K + k] = sum_m res[k*M + m] / (s_g - a_m) (vecfit.cpp:490-509); *hit is
