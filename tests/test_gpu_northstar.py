@@ -180,3 +180,21 @@ def test_afs_reference_defaults_failure_mode_pressurised_sphere():
     first = int(diff[0]) if len(diff) else po["n_c"]
     print(f"identical leading samples: {first} of {po['n_c']}; differing: {len(diff)}")
     assert first >= 16 + 100
+
+
+def test_cfg3_solution_matches_oracle_n36864():
+    """configs[2] at full size: the unit-cube cavity (12288 triangles, N = 36864,
+    21.7 GB per matrix) solved by the single-matrix look-ahead LU against the
+    oracle's assembly + OpenBLAS zgetrf/zgetrs on the host (~2 min on 16 cores),
+    rel-L2 < 1e-9."""
+    V, F = mesh.cube_cavity(32)
+    tr = mesh.pressure_traction(V, F)
+    s = contour(7)
+    gpu = P.BemSystem(V, F, tr, max_batch=1)
+    u = gpu.evaluate(s)
+    gpu.close()
+    orc = O.Bem(V, F, tr)
+    uo, t = orc.solve_openblas(s, O.openblas_path())
+    e = rel_l2(u, uo)
+    print(f"cfg3 N=36864 rel-L2 vs oracle: {e:.2e} (oracle assembly {t[0]:.1f} s, zgetrf+zgetrs {t[1]:.1f} s)")
+    assert e < 1e-9
