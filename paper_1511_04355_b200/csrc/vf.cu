@@ -592,20 +592,25 @@ __global__ void vf_gather_channels_kernel(int K, int M, int KT, const cplx* __re
 }
 
 // identify_residues apply, bulk-copy fed (default for J <= 64, M <= 64 per
-// slice): X (M x K) = W (M x 2J) B (2J x K). One persistent CTA per SM walks
-// 64-channel tiles; a producer warp streams each tile's J value rows (1 KB
-// contiguous runs of values[j][k0..k0+63]) into a ST-deep shared-memory ring
-// with cp.async.bulk (mbarrier transaction counts, no registers spent on the
-// copy); 2*MT consumer warps each own one 8-pole m-tile of W — its A fragments
-// for all steps live in registers for the whole kernel — and one 32-channel
-// half of the tile, reading B fragments from the ring (row stride 136 doubles:
-// the two value rows a fragment spans land 16 banks apart).
+// slice): X (M x K) = W (M x 2J) B (2J x K), computed transposed as
+// X^T = B^T W^T. One persistent CTA per SM walks 64-channel tiles; a producer
+// warp streams each tile's J value rows (1 KB contiguous runs of
+// values[j][k0..k0+63]) into a ST-deep shared-memory ring with cp.async.bulk
+// (mbarrier transaction counts, no registers spent on the copy); 2*MT consumer
+// warps each own one 8-pole m-tile of W — its fragments for all steps live in
+// registers for the whole kernel — and one 32-channel half of the tile, reading
+// value fragments from the ring (row stride 136 doubles: the two value rows a
+// fragment spans land 16 banks apart). With channels as the DMMA's M side, a
+// lane's two accumulators are poles 2 q, 2 q + 1 of one channel: both halves of
+// a conjugate pair, packed without shuffles. Step counts divisible by four run
+// as branch-free groups of four k-steps (16 DMMAs per group).
 constexpr int kRtTile = 64;        // channels per tile
 constexpr int kRtRow = 2 * kRtTile + 8;  // doubles per staged value row
 template <int MT, int SP, int ST>
 __global__ void __launch_bounds__(32 + 64 * MT, 1)
 vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals, const double* __restrict__ W,
                       cplx* __restrict__ res, int heads) {
+    static_assert(SP % 4 == 0, "step capacity in groups of four");
     extern __shared__ double rtm_raw[];
     double* ring = rtm_raw;
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(ST) * J * kRtRow);
@@ -642,15 +647,19 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
     const int cw = warp - 1, mt = cw >> 1, half = cw & 1;
     const int q_l = lane & 3, n_l = lane >> 2;
     const int j0 = q_l >> 1, part = q_l & 1;
-    // A fragments of this warp's m-tile for every step: W[m][4 st + q_l] (zero padded)
-    double fa[SP];
-    const int mrow = m0 + mt * 8 + n_l;
+    // W fragments of this warp's m-tile for every step: W[m][4 st + q_l] (zero padded)
+    double fw[SP];
+    {
+        const int mrow = m0 + mt * 8 + n_l;
 #pragma unroll
-    for (int st = 0; st < SP; ++st) {
-        const int q = 4 * st + q_l;
-        fa[st] = (mrow < M && q < Q) ? W[static_cast<size_t>(mrow) * Q + q] : 0.0;
+        for (int st = 0; st < SP; ++st) {
+            const int q = 4 * st + q_l;
+            fw[st] = (mrow < M && q < Q) ? W[static_cast<size_t>(mrow) * Q + q] : 0.0;
+        }
     }
     const int steps = (J + 1) / 2;
+    const bool grouped = steps % 4 == 0;
+    const int mb = m0 + mt * 8 + 2 * q_l;  // this lane's pole rows mb, mb + 1
     int i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int s = i % ST;
@@ -659,38 +668,58 @@ vf_residue_tma_kernel(int J, int K, int M, int P, const cplx* __restrict__ vals,
         double acc[4][2];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+        // value fragment of step st, channel group nt: row 2 st + j0 (the odd-J tail
+        // row meets zero W columns; clamp the read)
+        if (grouped) {
 #pragma unroll
-        for (int st = 0; st < SP; ++st) {
-            if (st < steps) {
-                // value row 2 st + j0 (the odd-J tail row meets zero A columns; clamp the read)
-                const int row = min(2 * st + j0, J - 1);
-                const double* b = st_base + row * kRtRow;
-                double fb[4];
+            for (int g = 0; g < SP / 4; ++g) {
+                if (4 * g < steps) {
+                    double fv[4][4];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) fb[nt] = b[nt * 16];
+                    for (int u = 0; u < 4; ++u) {
+                        const double* b = st_base + (2 * (4 * g + u) + j0) * kRtRow;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) dmma_v(acc[nt][0], acc[nt][1], fa[st], fb[nt]);
+                        for (int nt = 0; nt < 4; ++nt) fv[u][nt] = b[nt * 16];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) dmma_v(acc[nt][0], acc[nt][1], fv[u][nt], fw[4 * g + u]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int st = 0; st < SP; ++st) {
+                if (st < steps) {
+                    const double* b = st_base + min(2 * st + j0, J - 1) * kRtRow;
+                    double fv[4];
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) fv[nt] = b[nt * 16];
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma_v(acc[nt][0], acc[nt][1], fv[nt], fw[st]);
+                }
             }
         }
         fds_jitter(i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        // canonical packing: rows m (even, < 2P) and m+1 form one conjugate pair;
-        // the partner row sits 4 lanes away in the accumulator fragment
+        // canonical packing: rows m (even, < 2P) and m + 1 form one conjugate pair
+        // (m + 1 holds the conjugate); rows >= 2P are real poles
         const int k0 = t * kRtTile + half * 32;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double x = acc[nt][e];
-                const double y = __shfl_xor_sync(0xffffffffu, x, 4);
-                const int k = k0 + nt * 8 + 2 * q_l + e;
-                if (mrow >= M || k >= K || (heads && mrow < 2 * P && (mrow & 1))) continue;
-                cplx r;
-                if (mrow < 2 * P) r = (mrow % 2 == 0) ? mk(x, y) : mk(y, -x);
-                else r = mk(x, 0.0);
-                __stcs(reinterpret_cast<double2*>(res) + static_cast<size_t>(mrow) * K + k, make_double2(r.re, r.im));
+        for (int nt = 0; nt < 4; ++nt) {
+            const int k = k0 + nt * 8 + n_l;
+            if (k >= K) continue;
+            const double x = acc[nt][0], y = acc[nt][1];
+            double2* dst = reinterpret_cast<double2*>(res) + static_cast<size_t>(mb) * K + k;
+            if (mb < 2 * P) {
+                __stcs(dst, make_double2(x, y));
+                if (!heads) __stcs(dst + K, make_double2(x, -y));
+            } else {
+                if (mb < M) __stcs(dst, make_double2(x, 0.0));
+                if (mb + 1 < M) __stcs(dst + K, make_double2(y, 0.0));
             }
+        }
     }
 }
 

@@ -7,3 +7,4 @@ import bench  # noqa: E402
 
 r = bench.cfg5_vf_fsm(reps=3)
 print(r["api_ms"], r["kernel_ms"])
+print({k: v for k, v in r["residue_heads"].items() if k != "note"})
