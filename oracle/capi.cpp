@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "bem_oracle.hpp"
@@ -101,6 +102,33 @@ class OracleBemSystem : public fdsweep::FrequencySystem {
   private:
     std::shared_ptr<oracle::BemOracle> bem_;
     std::vector<int> dofs_;
+    fdsweep::SystemDescriptor desc_;
+};
+
+// A FrequencySystem whose evaluate() calls back into the test harness, so the
+// reference's own run_afs (afs.cpp, compiled unmodified) can be driven by
+// responses produced elsewhere (the GPU product's solves) at sizes where the
+// oracle BEM is too slow. evaluate() is serialised: the callback may hold a GIL.
+using orc_eval_cb = int (*)(void* ctx, double sr, double si, double* out);
+class OracleCallbackSystem : public fdsweep::FrequencySystem {
+  public:
+    OracleCallbackSystem(int channels, orc_eval_cb cb, void* ctx) : cb_(cb), ctx_(ctx) {
+        desc_.channel_count = channels;
+        for (int k = 0; k < channels; ++k) desc_.channel_labels.push_back("c" + std::to_string(k));
+    }
+    const fdsweep::SystemDescriptor& descriptor() const override { return desc_; }
+    std::vector<Complex> evaluate(Complex s) const override {
+        std::vector<Complex> out(static_cast<size_t>(desc_.channel_count));
+        std::lock_guard<std::mutex> lk(mu_);
+        if (cb_(ctx_, s.real(), s.imag(), reinterpret_cast<double*>(out.data())) != 0)
+            throw fdsweep::NumericError("callback system: evaluate failed");
+        return out;
+    }
+
+  private:
+    orc_eval_cb cb_;
+    void* ctx_;
+    mutable std::mutex mu_;
     fdsweep::SystemDescriptor desc_;
 };
 
@@ -359,6 +387,13 @@ int orc_system_bem(void* bem, int n_dofs, const int* dofs, void** out) {
         auto h = new OracleSystem;
         auto sp = std::shared_ptr<oracle::BemOracle>(static_cast<oracle::BemOracle*>(bem), [](oracle::BemOracle*) {});
         h->sys = std::make_unique<OracleBemSystem>(sp, std::vector<int>(dofs, dofs + n_dofs));
+        *out = h;
+    });
+}
+int orc_system_callback(int channels, orc_eval_cb cb, void* ctx, void** out) {
+    return guarded([&] {
+        auto h = new OracleSystem;
+        h->sys = std::make_unique<OracleCallbackSystem>(channels, cb, ctx);
         *out = h;
     });
 }

@@ -298,6 +298,28 @@ class System:
         s._keep = bem
         return s
 
+    @classmethod
+    def callback(cls, channels, fn):
+        """A system whose evaluate(s) returns fn(s) (a length-`channels` complex
+        vector): lets the reference run_afs run on responses computed elsewhere."""
+        proto = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                 ctypes.POINTER(ctypes.c_double))
+
+        def tramp(_ctx, sr, si, out):
+            try:
+                v = np.ascontiguousarray(fn(complex(sr, si)), np.complex128)
+                ctypes.memmove(out, v.ctypes.data, 16 * channels)
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a NumericError by the oracle
+                return 1
+
+        cb = proto(tramp)
+        h = ctypes.c_void_p()
+        call("orc_system_callback", int(channels), cb, None, ctypes.byref(h))
+        s = cls(h.value)
+        s._keep = cb
+        return s
+
     @property
     def channels(self):
         return lib().orc_system_channels(self.h)

@@ -734,8 +734,8 @@ lu_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 // tiles (2 CTAs/SM) — or 64 wide at 1 CTA/SM. Error: normwise like ZGEMM
 // (Higham, "Stability of a method for multiplying complex matrices with three
 // real matrix multiplications"), componentwise slightly weaker in Im.
-template <int BN>
-constexpr int g3_smem_doubles() { return GSTAGES * 3 * (GBK * GAS + BN * GBS); }
+template <int BN, int KC = GBK, int NS = GSTAGES>
+constexpr int g3_smem_doubles() { return NS * 3 * (KC * GAS + BN * (KC + 4)); }
 
 // Operand planes of one trailing update, formed once per (panel, matrix) so the
 // GEMM's inner loop is DMMA-only (FP64 adds there contend with DMMA for the
@@ -767,20 +767,29 @@ __global__ void lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, 
     }
 }
 
-template <int W, int BN, int WGM, int MINB, int NT = kGemmThreads, int PFIRST = 0>
+// Fragment mapping: a lane's two row fragments are rows 2j, 2j+1 of its warp's
+// 16 (j = lane / 4), so A fragments arrive by one 16-byte LDS and the C tile
+// moves in 16-byte accesses (a store instruction writes whole 128-byte lines).
+// (Measured: 16-byte B fragments through a permuted k order inside the chunk,
+// 8 instead of 12 shared loads per pass and chunk, gave no gain.)
+template <int W, int BN, int WGM, int MINB, int NT = kGemmThreads, int PFIRST = 0, int KC = GBK, int NS = GSTAGES>
 __global__ void __launch_bounds__(NT, MINB)
 lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmU, double* A,
                      size_t mstride, size_t plane, int n, int ld, int k, int c0) {
     constexpr int WGN = (NT / 32) / WGM;
     constexpr int MI = GBM / WGM / 8, NI = BN / WGN / 8;
-    constexpr int nk = W / GBK;
-    constexpr unsigned kStageBytes = 3u * (GBK * GAS + BN * GBS) * sizeof(double);
+    static_assert(MI == 2, "row-pair fragments");
+    // KC-deep k-chunks in an NS-stage ring (measured: KC = 8 with 4 or 5 stages,
+    // more latency slack but twice the per-chunk hand-offs, 6.5-9 % slower)
+    constexpr int AS = GAS, BS = KC + 4;  // KC + 4: conflict-free 8-byte B fragments for KC = 8, 16
+    constexpr int nk = W / KC;
+    constexpr unsigned kStageBytes = 3u * (KC * AS + BN * BS) * sizeof(double);
     extern __shared__ double gsm_raw[];
     const unsigned raw = static_cast<unsigned>(__cvta_generic_to_shared(gsm_raw));
     double* gsm = gsm_raw + ((128u - (raw & 127u)) & 127u) / sizeof(double);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + g3_smem_doubles<BN>());
-    unsigned* freed = reinterpret_cast<unsigned*>(bar + GSTAGES);  // per stage: warps done with it
+    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + g3_smem_doubles<BN, KC, NS>());
+    unsigned* freed = reinterpret_cast<unsigned*>(bar + NS);  // per stage: warps done with it
     const int b = blockIdx.z;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
@@ -788,12 +797,13 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int n0 = c0 + blockIdx.y * BN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp % WGM, wn = warp / WGM;
+    const int r0 = wm * (GBM / WGM) + 2 * (lane >> 2);  // this lane's row pair in the tile
     // A planes: Re L21, Re+Im, Re-Im; B planes: Re U12, Im U12, Re+Im
-    auto As = [&](int st, int pl) { return gsm + (st * 3 + pl) * (GBK * GAS); };
-    auto Bs = [&](int st, int pl) { return gsm + GSTAGES * 3 * (GBK * GAS) + (st * 3 + pl) * (BN * GBS); };
+    auto As = [&](int st, int pl) { return gsm + (st * 3 + pl) * (KC * AS); };
+    auto Bs = [&](int st, int pl) { return gsm + NS * 3 * (KC * AS) + (st * 3 + pl) * (BN * BS); };
     if (tid == 0) {
 #pragma unroll
-        for (int st = 0; st < GSTAGES; ++st) {
+        for (int st = 0; st < NS; ++st) {
             mbar_init(&bar[st], 1);
             freed[st] = 0;
         }
@@ -802,32 +812,33 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     __syncthreads();
     auto issue = [&](int st, int kc) {  // thread 0 only
         mbar_expect_tx(&bar[st], kStageBytes);
-        tma_load_3d(As(st, 0), &tmA, &bar[st], m0, k + kc * GBK, 2 * b);
-        tma_load_3d(As(st, 1), &tmL, &bar[st], m0, kc * GBK, 2 * b);
-        tma_load_3d(As(st, 2), &tmL, &bar[st], m0, kc * GBK, 2 * b + 1);
-        tma_load_3d(Bs(st, 0), &tmB, &bar[st], k + kc * GBK, n0, 2 * b);
-        tma_load_3d(Bs(st, 1), &tmB, &bar[st], k + kc * GBK, n0, 2 * b + 1);
-        tma_load_3d(Bs(st, 2), &tmU, &bar[st], kc * GBK, n0, b);
+        tma_load_3d(As(st, 0), &tmA, &bar[st], m0, k + kc * KC, 2 * b);
+        tma_load_3d(As(st, 1), &tmL, &bar[st], m0, kc * KC, 2 * b);
+        tma_load_3d(As(st, 2), &tmL, &bar[st], m0, kc * KC, 2 * b + 1);
+        tma_load_3d(Bs(st, 0), &tmB, &bar[st], k + kc * KC, n0, 2 * b);
+        tma_load_3d(Bs(st, 1), &tmB, &bar[st], k + kc * KC, n0, 2 * b + 1);
+        tma_load_3d(Bs(st, 2), &tmU, &bar[st], kc * KC, n0, b);
     };
     if (tid == 0)
-        for (int st = 0; st < GSTAGES && st < nk; ++st) issue(st, st);
+        for (int st = 0; st < NS && st < nk; ++st) issue(st, st);
     double q[MI][NI][2], r[MI][NI][2], p[MI][NI][2];
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
-        const int row = m0 + wm * (GBM / WGM) + mi * 8 + (lane >> 2);
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = n0 + wn * (BN / WGN) + ni * 8 + 2 * (lane & 3) + e;
-                const size_t gi = static_cast<size_t>(col) * ld + row;
-                q[mi][ni][e] = Are[gi];
-                r[mi][ni][e] = Aim[gi];
-                p[mi][ni][e] = 0.0;
-            }
-    }
+        for (int e = 0; e < 2; ++e) {
+            const int col = n0 + wn * (BN / WGN) + ni * 8 + 2 * (lane & 3) + e;
+            const size_t gi = static_cast<size_t>(col) * ld + m0 + r0;  // even: 16-byte aligned
+            const double2 cr = *reinterpret_cast<const double2*>(Are + gi);
+            const double2 ci = *reinterpret_cast<const double2*>(Aim + gi);
+            q[0][ni][e] = cr.x;
+            q[1][ni][e] = cr.y;
+            r[0][ni][e] = ci.x;
+            r[1][ni][e] = ci.y;
+            p[0][ni][e] = 0.0;
+            p[1][ni][e] = 0.0;
+        }
     // passes [p0, p1) of chunk kc (P: Re A x (Re+Im) B, Q: (Re+Im) A x Im B,
-    // R: (Re-Im) A x Re B), each holding only its own MI + NI fragments
+    // R: (Re-Im) A x Re B), each holding only its own fragments
     auto compute = [&](int st, int p0, int p1) {
         const double* ar = As(st, 0);
         const double* as = As(st, 1);
@@ -835,26 +846,28 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const double* br = Bs(st, 0);
         const double* bi = Bs(st, 1);
         const double* bs = Bs(st, 2);
+        const int qk = lane & 3;
 #pragma unroll
-        for (int k4 = 0; k4 < GBK; k4 += 4) {
-            const int kr = k4 + (lane & 3);
+        for (int k8 = 0; k8 < KC; k8 += 8) {
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
                 if (pass < p0 || pass >= p1) continue;
                 const double* pa = pass == 0 ? ar : (pass == 1 ? as : ad);
                 const double* pb = pass == 0 ? bs : (pass == 1 ? bi : br);
-                double fa[MI], fb[NI];
+                double(&acc)[MI][NI][2] = pass == 0 ? p : (pass == 1 ? q : r);
 #pragma unroll
-                for (int mi = 0; mi < MI; ++mi) fa[mi] = pa[kr * GAS + wm * (GBM / WGM) + mi * 8 + (lane >> 2)];
+                for (int h = 0; h < 2; ++h) {
+                    const int kr = k8 + 4 * h + qk;
+                    const double2 fa = *reinterpret_cast<const double2*>(pa + kr * AS + r0);
+                    double fb[NI];
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) fb[ni] = pb[(wn * (BN / WGN) + ni * 8 + (lane >> 2)) * GBS + kr];
-#pragma unroll
-                for (int mi = 0; mi < MI; ++mi)
+                    for (int ni = 0; ni < NI; ++ni) fb[ni] = pb[(wn * (BN / WGN) + ni * 8 + (lane >> 2)) * BS + kr];
 #pragma unroll
                     for (int ni = 0; ni < NI; ++ni) {
-                        double(&acc)[MI][NI][2] = pass == 0 ? p : (pass == 1 ? q : r);
-                        dmma(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
+                        dmma(acc[0][ni][0], acc[0][ni][1], fa.x, fb[ni]);
+                        dmma(acc[1][ni][0], acc[1][ni][1], fa.y, fb[ni]);
                     }
+                }
             }
         }
     };
@@ -862,23 +875,23 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     // C tile loads into the Q / R accumulators are still in flight
 #pragma unroll 1
     for (int kc = 0; kc < PFIRST && kc < nk; ++kc) {
-        mbar_wait(&bar[kc % GSTAGES], (kc / GSTAGES) & 1);
-        compute(kc % GSTAGES, 0, 1);
+        mbar_wait(&bar[kc % NS], (kc / NS) & 1);
+        compute(kc % NS, 0, 1);
     }
     // No CTA barrier per k-chunk: each warp's lane 0 counts itself out of a stage
     // once its fragment loads have been consumed, and the last warp out refills the
-    // stage with chunk kc + GSTAGES (fast warps never wait for slow ones).
+    // stage with chunk kc + NS (fast warps never wait for slow ones).
 #pragma unroll 1
     for (int kc = 0; kc < nk; ++kc) {
-        const int st = kc % GSTAGES;
+        const int st = kc % NS;
         if (kc < PFIRST) {
             compute(st, 1, 3);
         } else {
-            mbar_wait(&bar[st], (kc / GSTAGES) & 1);
+            mbar_wait(&bar[st], (kc / NS) & 1);
             compute(st, 0, 3);
         }
         fds_jitter(kc);
-        if (kc + GSTAGES < nk) {
+        if (kc + NS < nk) {
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
@@ -886,27 +899,27 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 if (old % (NT / 32) == NT / 32 - 1) {
                     __threadfence_block();
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    issue(st, kc + GSTAGES);
+                    issue(st, kc + NS);
                 }
             }
         }
     }
+    const int row = m0 + r0;
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
-        const int row = m0 + wm * (GBM / WGM) + mi * 8 + (lane >> 2);
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = n0 + wn * (BN / WGN) + ni * 8 + 2 * (lane & 3) + e;
-                if (row < n && col < n) {
-                    const size_t gi = static_cast<size_t>(col) * ld + row;
-                    Are[gi] = q[mi][ni][e] - p[mi][ni][e];
-                    Aim[gi] = r[mi][ni][e] - p[mi][ni][e];
-                }
+        for (int e = 0; e < 2; ++e) {
+            const int col = n0 + wn * (BN / WGN) + ni * 8 + 2 * (lane & 3) + e;
+            if (col >= n) continue;
+            const size_t gi = static_cast<size_t>(col) * ld + row;
+            if (row + 1 < n) {
+                *reinterpret_cast<double2*>(Are + gi) = make_double2(q[0][ni][e] - p[0][ni][e], q[1][ni][e] - p[1][ni][e]);
+                *reinterpret_cast<double2*>(Aim + gi) = make_double2(r[0][ni][e] - p[0][ni][e], r[1][ni][e] - p[1][ni][e]);
+            } else if (row < n) {
+                Are[gi] = q[0][ni][e] - p[0][ni][e];
+                Aim[gi] = r[0][ni][e] - p[0][ni][e];
             }
         }
-    }
 }
 
 // ------------------------------------------------------------------ TRSM via L11^{-1} (DMMA)
@@ -2187,7 +2200,8 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                                    static_cast<long long>(c1 - c0) * w;
             FDS_LAUNCH(lu_g3_prep_kernel, dim3(static_cast<unsigned>(std::min<long long>(ceil_div(work, 256LL), 64)), pb.batch),
                        256, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? 1 : 0);
-            constexpr size_t sm = g3_smem_doubles<32>() * sizeof(double) + kTmaSmemPad + GSTAGES * sizeof(unsigned);
+            constexpr size_t sm = g3_smem_doubles<32>() * sizeof(double) + 128 +
+                                  GSTAGES * (sizeof(uint64_t) + sizeof(unsigned));
             auto go = [&](auto kern) {
                 ensure_dynamic_smem(reinterpret_cast<const void*>(kern), sm);
                 dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, 32), pb.batch);

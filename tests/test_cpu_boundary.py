@@ -150,10 +150,11 @@ def test_bem_create_validates_on_the_host(case):
 
 
 def test_default_3m_gemm_kernel_is_tma_fed_dmma():
-    """The default trailing update (lu_gemm3m_tma_kernel<128, 32, 4, 2, 256, 1>)
+    """The default trailing update (lu_gemm3m_tma_kernel<128, 32, 4, 2, 256, 1, 16, 2>)
     issues only DMMA for its products (no FP64 adds in the k-loop: the operand
-    sums come from lu_g3_prep_kernel) and is fed by TMA tensor loads."""
-    fn = "_ZN4fdsb20lu_gemm3m_tma_kernelILi128ELi32ELi4ELi2ELi256ELi1EEEv14CUtensorMap_stS1_S1_S1_Pdmmiiii"
+    sums come from lu_g3_prep_kernel), is fed by TMA tensor loads and moves
+    its A fragments and the C tile in 16-byte accesses."""
+    fn = "_ZN4fdsb20lu_gemm3m_tma_kernelILi128ELi32ELi4ELi2ELi256ELi1ELi16ELi2EEEv14CUtensorMap_stS1_S1_S1_Pdmmiiii"
     out = subprocess.run(["cuobjdump", "-sass", "-fun", fn, str(P.library_path())], capture_output=True,
                          text=True).stdout
     assert "UTMALDG" in out
@@ -161,4 +162,8 @@ def test_default_3m_gemm_kernel_is_tma_fed_dmma():
     # 3 products x 4 k-steps x (MI = 2) x (NI = 2) per unrolled k-chunk, twice: the
     # steady-state chunk and the P-first first chunk (P alone, then Q and R)
     assert n_dmma == 2 * 3 * 4 * 2 * 2
-    assert out.count("DADD") <= 2 * 2 * 2 * 2  # epilogue only: Q - P, R - P per accumulator pair
+    lines = out.splitlines()
+    last_dmma = max(i for i, ln in enumerate(lines) if "DMMA.8x8x4" in ln)
+    dadd = [i for i, ln in enumerate(lines) if "DADD" in ln]
+    assert dadd and min(dadd) > last_dmma  # epilogue only: Q - P, R - P
+    assert "LDS.128" in out and "STG.E.128" in out and "LDG.E.128" in out
