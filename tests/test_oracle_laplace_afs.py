@@ -160,3 +160,19 @@ def test_afs_rod_example1_acceptance():  # SPEC.md acceptance #4 (N_c <= 55 vs F
                   orf=[0, 1, 2, 3, 4], test=[5, 6])
     assert r["converged"]
     assert r["n_c"] <= 55
+
+
+def test_afs_defaults_fixture_is_the_reference_run():
+    """tests/golden/afs_defaults_pressurised_sphere.json (the reference run_afs at
+    its defaults on the pressurised cfg1 sphere, used by the GPU failure-mode
+    test) starts with the reference's own initial frequencies (afs.cpp:302-304)
+    and records the reference's NumericError."""
+    from pathlib import Path
+
+    fx = json.loads((Path(__file__).parent / "golden" / "afs_defaults_pressurised_sphere.json").read_text())
+    kw = fx["config"]
+    s = np.array([complex(a, b) for a, b in fx["samples"]])
+    assert len(s) == fx["n_c"] == fx["solver_calls"]
+    np.testing.assert_array_equal(s[:16], O.initial_frequencies(16, kw["eta"], kw["omega_max"]))
+    assert fx["error"] == "NumericError" and "relocate_poles" in fx["message"]
+    assert len(set(s.tolist())) == len(s)  # every sample is a distinct solve
