@@ -66,9 +66,9 @@ try:
     rr = O.run_afs(sysr, **cfg)
     ref = dict(n_c=rr["n_c"], converged=rr["converged"], samples=rr["samples"], error=None)
 except O.OracleError as e:
-    part = getattr(e, "partial", {}) or {}
-    ref = dict(error=str(e).split(":")[0], msg=str(e), samples=part.get("samples", np.zeros(0)),
-               n_c=part.get("n_c"))
+    rpart = getattr(e, "partial", {}) or {}
+    ref = dict(error=str(e).split(":")[0], msg=str(e), samples=rpart.get("samples", np.zeros(0)),
+               n_c=rpart.get("n_c"))
 ref["wall_s"] = time.perf_counter() - t0
 ref["fresh_gpu_solves"] = calls[0]
 
