@@ -741,29 +741,39 @@ constexpr int g3_smem_doubles() { return NS * 3 * (KC * GAS + BN * (KC + 4)); }
 // GEMM's inner loop is DMMA-only (FP64 adds there contend with DMMA for the
 // same pipe): L21 planes Re+Im, Re-Im at [b][p][kk][m] (absolute row m, panel
 // column kk, ld rows per column), U12 plane Re+Im at [b][c][kk] (kG3Rows per column).
-__global__ void lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, size_t plane, int n, int ld, int k,
-                                  int w, int c0, int c1, double* __restrict__ g3, int do_l) {
+// Grid: x = [L column blocks (one per panel column kk, lblocks = w or 0 when the
+// L planes are current)] + [U blocks striding over (column, k-pair)], y = matrix.
+// 16-byte accesses throughout (k, w, ld and kG3Rows are even), no divisions.
+__global__ void __launch_bounds__(256) lu_g3_prep_kernel(const double* __restrict__ A, size_t mstride, size_t plane,
+                                                         int n, int ld, int k, int w, int c0, int c1,
+                                                         double* __restrict__ g3, int lblocks) {
     const int b = blockIdx.y;
     const double* Are = A + static_cast<size_t>(b) * mstride;
     const double* Aim = Are + plane;
-    double* L = g3 + static_cast<size_t>(b) * 2 * kG3W * ld;
-    double* U = g3 + static_cast<size_t>(gridDim.y) * 2 * kG3W * ld + static_cast<size_t>(b) * ld * kG3Rows;
-    const int rows = do_l ? n - k - w : 0;
-    const long long nl = static_cast<long long>(rows) * w, nu = static_cast<long long>(c1 - c0) * w;
-    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < nl + nu;
-         q += static_cast<long long>(gridDim.x) * blockDim.x) {
-        if (q < nl) {
-            const int kk = static_cast<int>(q / rows), m = k + w + static_cast<int>(q % rows);
-            const size_t gi = static_cast<size_t>(k + kk) * ld + m;
-            const double x = Are[gi], y = Aim[gi];
-            L[static_cast<size_t>(kk) * ld + m] = x + y;
-            L[static_cast<size_t>(kG3W + kk) * ld + m] = x - y;
-        } else {
-            const long long u = q - nl;
-            const int c = c0 + static_cast<int>(u / w), kk = static_cast<int>(u % w);
-            const size_t gi = static_cast<size_t>(c) * ld + k + kk;
-            U[static_cast<size_t>(c) * kG3Rows + kk] = Are[gi] + Aim[gi];
+    if (static_cast<int>(blockIdx.x) < lblocks) {
+        const int kk = blockIdx.x;
+        double* L = g3 + static_cast<size_t>(b) * 2 * kG3W * ld;
+        const double2* xr = reinterpret_cast<const double2*>(Are + static_cast<size_t>(k + kk) * ld);
+        const double2* xi = reinterpret_cast<const double2*>(Aim + static_cast<size_t>(k + kk) * ld);
+        double2* ls = reinterpret_cast<double2*>(L + static_cast<size_t>(kk) * ld);
+        double2* ld2 = reinterpret_cast<double2*>(L + static_cast<size_t>(kG3W + kk) * ld);
+        for (int m2 = (k + w) / 2 + threadIdx.x; 2 * m2 < n; m2 += blockDim.x) {
+            const double2 x = xr[m2], y = xi[m2];
+            ls[m2] = make_double2(x.x + y.x, x.y + y.y);
+            ld2[m2] = make_double2(x.x - y.x, x.y - y.y);
         }
+        return;
+    }
+    double* U = g3 + static_cast<size_t>(gridDim.y) * 2 * kG3W * ld + static_cast<size_t>(b) * ld * kG3Rows;
+    const int sh = __ffs(w) - 2;  // log2(w / 2): w is 64, 128 or 256
+    const int total = (c1 - c0) << sh;
+    const int nub = gridDim.x - lblocks;
+    for (int idx = (blockIdx.x - lblocks) * blockDim.x + threadIdx.x; idx < total; idx += nub * blockDim.x) {
+        const int c = c0 + (idx >> sh), k2 = idx & ((1 << sh) - 1);
+        const size_t gi = static_cast<size_t>(c) * ld + k + 2 * k2;
+        const double2 x = *reinterpret_cast<const double2*>(Are + gi);
+        const double2 y = *reinterpret_cast<const double2*>(Aim + gi);
+        *reinterpret_cast<double2*>(U + static_cast<size_t>(c) * kG3Rows + 2 * k2) = make_double2(x.x + y.x, x.y + y.y);
     }
 }
 
@@ -2196,10 +2206,11 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
             t_g3_ws->g3_key_A = pb.A;
             t_g3_ws->g3_key_k = k;
             t_g3_ws->g3_key_w = w;
-            const long long work = (do_l ? static_cast<long long>(pb.n - k - w) * w : 0) +
-                                   static_cast<long long>(c1 - c0) * w;
-            FDS_LAUNCH(lu_g3_prep_kernel, dim3(static_cast<unsigned>(std::min<long long>(ceil_div(work, 256LL), 64)), pb.batch),
-                       256, 0, st, pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? 1 : 0);
+            if (w != 64 && w != 128 && w != 256) throw CudaError("lu: 3M operand planes need w = 64, 128 or 256");
+            const int ublocks = static_cast<int>(std::min<long long>(
+                ceil_div(static_cast<long long>(c1 - c0) * (w / 2), 256LL), 2LL * device_info().sms));
+            FDS_LAUNCH(lu_g3_prep_kernel, dim3(static_cast<unsigned>((do_l ? w : 0) + ublocks), pb.batch), 256, 0, st,
+                       pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? w : 0);
             constexpr size_t sm = g3_smem_doubles<32>() * sizeof(double) + 128 +
                                   GSTAGES * (sizeof(uint64_t) + sizeof(unsigned));
             auto go = [&](auto kern) {
