@@ -204,3 +204,29 @@ def test_cfg3_solution_matches_oracle_n36864():
     e = rel_l2(u, uo)
     print(f"cfg3 N=36864 rel-L2 vs oracle: {e:.2e} (oracle assembly {t[0]:.1f} s, zgetrf+zgetrs {t[1]:.1f} s)")
     assert e < 1e-9
+
+
+def test_afs_bem_cfg2_mesh_identical_sequence_vs_independent_oracle():
+    """AFS parity on the cfg2 mesh (1280 triangles, N = 3840) with finite,
+    converging thresholds: the product run_afs (GPU BEM + GPU VF) against the
+    reference's own run_afs (afs.cpp:226-396, oracle VF) whose system is the
+    oracle BEM assembly + OpenBLAS zgetrf/zgetrs on the host — no GPU result
+    enters the reference side. 16 normal-displacement channels (the cfg2
+    16 surface points), J0 = 8, E1 = E2 = 1e-3."""
+    V, F = mesh.icosphere(3)
+    tr = mesh.pressure_traction(V, F)
+    ch = _normal_channels(V, F, 16)
+    kw = dict(omega_max=math.pi * 256 / T_PERIOD, eta=0.25, period=T_PERIOD, initial_count=8,
+              e1_threshold=1e-3, e2_threshold=1e-3)
+    r = P.run_afs(P.BemSystem(V, F, tr, channels=ch, max_batch=8), **kw)
+    assert r["converged"]
+    orc = O.Bem(V, F, tr)
+    ob = O.openblas_path()
+    o = O.run_afs(O.System.callback(len(ch), lambda s: orc.solve_openblas(s, ob)[0][ch]), **kw)
+    print(f"cfg2 mesh AFS: product n_c {r['n_c']}, reference n_c {o['n_c']}")
+    assert o["converged"] and r["n_c"] == o["n_c"]
+    np.testing.assert_array_equal(r["samples"], o["samples"])
+    np.testing.assert_array_equal(r["history"][:, :6], o["history"][:, :6])
+    np.testing.assert_allclose(r["history"][:, 7], o["history"][:, 7], rtol=1e-6)
+    np.testing.assert_allclose(r["history"][1:, 6], o["history"][1:, 6], rtol=1e-6)
+    assert worst_match(r["poles"], o["poles"]) < 1e-6
