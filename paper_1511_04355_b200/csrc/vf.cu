@@ -195,12 +195,17 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(256)
+// 32 warps: each Householder step's column updates are latency-bound (the
+// matrix lives in global memory once 2J x (2M+1) exceeds shared memory), so the
+// CTA keeps up to 32 columns in flight (J = 210, M = 104: 8 warps took 6.7 ms)
+constexpr int kRelocQrThreads = 1024;
+
+__global__ void __launch_bounds__(kRelocQrThreads)
 vf_reloc_qr_kernel(int J, int M, int K, const cplx* __restrict__ vals, const cplx* __restrict__ phi,
                    const double* __restrict__ cscale, const double* __restrict__ sscale, double* gwork,
                    double* __restrict__ r22, double* __restrict__ beta_out, double* __restrict__ tail) {
     extern __shared__ double qsm[];
-    __shared__ double red[8];
+    __shared__ double red[32];
     __shared__ double s_tau, s_beta, s_inv;
     const int k = blockIdx.x;
     const int rows = 2 * J, cols = 2 * M + 1;
@@ -442,6 +447,25 @@ __global__ void vf_rms_kernel(int J, int K, int M, const cplx* __restrict__ vals
         sq += abs2(d);
     }
     rms[k] = sqrt(sq / J);
+}
+
+// Few channels (the AFS fits: K = 5 ... 48): one CTA per channel, threads over
+// the samples, fixed-order block reduction (the thread-per-channel kernel above
+// runs a J x M loop on one thread per channel and only K threads in total).
+__global__ void __launch_bounds__(128) vf_rms_cta_kernel(int J, int K, int M, const cplx* __restrict__ vals,
+                                                         const cplx* __restrict__ res,
+                                                         const cplx* __restrict__ invd /*[m][j]*/,
+                                                         double* __restrict__ rms) {
+    __shared__ double red[8];
+    const int k = blockIdx.x;
+    double sq = 0.0;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+        cplx fit = mk(0.0, 0.0);
+        for (int m = 0; m < M; ++m) fit = fit + res[static_cast<size_t>(m) * K + k] * invd[static_cast<size_t>(m) * J + j];
+        sq += abs2(fit - vals[static_cast<size_t>(j) * K + k]);
+    }
+    const double t = block_sum(sq, red);
+    if (threadIdx.x == 0) rms[k] = sqrt(t / J);
 }
 
 __global__ void vf_inv_table_kernel(int G, int M, const cplx* __restrict__ grid, const cplx* __restrict__ poles,
@@ -876,7 +900,7 @@ RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const
     } else {
         ensure_dynamic_smem(reinterpret_cast<const void*>(vf_reloc_qr_kernel), smem);
     }
-    FDS_LAUNCH(vf_reloc_qr_kernel, K, 256, smem, cx.st, J, M, K, dvals, dphi, dsc, dsc + M, gwork, dr22, dbeta,
+    FDS_LAUNCH(vf_reloc_qr_kernel, K, kRelocQrThreads, smem, cx.st, J, M, K, dvals, dphi, dsc, dsc + M, gwork, dr22, dbeta,
                dtail);
     // stacked sigma least squares (vecfit.cpp:281-285) and the per-channel RMS
     // (:287-295) on the device; only y, the RMS and the rank come back
@@ -1067,7 +1091,10 @@ void vf_residues_device(const std::vector<Cx>& s, const cplx* values_dev, int K,
             for (int j = 0; j < J; ++j) invd[static_cast<size_t>(m) * J + j] = 1.0 / (s[j] - poles[m]);
         cplx* dinv = dev<cplx>(cx.phi, invd.size());
         FDS_CUDA(cudaMemcpyAsync(dinv, invd.data(), invd.size() * sizeof(cplx), cudaMemcpyHostToDevice, st));
-        FDS_LAUNCH(vf_rms_kernel, ceil_div(K, 128), 128, 0, st, J, K, M, values_dev, res_dev, dinv, rms_dev);
+        if (K < 4 * device_info().sms * 128 / 16)  // fewer channels than ~1/16 of a thread per SM slot
+            FDS_LAUNCH(vf_rms_cta_kernel, K, 128, 0, st, J, K, M, values_dev, res_dev, dinv, rms_dev);
+        else
+            FDS_LAUNCH(vf_rms_kernel, ceil_div(K, 128), 128, 0, st, J, K, M, values_dev, res_dev, dinv, rms_dev);
     }
 }
 
