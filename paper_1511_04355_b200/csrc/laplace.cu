@@ -604,15 +604,17 @@ __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
 
 // QS > 0: the term count padded to 4 is known at compile time (fully unrolled
 // DMMA k-loop); QS = 0: runtime Q.
-template <int QS>
+// (Measured: three exponential buffers with one barrier per chunk instead of
+// two buffers and two barriers made no difference.)
+template <int QS, int NBUF = 2>
 __global__ void __launch_bounds__(256)
 rat_invert_kernel(int K, int T, int Qrt, int nt, const int* __restrict__ term_m, const double* __restrict__ term_w,
                   const cplx* __restrict__ res /*[m][K]*/, const double* __restrict__ E, double* __restrict__ out) {
     const int Q = QS > 0 ? QS : Qrt;
     extern __shared__ __align__(16) double rsm[];
     double* As = rsm;                 // [Q][RS]  (q, channel)
-    double* Bs0 = rsm + Q * RS;       // [Q][RS]  (q, time) x 2 buffers
-    double* Bs1 = Bs0 + Q * RS;
+    double* Bs0 = rsm + Q * RS;       // [Q][RS]  (q, time) x NBUF buffers
+    auto Bsb = [&](int i) { return Bs0 + static_cast<size_t>(i) * Q * RS; };
     const int k0 = blockIdx.x * RBM;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nchunks = (T + RBN - 1) / RBN;
@@ -631,23 +633,55 @@ rat_invert_kernel(int K, int T, int Qrt, int nt, const int* __restrict__ term_m,
         asm volatile("cp.async.commit_group;\n" ::);
     };
     load_e(Bs0, 0);
-    for (int idx = tid; idx < (Q / 2) * RBM; idx += blockDim.x) {
-        const int p = idx / RBM, c = idx % RBM;
-        const int k = k0 + c;
-        double re = 0.0, im = 0.0;
-        if (p < nt && k < K) {
-            const double2 r = __ldcs(reinterpret_cast<const double2*>(res) + static_cast<size_t>(term_m[p]) * K + k);
-            re = term_w[p] * r.x;
-            im = -term_w[p] * r.y;
+    if constexpr (QS > 0) {
+        // residue tile: all loads in flight before the first use (a dependent
+        // load-multiply-store loop was ~20 % of the kernel's warp samples)
+        constexpr int NLD = ((QS / 2) * RBM + 255) / 256;
+        __shared__ int s_tm[QS / 2];
+        __shared__ double s_tw[QS / 2];
+        if (tid < QS / 2) {
+            s_tm[tid] = tid < nt ? term_m[tid] : 0;
+            s_tw[tid] = tid < nt ? term_w[tid] : 0.0;
         }
-        As[(2 * p) * RS + c] = re;
-        As[(2 * p + 1) * RS + c] = im;
+        __syncthreads();
+        double2 rv[NLD];
+#pragma unroll
+        for (int i = 0; i < NLD; ++i) {
+            const int idx = tid + i * 256;
+            const int p = idx / RBM, k = k0 + idx % RBM;
+            rv[i] = (idx < (QS / 2) * RBM && p < nt && k < K)
+                        ? __ldcs(reinterpret_cast<const double2*>(res) + static_cast<size_t>(s_tm[p]) * K + k)
+                        : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < NLD; ++i) {
+            const int idx = tid + i * 256;
+            if (idx < (QS / 2) * RBM) {
+                const int p = idx / RBM, c = idx % RBM;
+                const double wp = s_tw[p];
+                As[(2 * p) * RS + c] = wp * rv[i].x;
+                As[(2 * p + 1) * RS + c] = -wp * rv[i].y;
+            }
+        }
+    } else {
+        for (int idx = tid; idx < (Q / 2) * RBM; idx += blockDim.x) {
+            const int p = idx / RBM, c = idx % RBM;
+            const int k = k0 + c;
+            double re = 0.0, im = 0.0;
+            if (p < nt && k < K) {
+                const double2 r = __ldcs(reinterpret_cast<const double2*>(res) + static_cast<size_t>(term_m[p]) * K + k);
+                re = term_w[p] * r.x;
+                im = -term_w[p] * r.y;
+            }
+            As[(2 * p) * RS + c] = re;
+            As[(2 * p + 1) * RS + c] = im;
+        }
     }
     const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps, 32 channels x 16 steps each
     for (int ch = 0; ch < nchunks; ++ch) {
-        double* Bs = (ch & 1) ? Bs1 : Bs0;
+        double* Bs = Bsb(ch % NBUF);
         if (ch + 1 < nchunks) {
-            load_e((ch & 1) ? Bs0 : Bs1, (ch + 1) * RBN);
+            load_e(Bsb((ch + 1) % NBUF), (ch + 1) * RBN);
             asm volatile("cp.async.wait_group 1;\n" ::);
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::);
@@ -684,7 +718,7 @@ rat_invert_kernel(int K, int T, int Qrt, int nt, const int* __restrict__ term_m,
                 }
             }
         }
-        __syncthreads();
+        if constexpr (NBUF == 2) __syncthreads();
     }
 }
 
