@@ -65,16 +65,18 @@ def test_cfg5_vf_and_reconstruction_subset_parity():
     worst = max(min(abs(g - w) / abs(w) for g in model.poles) for w in o["poles"])
     assert worst < 1e-6
     R, _ = P.identify_residues(s, vals, model.poles)  # all 300k DOFs on the GPU
-    sub = rng.choice(D, 25, replace=False)
-    for k in sub:
-        ro, _ = O.identify_residues(s, vals[:, k], model.poles)
-        assert rel_l2(R[k], ro) < 1e-9
+    # 3000 DOFs spread over the whole set against the oracle (per-DOF rel-L2)
+    sub = np.sort(rng.choice(D, 3000, replace=False))
+    ro = O.identify_residues_many(s, vals[:, sub], model.poles, threads=8)
+    err = np.linalg.norm(R[sub] - ro, axis=1) / np.linalg.norm(ro, axis=1)
+    print(f"cfg5 residues, 3000 DOFs: max rel-L2 {err.max():.2e}")
+    assert err.max() < 1e-9
     t = np.arange(512) * T / 512
     h = P.rational_invert(P.RationalModel(model.poles, R[sub]), t)
     ho = O.rational_invert(model.poles, R[sub], t)
     assert rel_l2(h, ho) < 1e-10
     sk = eta + 1j * (2 * math.pi / T) * np.arange(257)
-    half = (1.0 / (sk[:, None] - poles[None, :])) @ res[sub].T  # (257, 25)
+    half = (1.0 / (sk[:, None] - poles[None, :])) @ res[sub].T  # (257, 3000)
     f = P.fsm_invert(T, 512, eta, half.T.copy())
     fo = O.fsm_invert(T, 512, eta, half.T.copy())
     assert rel_l2(f, fo) < 1e-10
