@@ -5,7 +5,7 @@ libfdsweep_b200_jitter.so is the product code compiled with FDS_JITTER: every
 hand-rolled synchronisation point sleeps a pseudo-random 0-8 us before it
 proceeds (common.cuh fds_jitter):
   * the 3M GEMM's barrier-free stage ring ("last warp out refills",
-    lu_gemm3m_tma_kernel / lu_gemm3m_ws_kernel) at every k-chunk;
+    lu_gemm3m_tma_kernel) at every k-chunk;
   * the cluster/DSMEM panel before every per-column cluster barrier and the
     global-slot panel's software group barrier;
   * the dataflow substitution's flag publication and readiness polls;
