@@ -230,3 +230,29 @@ def test_afs_bem_cfg2_mesh_identical_sequence_vs_independent_oracle():
     np.testing.assert_allclose(r["history"][:, 7], o["history"][:, 7], rtol=1e-6)
     np.testing.assert_allclose(r["history"][1:, 6], o["history"][1:, 6], rtol=1e-6)
     assert worst_match(r["poles"], o["poles"]) < 1e-6
+
+
+def test_cfg4_sphere_pressure_converges_to_the_analytic_cavity():
+    """The north_star mesh against the closed-form pressurised spherical cavity
+    (SURVEY.md Appendix A.3), an answer independent of both the oracle and the
+    product: constant flat elements converge O(h), so the max error of u_r
+    halves per icosphere refinement (oracle: 10.8 % / 4.9 % / 2.2 % at 80 / 320 /
+    1280 triangles, tests/test_oracle_bem.py); the GPU solution on the 1280- and
+    5120-triangle (N = 15360) spheres continues the sequence."""
+    errs = {}
+    for level in (3, 4):
+        V, F = mesh.icosphere(level)
+        g = P.BemSystem(V, F, mesh.pressure_traction(V, F), max_batch=2)
+        _, n, _ = mesh.element_geometry(V, F)
+        for s in (complex(0.9, 0.4), complex(0.25, 1.5)):
+            u = g.evaluate(s).reshape(-1, 3)
+            ur = -np.einsum("ij,ij->i", u, n)
+            ref = mesh.sphere_radial_analytic(s)
+            errs[(level, s)] = np.max(np.abs(ur - ref)) / abs(ref)
+            tang = np.max(np.abs(u + ur[:, None] * n)) / abs(ref)
+            assert tang < 1e-2  # tangential components vanish by symmetry
+        g.close()
+    print({f"{k[0]}@{k[1]}": f"{v:.3%}" for k, v in errs.items()})
+    for s in (complex(0.9, 0.4), complex(0.25, 1.5)):
+        assert errs[(4, s)] < 0.015
+        assert errs[(4, s)] < 0.6 * errs[(3, s)]
