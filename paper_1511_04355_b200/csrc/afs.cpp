@@ -4,7 +4,16 @@
 // J0 initial frequencies of a BEM system are solved as one batched launch.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <exception>
 #include <functional>
+#include <future>
+#include <mutex>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
 #include <limits>
 #include <map>
 #include <numbers>
@@ -114,7 +123,78 @@ double afs_error_e1(const std::vector<double>& t, const std::vector<double>& cur
     return worst;
 }
 
+namespace {
+
+// One host worker thread for the run: the low-order fit of each iteration runs
+// on it (its own thread-local VfContext: stream, scratch, solve-operator cache)
+// while the calling thread fits the high-order model. The two fits are
+// independent (afs.cpp:337-340), so the results are those of the sequential
+// order; an exception is reported in that order too (high first).
+class FitWorker {
+  public:
+    explicit FitWorker(int device) : dev_(device), th_([this] { loop(); }) {}
+    ~FitWorker() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    std::future<void> submit(std::function<void()> f) {
+        auto task = std::make_shared<std::packaged_task<void()>>(std::move(f));
+        std::future<void> fut = task->get_future();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back([task] { (*task)(); });
+        }
+        cv_.notify_one();
+        return fut;
+    }
+
+  private:
+    void loop() {
+        cudaSetDevice(dev_);
+        for (;;) {
+            std::function<void()> job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (q_.empty()) return;
+                job = std::move(q_.front());
+                q_.pop_front();
+            }
+            job();
+        }
+    }
+    int dev_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    bool stop_ = false;
+    std::thread th_;
+};
+
+}  // namespace
+
 void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut& r) {
+    // FDSWEEP_AFS_TIMING=1: per-phase host wall times on stderr (development aid)
+    static const bool timing = [] {
+        const char* e = std::getenv("FDSWEEP_AFS_TIMING");
+        return e && std::atoi(e) == 1;
+    }();
+    double t_eval = 0, t_upload = 0, t_fit = 0, t_err = 0, t_e1 = 0, t_sel = 0;
+    using clk = std::chrono::steady_clock;
+    auto since = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
+    struct Report {
+        bool on;
+        double *a, *b, *c, *d, *e, *f;
+        ~Report() {
+            if (on)
+                std::fprintf(stderr, "afs timing: eval %.3f upload %.3f fits %.3f errors %.3f e1 %.3f select %.3f s\n", *a,
+                             *b, *c, *d, *e, *f);
+        }
+    } report{timing, &t_eval, &t_upload, &t_fit, &t_err, &t_e1, &t_sel};
     validate(cfg);
     r = AfsOut{};
     r.orf = cfg.orf.empty() ? draw_channels(channels, std::min(5, channels), cfg.seed) : cfg.orf;
@@ -154,7 +234,9 @@ void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut
                 miss.push_back(s);
         if (!miss.empty()) {
             std::vector<Cx> vals(miss.size() * static_cast<size_t>(channels));
+            const auto t0 = clk::now();
             eval(miss, vals);
+            t_eval += since(t0);
             for (size_t i = 0; i < miss.size(); ++i) {
                 cache[{miss[i].real(), miss[i].imag()}] =
                     std::vector<Cx>(vals.begin() + i * channels, vals.begin() + (i + 1) * channels);
@@ -182,6 +264,9 @@ void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut
     // the per-channel E1 ratios and the selected grid index come back.
     auto& vcx = VfContext::get();
     const cudaStream_t st = vcx.st;
+    int device = 0;
+    FDS_CUDA(cudaGetDevice(&device));
+    FitWorker worker(device);
     DevMem samp[2], res_h, res_l, res_t, ce, pos, red, ser[2];
     int samp_cur = 0, jcap = 0, j_dev = 0;
     const bool test_all = static_cast<int>(test_pos.size()) == KF &&
@@ -222,15 +307,37 @@ void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut
             throw ConvergenceError("afs: no convergence within max_iterations");
         const int J = static_cast<int>(r.samples.size());
         const auto [MH, ML] = afs_fit_orders(J, cfg.alpha_high, cfg.alpha_low);
+        auto t0 = clk::now();
         upload_samples();
+        t_upload += since(t0);
+        t0 = clk::now();
         const cplx* dsamp = static_cast<const cplx*>(samp[samp_cur].p);
         std::vector<Cx> ov(static_cast<size_t>(J) * KO);  // ORF samples for the host relocation step
         for (int j = 0; j < J; ++j)
             for (int q = 0; q < KO; ++q) ov[static_cast<size_t>(j) * KO + q] = r.values[static_cast<size_t>(j) * channels + r.orf[q]];
         cplx* drh = res_h.get<cplx>(static_cast<size_t>(MH) * KF);
         cplx* drl = res_l.get<cplx>(static_cast<size_t>(ML) * KF);
-        const std::vector<Cx> p_h = vf_vector_fit_device(r.samples, ov.data(), dsamp, KF, orf_pos, MH, cfg.n_relocations, drh, st);
-        const std::vector<Cx> p_l = vf_vector_fit_device(r.samples, ov.data(), dsamp, KF, orf_pos, ML, cfg.n_relocations, drl, st);
+        // afs.cpp:337-340: the high- and low-order fits, concurrently
+        std::vector<Cx> p_h, p_l;
+        std::future<void> low = worker.submit([&] {
+            auto& wcx = VfContext::get();
+            p_l = vf_vector_fit_device(r.samples, ov.data(), dsamp, KF, orf_pos, ML, cfg.n_relocations, drl, wcx.st);
+            FDS_CUDA(cudaStreamSynchronize(wcx.st));  // drl complete before the caller's stream reads it
+        });
+        std::exception_ptr fail;
+        try {
+            p_h = vf_vector_fit_device(r.samples, ov.data(), dsamp, KF, orf_pos, MH, cfg.n_relocations, drh, st);
+        } catch (...) {
+            fail = std::current_exception();
+        }
+        try {
+            low.get();
+        } catch (...) {
+            if (!fail) fail = std::current_exception();
+        }
+        if (fail) std::rethrow_exception(fail);
+        t_fit += since(t0);
+        t0 = clk::now();
         vf_channel_errors_device(p_h, drh, p_l, drl, KF, grid, dtest, KT, dorf, KO, dce, dred, st);
         AfsErrReduce er;
         FDS_CUDA(cudaMemcpyAsync(&er, dred, sizeof(er), cudaMemcpyDeviceToHost, st));
@@ -240,6 +347,8 @@ void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut
                                " has identically zero high-order fit");
         if (test_pos.empty()) throw ValidationError("error_e2: no test channels");
         const double e2 = er.e2;
+        t_err += since(t0);
+        t0 = clk::now();
         const cplx* drt = drh;
         if (!test_all) {
             cplx* g = res_t.get<cplx>(static_cast<size_t>(MH) * KT);
@@ -252,6 +361,7 @@ void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut
                                     : std::numeric_limits<double>::infinity();
         have_prev = true;
         cur_slot ^= 1;
+        t_e1 += since(t0);
         r.history.push_back({J, MH, ML, false, Cx(0, 0), e1, e2});
         ph = p_h;
         if (e1 <= cfg.e1_threshold && e2 <= cfg.e2_threshold) {
@@ -264,9 +374,11 @@ void run_afs_impl(const BatchEval& eval, int channels, const AfsCfg& cfg, AfsOut
         }
         // select_new_frequency (afs.cpp:147-187) reuses this iteration's channel
         // errors (the reference recomputes identical values, afs.cpp:156)
+        t0 = clk::now();
         const int sel = vf_select_device(p_h, drh + er.kmax, p_l, drl + er.kmax, static_cast<size_t>(KF), grid,
                                          r.samples, radius, st);
         const Cx s_new = grid[sel];
+        t_sel += since(t0);
         r.history.back().has_s_new = true;
         r.history.back().s_new = s_new;
         evaluate({s_new});

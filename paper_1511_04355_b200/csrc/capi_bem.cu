@@ -56,6 +56,7 @@ void KernelProfile::end(cudaStream_t st, cudaEvent_t a, int kind, double work) {
     cudaEvent_t b;
     FDS_CUDA(cudaEventCreate(&b));
     FDS_CUDA(cudaEventRecord(b, st));
+    std::lock_guard<std::mutex> lk(mu);
     recs.push_back({a, b, work, kind});
 }
 
@@ -295,6 +296,7 @@ int64_t fds_kernel_launches(void) { return g_launches.load(); }
 int fds_profile_enable(int on) {
     return fds_guard([&] {
         auto& p = profiler();
+        std::lock_guard<std::mutex> lk(p.mu);
         for (auto& r : p.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
         p.recs.clear();
         p.enabled = on != 0;
@@ -304,6 +306,7 @@ int fds_profile_enable(int on) {
 int fds_profile_read(int kind, int* count, double* total_ms, double* total_work) {
     return fds_guard([&] {
         auto& p = profiler();
+        std::lock_guard<std::mutex> lk(p.mu);
         int c = 0;
         double ms = 0, w = 0;
         for (auto& r : p.recs) {

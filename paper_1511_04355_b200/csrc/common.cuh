@@ -195,6 +195,7 @@ struct KernelProfile {
     bool enabled = false;
     struct Rec { cudaEvent_t a, b; double work; int kind; };
     std::vector<Rec> recs;
+    std::mutex mu;  // the AFS driver fits its two models on two host threads
     void begin(cudaStream_t st, int kind, double work, cudaEvent_t& a);
     void end(cudaStream_t st, cudaEvent_t a, int kind, double work);
 };
