@@ -51,7 +51,7 @@ void* VfContext::Buf::get(size_t need) {
 
 void VfContext::release() {
     if (st) cudaStreamSynchronize(st);
-    for (Buf* b : {&values, &resid, &W, &phi, &rms, &tab, &tab2, &out, &misc, &misc2, &qr, &lsq, &lsq_io}) {
+    for (Buf* b : {&values, &resid, &W, &phi, &rms, &tab, &tab2, &out, &misc, &misc2, &qr, &lsq, &lsq_io, &chanerr}) {
         if (b->p) cudaFree(b->p);
         b->p = nullptr;
         b->bytes = 0;
@@ -493,7 +493,11 @@ vf_chanerr_kernel(int G, int MH, int ML, int K, const cplx* __restrict__ rh, con
     for (int m = threadIdx.x; m < ML; m += blockDim.x) rsm[MH + m] = rl[k * sk_l + m * sm_l];
     __syncthreads();
     double md = 0.0, mh = 0.0;
-    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    // grid chunk blockIdx.y of gridDim.y (partial maxima, combined by
+    // vf_chanerr_combine_kernel: max is exact, so the result is split-independent)
+    const int gc = (G + gridDim.y - 1) / gridDim.y;
+    const int g1 = min(G, static_cast<int>(blockIdx.y + 1) * gc);
+    for (int g = blockIdx.y * gc + threadIdx.x; g < g1; g += blockDim.x) {
         cplx fh, fl;
         model_at(g, G, MH, rsm, invh, fh);
         model_at(g, G, ML, rsm + MH, invl, fl);
@@ -513,9 +517,21 @@ vf_chanerr_kernel(int G, int MH, int ML, int K, const cplx* __restrict__ rh, con
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { md = fmax(md, red[0][w]); mh = fmax(mh, red[1][w]); }
         md = fmax(md, red[0][0]);
         mh = fmax(mh, red[1][0]);
-        out[2 * k] = md;
-        out[2 * k + 1] = mh;
+        out[2 * (static_cast<size_t>(blockIdx.y) * K + k)] = md;
+        out[2 * (static_cast<size_t>(blockIdx.y) * K + k) + 1] = mh;
     }
+}
+
+__global__ void vf_chanerr_combine_kernel(int K, int S, const double* __restrict__ part, double* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double md = part[2 * k], mh = part[2 * k + 1];
+    for (int s = 1; s < S; ++s) {
+        md = fmax(md, part[2 * (static_cast<size_t>(s) * K + k)]);
+        mh = fmax(mh, part[2 * (static_cast<size_t>(s) * K + k) + 1]);
+    }
+    out[2 * k] = md;
+    out[2 * k + 1] = mh;
 }
 
 __global__ void __launch_bounds__(1024)
@@ -856,6 +872,36 @@ T* dev(VfContext::Buf& b, size_t count) {
     return static_cast<T*>(b.get(count * sizeof(T)));
 }
 
+// vf_chanerr_kernel over K channels, the grid split into S chunks when K alone
+// cannot fill the GPU (the AFS fits have K = 5 ... 48 channels).
+void chanerr_run(VfContext& cx, cudaStream_t st, int G, int MH, int ML, int K, const cplx* rh, const cplx* rl,
+                 size_t sk_h, size_t sm_h, size_t sk_l, size_t sm_l, const cplx* invh, const cplx* invl,
+                 double* out) {
+    const int S = std::max(1, std::min(std::min(16, G), ceil_div(4 * device_info().sms, K)));
+    const size_t smem = (MH + ML) * sizeof(cplx);
+    if (S == 1) {
+        FDS_LAUNCH(vf_chanerr_kernel, K, 256, smem, st, G, MH, ML, K, rh, rl, sk_h, sm_h, sk_l, sm_l, invh, invl, out);
+        return;
+    }
+    double* part = dev<double>(cx.chanerr, 2 * static_cast<size_t>(K) * S);
+    FDS_LAUNCH(vf_chanerr_kernel, dim3(K, S), 256, smem, st, G, MH, ML, K, rh, rl, sk_h, sm_h, sk_l, sm_l, invh,
+               invl, part);
+    FDS_LAUNCH(vf_chanerr_combine_kernel, ceil_div(K, 128), 128, 0, st, K, S, part, out);
+}
+
+// Does any grid point coincide with a pole (eval_model's collision check,
+// vecfit.cpp:494-496, over every (grid point, pole) pair)? Sorted-grid lookup
+// instead of the G x M scan (4096 x 240 pairs per AFS iteration).
+bool grid_hits_pole(const std::vector<Cx>& grid, const std::vector<Cx>& a, const std::vector<Cx>& b) {
+    auto less = [](const Cx& x, const Cx& y) { return x.real() < y.real() || (x.real() == y.real() && x.imag() < y.imag()); };
+    std::vector<Cx> g(grid);
+    std::sort(g.begin(), g.end(), less);
+    for (const auto* ps : {&a, &b})
+        for (const Cx& p : *ps)
+            if (std::binary_search(g.begin(), g.end(), p, less)) return true;
+    return false;
+}
+
 }  // namespace
 
 RelocResult vf_relocate(const std::vector<Cx>& s, const Cx* values, int K, const std::vector<Cx>& poles_in) {
@@ -1183,10 +1229,7 @@ std::vector<double> vf_channel_errors(const std::vector<Cx>& ph, const std::vect
     // afs.cpp:118-145
     if (grid.empty()) throw ValidationError("channel_errors: empty grid");
     const int G = static_cast<int>(grid.size()), MH = static_cast<int>(ph.size()), ML = static_cast<int>(pl.size());
-    for (Cx g : grid) {
-        for (Cx p : ph) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
-        for (Cx p : pl) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
-    }
+    if (grid_hits_pole(grid, ph, pl)) throw NumericError("eval_model: s coincides with a pole");
     auto& cx = VfContext::get();
     cplx* dgrid = dev<cplx>(cx.misc2, G + MH + ML);
     cplx* dph = dgrid + G;
@@ -1205,9 +1248,8 @@ std::vector<double> vf_channel_errors(const std::vector<Cx>& ph, const std::vect
                dinv + static_cast<size_t>(G) * MH);
     cudaEvent_t pe;
     profiler().begin(cx.st, kProfChanErr, 0.0, pe);
-    FDS_LAUNCH(vf_chanerr_kernel, K, 256, (MH + ML) * sizeof(cplx), cx.st, G, MH, ML, K, dr,
-               dr + static_cast<size_t>(K) * MH, size_t(MH), size_t(1), size_t(ML), size_t(1), dinv,
-               dinv + static_cast<size_t>(G) * MH, dout);
+    chanerr_run(cx, cx.st, G, MH, ML, K, dr, dr + static_cast<size_t>(K) * MH, size_t(MH), size_t(1), size_t(ML),
+                size_t(1), dinv, dinv + static_cast<size_t>(G) * MH, dout);
     profiler().end(cx.st, pe, kProfChanErr, 8.0 * G * static_cast<double>(K) * (MH + ML));
     std::vector<double> h(2 * static_cast<size_t>(K));
     FDS_CUDA(cudaMemcpyAsync(h.data(), dout, h.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
@@ -1229,10 +1271,7 @@ void vf_channel_errors_device(const std::vector<Cx>& ph, const cplx* rh_mk, cons
     // reduced on the device (E2, worst ORF channel, first zero-energy channel).
     if (grid.empty()) throw ValidationError("channel_errors: empty grid");
     const int G = static_cast<int>(grid.size()), MH = static_cast<int>(ph.size()), ML = static_cast<int>(pl.size());
-    for (Cx g : grid) {
-        for (Cx p : ph) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
-        for (Cx p : pl) if (g - p == Cx(0, 0)) throw NumericError("eval_model: s coincides with a pole");
-    }
+    if (grid_hits_pole(grid, ph, pl)) throw NumericError("eval_model: s coincides with a pole");
     auto& cx = VfContext::get();
     std::vector<Cx> tabs(grid);
     tabs.insert(tabs.end(), ph.begin(), ph.end());
@@ -1247,8 +1286,8 @@ void vf_channel_errors_device(const std::vector<Cx>& ph, const cplx* rh_mk, cons
                dinv + static_cast<size_t>(G) * MH);
     cudaEvent_t pe;
     profiler().begin(st, kProfChanErr, 0.0, pe);
-    FDS_LAUNCH(vf_chanerr_kernel, K, 256, (MH + ML) * sizeof(cplx), st, G, MH, ML, K, rh_mk, rl_mk, size_t(1),
-               size_t(K), size_t(1), size_t(K), dinv, dinv + static_cast<size_t>(G) * MH, ce_dev);
+    chanerr_run(cx, st, G, MH, ML, K, rh_mk, rl_mk, size_t(1), size_t(K), size_t(1), size_t(K), dinv,
+                dinv + static_cast<size_t>(G) * MH, ce_dev);
     profiler().end(st, pe, kProfChanErr, 8.0 * G * static_cast<double>(K) * (MH + ML));
     FDS_LAUNCH(afs_reduce_errors_kernel, 1, 1024, 0, st, K, ce_dev, KT, test_pos_dev, KO, orf_pos_dev, red_dev);
     // tabs is read by the async copy above

@@ -20,7 +20,7 @@ struct VfContext {
         size_t bytes = 0;
         void* get(size_t need);
     };
-    Buf values, resid, W, phi, rms, tab, tab2, out, misc, misc2, qr, lsq, lsq_io;
+    Buf values, resid, W, phi, rms, tab, tab2, out, misc, misc2, qr, lsq, lsq_io, chanerr;
     std::vector<double> w_key;  // (J, M, s, poles) of the solve operator held in W
     bool w_valid = false;
     void release();  // frees every buffer (and forgets the cached solve operator)
