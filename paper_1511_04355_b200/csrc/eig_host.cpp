@@ -1,6 +1,6 @@
 // Eigenvalues of the M x M relocation matrix H = blockdiag(poles) - b c^T
 // (vecfit.cpp:297-324; the reference calls Eigen::EigenSolver). M <= ~120, so
-// this stays on the host: a few hundred microseconds of sequential bulge
+// this stays on the host: a few milliseconds at most of sequential bulge
 // chasing that a GPU cannot shorten.
 //
 // Algorithm: Householder reduction to upper Hessenberg form followed by the
@@ -111,7 +111,7 @@ void schur2(double a, double b, double c, double d, std::complex<double>& e1, st
 
 void to_hessenberg(Hm& h) {
     const int n = h.n;
-    std::vector<double> v(n);
+    std::vector<double> v(n), w(n);
     for (int k = 0; k + 2 < n; ++k) {
         const int len = n - k - 1;  // rows k+1 .. n-1
         double alpha = h(k + 1, k);
@@ -128,11 +128,18 @@ void to_hessenberg(Hm& h) {
             d *= tau;
             for (int i = 0; i < len; ++i) h(k + 1 + i, j) -= d * v[i];
         }
-        for (int i = 0; i < n; ++i) {  // right: H (I - tau v v^T)
-            double d = 0.0;
-            for (int c = 0; c < len; ++c) d += h(i, k + 1 + c) * v[c];
-            d *= tau;
-            for (int c = 0; c < len; ++c) h(i, k + 1 + c) -= d * v[c];
+        // right: H (I - tau v v^T), column-oriented (same per-row summation order)
+        std::fill(w.begin(), w.end(), 0.0);
+        for (int c = 0; c < len; ++c) {
+            const double vc = v[c];
+            const double* col = &h(0, k + 1 + c);
+            for (int i = 0; i < n; ++i) w[i] += col[i] * vc;
+        }
+        for (int i = 0; i < n; ++i) w[i] *= tau;
+        for (int c = 0; c < len; ++c) {
+            const double vc = v[c];
+            double* col = &h(0, k + 1 + c);
+            for (int i = 0; i < n; ++i) col[i] -= w[i] * vc;
         }
     }
 }
