@@ -786,7 +786,7 @@ template <int W, int BN, int WGM, int MINB, int NT = kGemmThreads, int PFIRST = 
 __global__ void __launch_bounds__(NT, MINB)
 lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmU, double* A,
-                     size_t mstride, size_t plane, int n, int ld, int k, int c0) {
+                     size_t mstride, size_t plane, int n, int ld, int k, int c0, int band) {
     constexpr int WGN = (NT / 32) / WGM;
     constexpr int MI = GBM / WGM / 8, NI = BN / WGN / 8;
     static_assert(MI == 2, "row-pair fragments");
@@ -803,8 +803,23 @@ lu_gemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int b = blockIdx.z;
     double* Are = A + static_cast<size_t>(b) * mstride;
     double* Aim = Are + plane;
-    const int m0 = k + W + blockIdx.x * GBM;
-    const int n0 = c0 + blockIdx.y * BN;
+    // Tile order: launch order runs down the rows of one column block (x fastest);
+    // with band > 0 it runs through bands of `band` row tiles across every
+    // column block, so a band's L21 rows stay in L2 while the U12 column blocks
+    // stream (a 128-deep L21 panel of N = 36864 is 113 MB, beyond the L2).
+    int tx = blockIdx.x, ty = blockIdx.y;
+    if (band > 0) {
+        const int ntx = gridDim.x, nty = gridDim.y;
+        const int lin = blockIdx.x + ntx * blockIdx.y;
+        const int bi = lin / (band * nty);
+        const int b0 = bi * band;
+        const int hb = min(band, ntx - b0);
+        const int rem = lin - bi * band * nty;
+        ty = rem / hb;
+        tx = b0 + rem % hb;
+    }
+    const int m0 = k + W + tx * GBM;
+    const int n0 = c0 + ty * BN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp % WGM, wn = warp / WGM;
     const int r0 = wm * (GBM / WGM) + 2 * (lane >> 2);  // this lane's row pair in the tile
@@ -2213,11 +2228,24 @@ void gemm_step(const LuProblem& pb, int k, int w, cudaStream_t st, int c0 = -1, 
                        pb.A, pb.mstride, pb.plane, pb.n, pb.ld, k, w, c0, c1, gm.base, do_l ? w : 0);
             constexpr size_t sm = g3_smem_doubles<32>() * sizeof(double) + 128 +
                                   GSTAGES * (sizeof(uint64_t) + sizeof(unsigned));
+            // banded tile order once the L21 panel (3 planes, w deep) is a sizeable
+            // part of the L2 (FDSWEEP_GEMM_BAND_MB, default 24 MB; FDSWEEP_GEMM_BAND
+            // forces a band height in row tiles, 0 = off)
+            static const int band_env = [] {
+                const char* e = std::getenv("FDSWEEP_GEMM_BAND");
+                return e ? std::atoi(e) : -1;
+            }();
+            static const double band_mb = [] {
+                const char* e = std::getenv("FDSWEEP_GEMM_BAND_MB");
+                return e ? std::atof(e) : 24.0;
+            }();
+            const double l21_bytes = 3.0 * sizeof(double) * w * static_cast<double>(rest);
+            const int band = band_env >= 0 ? band_env : (l21_bytes > band_mb * 1e6 ? 64 : 0);
             auto go = [&](auto kern) {
                 ensure_dynamic_smem(reinterpret_cast<const void*>(kern), sm);
                 dim3 g3(ceil_div(rest, GBM), ceil_div(c1 - c0, 32), pb.batch);
                 FDS_LAUNCH(kern, g3, kGemmThreads, sm, st, tm.a, tm.b32, gm.l, gm.u32, pb.A, pb.mstride, pb.plane,
-                           pb.n, pb.ld, k, c0);
+                           pb.n, pb.ld, k, c0, band);
             };
             // P-first prologue on the first chunk (measured 0.4 % faster at cfg4)
             if (w == 256) go(lu_gemm3m_tma_kernel<256, 32, 4, 2, kGemmThreads, 1>);

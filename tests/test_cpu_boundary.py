@@ -154,7 +154,7 @@ def test_default_3m_gemm_kernel_is_tma_fed_dmma():
     issues only DMMA for its products (no FP64 adds in the k-loop: the operand
     sums come from lu_g3_prep_kernel), is fed by TMA tensor loads and moves
     its A fragments and the C tile in 16-byte accesses."""
-    fn = "_ZN4fdsb20lu_gemm3m_tma_kernelILi128ELi32ELi4ELi2ELi256ELi1ELi16ELi2EEEv14CUtensorMap_stS1_S1_S1_Pdmmiiii"
+    fn = "_ZN4fdsb20lu_gemm3m_tma_kernelILi128ELi32ELi4ELi2ELi256ELi1ELi16ELi2EEEv14CUtensorMap_stS1_S1_S1_Pdmmiiiii"
     out = subprocess.run(["cuobjdump", "-sass", "-fun", fn, str(P.library_path())], capture_output=True,
                          text=True).stdout
     assert "UTMALDG" in out
