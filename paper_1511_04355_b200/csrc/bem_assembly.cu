@@ -41,33 +41,93 @@ struct KTerms {
     cplx A, B, CB, G, B4;
 };
 
-__device__ __forceinline__ KTerms kterms(const BemParams& P, cplx z) {
+// sincos without the Payne-Hanek slow path: Cody-Waite reduction by pi/2 in
+// three FMA steps (fdlibm's 33-bit split of pi/2; with FMA each step rounds
+// once, so the reduced argument stays within a few ulp of exact for |x| up to
+// ~2^30, where the rounding already carried by x = Im(s) r / c_s dominates)
+// and fdlibm's __kernel_sin/__kernel_cos minimax polynomials on |r| <= pi/4.
+// Keeping CUDA's sincos out of the quadrature loops removes its local-memory
+// reduction array and slow-path registers.
+__device__ __forceinline__ void sincos_b(double x, double& s, double& c) {
+    const double q = rint(x * 6.36619772367581382433e-01);
+    double r = fma(-q, 1.57079632673412561417e+00, x);
+    r = fma(-q, 6.07710050630396597660e-11, r);
+    r = fma(-q, 2.02226624871116645580e-21, r);
+    const double z = r * r;
+    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
+                                                2.75573137070700676789e-06),
+                                         -1.98412698298579493134e-04),
+                                  8.33333333332248946124e-03),
+                           -1.66666666666666324348e-01);
+    const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09),
+                                                -2.75573143513906633035e-07),
+                                         2.48015872894767294178e-05),
+                                  -1.38888888888741095749e-03),
+                           4.16666666666666019037e-02);
+    const double sr = fma(r * z, ps, r);
+    const double hz = 0.5 * z, w = 1.0 - hz;
+    const double cr = w + (((1.0 - w) - hz) + z * z * pc);
+    const long long iq = static_cast<long long>(q);
+    double ss = (iq & 1) ? cr : sr;
+    double cc = (iq & 1) ? sr : cr;
+    if (iq & 2) ss = -ss;
+    if ((iq + 1) & 2) cc = -cc;
+    s = ss;
+    c = cc;
+}
+
+// e^{-(a + i b)}
+__device__ __forceinline__ cplx cexp_neg(double a, double b) {
+    double sn, cs;
+    sincos_b(b, sn, cs);
+    const double e = exp(-a);
+    return mk(e * cs, -e * sn);
+}
+
+// Per-thread constants of one frequency s: z = s r / c_s = (za + i zb) r and
+// 1/z = w / r, so the quadrature loops need no complex division.
+struct FreqK {
+    double za, zb;   // s / c_s
+    cplx w, w2;      // c_s / s and its square
+    cplx wk, wk2;    // (c_s / s) / k and its square (1/x1 = wk / r)
+    double r2ser;    // r^2 below which |z|^2 < kSeriesR2 (Taylor branch)
+};
+
+__device__ __forceinline__ FreqK freq_consts(const BemParams& P, cplx s) {
+    FreqK F;
+    F.za = s.re * P.inv_cs;
+    F.zb = s.im * P.inv_cs;
+    F.w = crecip(mk(F.za, F.zb));
+    F.w2 = F.w * F.w;
+    F.wk = F.w * P.inv_k;
+    F.wk2 = F.wk * F.wk;
+    const double zz = F.za * F.za + F.zb * F.zb;
+    F.r2ser = BemParams::kSeriesR2 / zz;
+    return F;
+}
+
+// Taylor branch (|z| < 0.3): A, B, C, D as power series in z.
+__device__ __forceinline__ KTerms kterms_series(const BemParams& P, cplx z) {
     KTerms o;
-    if (abs2(z) < BemParams::kSeriesR2) {
-        cplx A = mk(0.0, 0.0), B = A, C = A, D = A;
+    cplx A = mk(0.0, 0.0), B = A, C = A, D = A;
 #pragma unroll
-        for (int m = BemParams::kTerms - 1; m >= 0; --m) {
-            A = A * z + P.ta[m];
-            B = B * z + P.tb[m];
-            C = C * z + P.tc[m];
-            D = D * z + P.td[m];
-        }
-        o.A = A;
-        o.B = B;
-        o.CB = C - B;
-        o.G = C - D - 2.0 * B;
-        o.B4 = 4.0 * B - 2.0 * D;
-        return o;
+    for (int m = BemParams::kTerms - 1; m >= 0; --m) {
+        A = A * z + P.ta[m];
+        B = B * z + P.tb[m];
+        C = C * z + P.tc[m];
+        D = D * z + P.td[m];
     }
-    const double k = P.k, ik = P.inv_k;
-    const cplx x1 = z * k;
-    const double d = 1.0 / abs2(z);
-    const cplx iz = mk(z.re * d, -z.im * d);
-    const cplx iz2 = iz * iz;
-    const cplx P2 = iz + iz2;
-    const cplx P1 = iz * ik + iz2 * (ik * ik);
-    const cplx E2 = cexpd(-z);
-    const cplx E1 = cexpd(-x1) * (k * k);
+    o.A = A;
+    o.B = B;
+    o.CB = C - B;
+    o.G = C - D - 2.0 * B;
+    o.B4 = 4.0 * B - 2.0 * D;
+    return o;
+}
+
+// Closed form given P2 = 1/z + 1/z^2, P1 = 1/x + 1/x^2, E2 = e^{-z}, E1 = k^2 e^{-x}.
+__device__ __forceinline__ KTerms kterms_closed(cplx z, cplx x1, cplx P2, cplx P1, cplx E2, cplx E1) {
+    KTerms o;
     const cplx q1E1 = (3.0 * P1 + 1.0) * E1;
     o.A = (P2 + 1.0) * E2 - P1 * E1;
     o.B = (3.0 * P2 + 1.0) * E2 - q1E1;
@@ -75,6 +135,32 @@ __device__ __forceinline__ KTerms kterms(const BemParams& P, cplx z) {
     o.G = -((x1 + 1.0) * E1);
     o.B4 = (2.0 * z + 30.0 * P2 + 12.0) * E2 - (2.0 * x1 + 30.0 * P1 + 12.0) * E1;
     return o;
+}
+
+__device__ __forceinline__ KTerms kterms(const BemParams& P, cplx z) {
+    if (abs2(z) < BemParams::kSeriesR2) return kterms_series(P, z);
+    const double k = P.k, ik = P.inv_k;
+    const cplx x1 = z * k;
+    const double d = 1.0 / abs2(z);
+    const cplx iz = mk(z.re * d, -z.im * d);
+    const cplx iz2 = iz * iz;
+    const cplx E2 = cexp_neg(z.re, z.im);
+    const cplx E1 = cexp_neg(x1.re, x1.im) * (k * k);
+    return kterms_closed(z, x1, iz + iz2, iz * ik + iz2 * (ik * ik), E2, E1);
+}
+
+// Same terms at distance r (1/r = ir, 1/r^2 = ir2) from the per-thread
+// frequency constants: no complex division per point.
+__device__ __forceinline__ KTerms kterms_r(const BemParams& P, const FreqK& F, double r, double ir, double ir2) {
+    const cplx z = mk(F.za * r, F.zb * r);
+    if (r * r < F.r2ser) return kterms_series(P, z);
+    const double k = P.k;
+    const cplx x1 = z * k;
+    const cplx P2 = F.w * ir + F.w2 * ir2;
+    const cplx P1 = F.wk * ir + F.wk2 * ir2;
+    const cplx E2 = cexp_neg(z.re, z.im);
+    const cplx E1 = cexp_neg(x1.re, x1.im) * (k * k);
+    return kterms_closed(z, x1, P2, P1, E2, E1);
 }
 
 // Quadrature-point sums over one flat source element (n constant):
@@ -135,26 +221,27 @@ struct KAcc {
 
 // One regular quadrature point y (relative position r = y − x) of weight w.
 __device__ __forceinline__ void kpoint(const BemParams& P, KAcc& acc, double rx, double ry, double rz,
-                                       const double n[3], const double t[3], cplx s, double w) {
+                                       const double n[3], const double t[3], const FreqK& F, double w) {
     const double r2 = rx * rx + ry * ry + rz * rz;
     const double r = sqrt(r2);
     const double ir = 1.0 / r;
+    const double ir2 = ir * ir;
     const double e[3] = {rx * ir, ry * ir, rz * ir};
     const double rn = e[0] * n[0] + e[1] * n[1] + e[2] * n[2];
-    const KTerms k = kterms(P, s * (r * P.inv_cs));
+    const KTerms k = kterms_r(P, F, r, ir, ir2);
     const double fu = w * ir * P.inv_4pi_mu;
-    const double ft = w * ir * ir * (1.0 / (4.0 * kPi));
+    const double ft = w * ir2 * (1.0 / (4.0 * kPi));
     const double et = e[0] * t[0] + e[1] * t[1] + e[2] * t[2];
     acc.add(P, k, e, rn, fu, ft, et);
 }
 
 // Displacement-only point (the far 7-point U·t a near pair must cancel).
 __device__ __forceinline__ void kpoint_u(const BemParams& P, KAcc& acc, double rx, double ry, double rz,
-                                         const double t[3], cplx s, double w) {
+                                         const double t[3], const FreqK& F, double w) {
     const double r = sqrt(rx * rx + ry * ry + rz * rz);
     const double ir = 1.0 / r;
     const double e[3] = {rx * ir, ry * ir, rz * ir};
-    const KTerms k = kterms(P, s * (r * P.inv_cs));
+    const KTerms k = kterms_r(P, F, r, ir, ir * ir);
     acc.add_u(k, e, w * ir * P.inv_4pi_mu, e[0] * t[0] + e[1] * t[1] + e[2] * t[2]);
 }
 
@@ -184,7 +271,7 @@ __device__ __forceinline__ void kpoint_cpv(const BemParams& P, KAcc& acc, const 
 }  // namespace
 
 // ------------------------------------------------------------------ far field
-__global__ void __launch_bounds__(kFarThreads, 3)
+__global__ void __launch_bounds__(kFarThreads, 2)
 bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __restrict__ trac,
                int ne, const cplx* __restrict__ svec, double* __restrict__ A, size_t mstride,
                size_t plane, int ld, cplx* __restrict__ partial, size_t pstride) {
@@ -200,6 +287,7 @@ bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __rest
     __syncthreads();
     if (c >= ne) return;
     const cplx s = svec[b];
+    const FreqK F = freq_consts(P, s);
     const double x0 = geo[(size_t)c * 16 + 9], x1 = geo[(size_t)c * 16 + 10], x2 = geo[(size_t)c * 16 + 11];
     double* Are = A + (size_t)b * mstride;
     double* Aim = Are + plane;
@@ -212,13 +300,16 @@ bem_far_kernel(BemParams P, const double* __restrict__ geo, const double* __rest
         const double t[3] = {st[el][0], st[el][1], st[el][2]};
         KAcc acc;
         acc.zero();
-#pragma unroll 1
+        // two quadrature points in flight (independent transcendental chains);
+        // at 2 CTAs/SM the kernel keeps 255 registers (measured: cfg2 far
+        // stage 35.1 -> 32.8 ms; full unrolling or 3 CTAs/SM spill heavily)
+#pragma unroll 2
         for (int q = 0; q < 7; ++q) {
             const double l0 = P.r7l[q][0], l1 = P.r7l[q][1], l2 = P.r7l[q][2];
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
             const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
             const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
-            kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[q] * g[15]);
+            kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, F, P.r7w[q] * g[15]);
         }
         cplx T[9], Ue[3];
         acc.finish(n, t, T, Ue);
@@ -258,6 +349,7 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
     const bool active = b < B;
     const int c = pairs[3 * pair], e = pairs[3 * pair + 1], level = pairs[3 * pair + 2];
     const cplx s = svec[active ? b : 0];
+    const FreqK F = freq_consts(P, s);
     const double* g = geo + (size_t)e * 16;
     const double x0 = geo[(size_t)c * 16 + 9], x1 = geo[(size_t)c * 16 + 10], x2 = geo[(size_t)c * 16 + 11];
     const double n[3] = {g[12], g[13], g[14]};
@@ -337,7 +429,7 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
                 const double yx = l0 * p[0][0] + l1 * p[1][0] + l2 * p[2][0];
                 const double yy = l0 * p[0][1] + l1 * p[1][1] + l2 * p[2][1];
                 const double yz = l0 * p[0][2] + l1 * p[1][2] + l2 * p[2][2];
-                kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area);
+                kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, F, P.r7w[gq] * area);
             }
         }
         // subtract the far kernel's 7-point U·t for this pair (it is in the partials)
@@ -349,7 +441,7 @@ bem_near_kernel(BemParams P, const double* __restrict__ geo, const double* __res
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
             const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
             const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
-            kpoint_u(P, accf, yx - x0, yy - x1, yz - x2, t, s, P.r7w[gq] * g[15]);
+            kpoint_u(P, accf, yx - x0, yy - x1, yz - x2, t, F, P.r7w[gq] * g[15]);
         }
         acc.finish(n, t, T, Ut);
 #pragma unroll
@@ -402,6 +494,7 @@ bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* _
     if (warp >= npairs) return;
     const int c = pairs[3 * warp], e = pairs[3 * warp + 1], level = pairs[3 * warp + 2];
     const cplx s = svec[b];
+    const FreqK F = freq_consts(P, s);
     const double* g = geo + (size_t)e * 16;
     const double x0 = geo[(size_t)c * 16 + 9], x1 = geo[(size_t)c * 16 + 10], x2 = geo[(size_t)c * 16 + 11];
     const double n[3] = {g[12], g[13], g[14]};
@@ -477,7 +570,7 @@ bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* _
             const double yx = l0 * p[0][0] + l1 * p[1][0] + l2 * p[2][0];
             const double yy = l0 * p[0][1] + l1 * p[1][1] + l2 * p[2][1];
             const double yz = l0 * p[0][2] + l1 * p[1][2] + l2 * p[2][2];
-            kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, s, P.r7w[gq] * area);
+            kpoint(P, acc, yx - x0, yy - x1, yz - x2, n, t, F, P.r7w[gq] * area);
         }
         acc.finish(n, t, T, Ut);
         // subtract the far kernel's 7-point U·t for this pair (it is in the partials)
@@ -488,7 +581,7 @@ bem_near_pts_kernel(BemParams P, const double* __restrict__ geo, const double* _
             const double yx = l0 * g[0] + l1 * g[3] + l2 * g[6];
             const double yy = l0 * g[1] + l1 * g[4] + l2 * g[7];
             const double yz = l0 * g[2] + l1 * g[5] + l2 * g[8];
-            kpoint_u(P, accf, yx - x0, yy - x1, yz - x2, t, s, P.r7w[lane] * g[15]);
+            kpoint_u(P, accf, yx - x0, yy - x1, yz - x2, t, F, P.r7w[lane] * g[15]);
 #pragma unroll
             for (int i = 0; i < 3; ++i) Ut[i] = Ut[i] - (accf.sa * t[i] - accf.sb[i]);
         }
