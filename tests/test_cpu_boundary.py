@@ -89,26 +89,48 @@ def _free_port():
 
 
 def test_bench_replica_reduction_gloo():
-    """bench.py's max-over-ranks reduction over world_size 2 (gloo, CPU)."""
+    """bench.py's N > 1 plumbing over world_size 2 (gloo, CPU): the contour's
+    sub-batches are dealt to the replicas without overlap inside a step, the
+    step time is the max over ranks and the value is the whole-job aggregate."""
     code = r'''
-import os, torch, torch.distributed as dist
+import os, sys, numpy as np, torch.distributed as dist
+sys.path.insert(0, os.environ["FDS_ROOT"])
+import bench
 dist.init_process_group("gloo")
-r = dist.get_rank()
-t = torch.tensor([10.0 + 5.0 * r], dtype=torch.float64)
-dist.all_reduce(t, op=dist.ReduceOp.MAX)
-assert t.item() == 15.0
-dist.barrier()
-if r == 0: print("OK", dist.get_world_size())
+r, w = dist.get_rank(), dist.get_world_size()
+s = bench.contour(bench.NS4)
+mine = [bench.sub_batch(s, i, r, w) for i in range(4)]
+assert all(len(b) == bench.SUB for b in mine)
+# every step: the two replicas hold different frequencies of the contour
+import torch
+for b in mine:
+    first = torch.tensor([b[0].imag], dtype=torch.float64)
+    both = [torch.zeros(1, dtype=torch.float64) for _ in range(w)]
+    dist.all_gather(both, first)
+    assert len({float(x) for x in both}) == w
+# over NSUB / w steps the replicas cover the 8 full sub-batches exactly once
+cover = torch.zeros(bench.NSUB, dtype=torch.float64)
+for i in range(bench.NSUB // w):
+    cover[(i * w + r) % bench.NSUB] += 1
+dist.all_reduce(cover)
+assert cover.tolist() == [1.0] * bench.NSUB
+total_ms = bench.allreduce_max(dist, 1000.0 + 500.0 * r)   # slowest rank wins
+assert total_ms == 1500.0
+v = bench.whole_job_rate(bench.SUB, w, 3, total_ms)
+assert abs(v - bench.SUB * w * 3 / 1.5) < 1e-12
+bench.barrier(dist)
+if r == 0: print("OK", w)
 dist.destroy_process_group()
 '''
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), FDS_ROOT=str(ROOT))
     procs = []
     for r in range(2):
         e = dict(env, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r))
-        procs.append(subprocess.Popen([sys.executable, "-c", code], env=e, stdout=subprocess.PIPE, text=True))
-    outs = [p.communicate(timeout=120)[0] for p in procs]
-    assert all(p.returncode == 0 for p in procs)
-    assert "OK 2" in outs[0]
+        procs.append(subprocess.Popen([sys.executable, "-c", code], env=e, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=180) for p in procs]
+    assert all(p.returncode == 0 for p in procs), [o[1][-2000:] for o in outs]
+    assert "OK 2" in outs[0][0]
 
 
 def test_version_string_names_the_target():
