@@ -1979,6 +1979,26 @@ int panel_rows_max() {
     return std::min(by_smem, kPanelThreads);  // one thread per row
 }
 
+// Co-resident CTAs of lu_panel_kernel<NB> at its largest row block (the group
+// barrier needs a matrix's P CTAs on chip together): 16-wide sub-panels of 256
+// rows take 66 KB, so three fit an SM and one matrix may have up to 3 x 148 x 256
+// = 113 664 rows (N = 37 888 when it was one CTA per SM).
+template <int NB>
+int panel_ctas_max() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    FDS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    const size_t smem = panel_smem(NB, panel_rows_max<NB>());
+    ensure_dynamic_smem(reinterpret_cast<const void*>(lu_panel_kernel<NB>), smem);
+    int per_sm = 1;
+    FDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_kernel<NB>, kPanelThreads, smem));
+    return cache[dev] = device_info().sms * std::max(per_sm, 1);
+}
+
 bool use_cluster_panel() {
     static const bool on = [] {
         const char* e = std::getenv("FDSWEEP_PANEL_CLUSTER");
@@ -2026,7 +2046,7 @@ void panel_step(const LuProblem& pb, LuWorkspace& ws, int k, int w, cudaStream_t
     const int rows = pb.n - k;
     const int rmax = panel_rows_max<NB>();
     int P = ceil_div(rows, rmax);
-    if (P > sms) throw NumericError("lu: panel does not fit in on-chip memory");
+    if (P > panel_ctas_max<NB>()) throw NumericError("lu: panel does not fit in on-chip memory");
     const int R = ceil_div(rows, P);
     const size_t smem = panel_smem(NB, R);
     ensure_dynamic_smem(reinterpret_cast<const void*>(lu_panel_kernel<NB>), smem);
@@ -2293,9 +2313,8 @@ bool use_subpanels(const LuProblem&) { return subpanels_enabled(); }
 int lu_panel_width(int n) {
     // NB = 64; the panel must fit one matrix's rows in the SMs' shared memory:
     // as 16-wide sub-panels (default) or as one 64-wide GEPP panel; otherwise 32.
-    const int sms = device_info().sms;
-    if (ceil_div(n, panel_rows_max<64>()) <= sms) return 64;
-    if (subpanels_enabled() && ceil_div(n, panel_rows_max<kSub>()) <= sms) return 64;
+    if (ceil_div(n, panel_rows_max<64>()) <= panel_ctas_max<64>()) return 64;
+    if (subpanels_enabled() && ceil_div(n, panel_rows_max<kSub>()) <= panel_ctas_max<kSub>()) return 64;
     return 32;
 }
 

@@ -337,3 +337,25 @@ def test_manufactured_point_source_converges_on_device_cube_n36864():
     assert abs(errs[0] - 0.01499) < 1e-4 and abs(errs[1] - 0.007457) < 1e-4  # the oracle's values
     # the cube's edges and corners slow the rate at the finest mesh (0.49 % measured)
     assert errs[2] < 0.75 * errs[1] and errs[2] < 0.006
+
+
+def test_lu_panel_with_several_ctas_per_sm_n46656():
+    """Beyond configs[2]: a 36 x 36 cube (15552 triangles, N = 46656, 34.8 GB) needs
+    183 panel CTAs of 256 rows for one matrix — more than one per SM, so the group
+    barrier runs over CTAs that share SMs (`panel_ctas_max`, csrc/lu.cu). Backward
+    error of the LU solution and sampled assembly entries against the oracle."""
+    V, F = mesh.cube_cavity(36)
+    tr = mesh.pressure_traction(V, F)
+    assert 3 * F.shape[0] == 46656
+    s = contour(7)
+    gpu = P.BemSystem(V, F, tr, max_batch=1)
+    u = gpu.evaluate(s)
+    nr = gpu.residual(s, u)
+    back = nr["res"] / (nr["a_inf"] * nr["u"] + nr["b"])
+    print(f"N=46656: backward error {back:.2e}, ||Au-b||/||b|| = {nr['res'] / nr['b']:.2e}, LU {gpu.last_timing()}")
+    assert back < 1e-13 and nr["res"] / nr["b"] < 1e-10
+    rows, cols = _sample_entries(V, F, 1000, 6, seed=5)
+    ag, _ = gpu.assemble_entries(s, rows, cols, with_rhs=True)
+    ao = O.Bem(V, F, tr).entries(s, rows, cols)
+    assert np.abs(ag - ao).max() < 1e-12 * np.abs(ao).max()
+    gpu.close()

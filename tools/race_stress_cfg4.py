@@ -3,7 +3,8 @@ tests/test_gpu_race_stress.py, which runs small systems inside the test budget):
 cfg4 (N = 15360) solved as a batch of 2 (super-panel schedule, global-slot and
 cluster panels, 3M GEMM ring, dataflow solve) and as a single matrix
 (look-ahead schedule with the side-stream panel), and cfg3 (N = 36864) as a
-single matrix (a 144-CTA global-slot panel behind one software barrier), twice
+single matrix (a 144-CTA global-slot panel behind one software barrier), a
+36 x 36 cube (N = 46656: 183 panel CTAs, more than one per SM), twice
 under the product build
 and twice under the timing-perturbed FDS_JITTER build. Correct synchronisation
 means identical SHA-256 digests. Prints one JSON object."""
@@ -34,6 +35,11 @@ g.close()
 V3, F3 = mesh.cube_cavity(32)
 g3 = P.BemSystem(V3, F3, mesh.pressure_traction(V3, F3), max_batch=1)
 out["cfg3_single"] = [h(g3.evaluate(s2[0])) for _ in range(2)]  # P = 144 CTAs behind one software barrier
+g3.close()
+V5, F5 = mesh.cube_cavity(36)
+g5 = P.BemSystem(V5, F5, mesh.pressure_traction(V5, F5), max_batch=1)
+out["n46656_single"] = [h(g5.evaluate(s2[0])) for _ in range(2)]  # P = 183 CTAs, several per SM
+g5.close()
 out["wall_s"] = time.perf_counter() - t0
 out["library"] = str(P.library_path())
 print("RESULT" + json.dumps(out))
@@ -53,7 +59,7 @@ def run(variant):
 
 
 base, jit = run(None), run("jitter")
-ok = all(len(set(base[k])) == 1 and set(jit[k]) == set(base[k]) for k in ("batch2", "single", "cfg3_single"))
+ok = all(len(set(base[k])) == 1 and set(jit[k]) == set(base[k]) for k in ("batch2", "single", "cfg3_single", "n46656_single"))
 print(json.dumps({"workload": "cfg4 N=15360: batch of 2 (k = 7, 200) and a single matrix (k = 7); cfg3 N=36864 single "
-                              "matrix (k = 7); 2 runs per build",
+                              "matrix (k = 7); N=46656 cube single matrix (panel CTAs share SMs); 2 runs per build",
                   "product": base, "jitter": jit, "bit_identical": ok}))
