@@ -239,10 +239,15 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU leg
-# FP64 flops per far-field kernel evaluation: 32 x (2 DFMA + DMUL + DADD) warp
-# instructions of bem_far_kernel (ncu sass__inst_executed_per_opcode on cfg2)
-# divided by its 7 N_e (N_e - 1) B evaluations (profiles/r01_assembly_ncu_full.json).
-ASM_FLOPS_PER_EVAL = 439.0
+# FP64 work per far-field kernel evaluation: executed thread instructions of
+# bem_far_kernel at HEAD (ncu sm__sass_thread_inst_executed_op_{dfma,dadd,dmul}
+# on cfg2: 2 DFMA + DADD + DMUL flops, DFMA + DADD + DMUL issue slots) divided by
+# its 7 N_e (N_e - 1) B evaluations (profiles/r02_far_ncu.json, round2_op_counts).
+# A DADD or DMUL takes the same FP64-pipe slot as a DFMA, so the pipe fraction
+# (instructions against peak / 2 flops per slot) is the bound; the flop fraction
+# is reported beside it.
+ASM_FLOPS_PER_EVAL = 425.8
+ASM_FP64_INST_PER_EVAL = 274.1
 
 
 def profile_stages(P, L):
@@ -366,7 +371,10 @@ def run_ours(args, world, rank, local, dist):
                          "flops_per_evaluation": ASM_FLOPS_PER_EVAL,
                          "tflops": ASM_FLOPS_PER_EVAL * far["work"] / max(far["ms"], 1e-9) / 1e9,
                          "fp64_frac": ASM_FLOPS_PER_EVAL * far["work"] / max(far["ms"], 1e-9) / 1e9 /
-                         measured_fp64_peak()[0]},
+                         measured_fp64_peak()[0],
+                         "fp64_instructions_per_evaluation": ASM_FP64_INST_PER_EVAL,
+                         "fp64_pipe_frac": ASM_FP64_INST_PER_EVAL * far["work"] / max(far["ms"], 1e-9) / 1e9 /
+                         (measured_fp64_peak()[0] / 2.0)},
         "wall_ms_per_step": wall * 1e3 / args.steps,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
