@@ -259,6 +259,16 @@ int64_t fds_kernel_launches(void);
 int fds_profile_enable(int on);
 int fds_profile_read(int kind, int* count, double* total_ms, double* total_work);
 
+/* Debug: red-zone check of the library's device allocations (no reference
+ * counterpart; stands in for compute-sanitizer memcheck, which this GPU pool
+ * does not allow). With FDSWEEP_REDZONE set in the environment before the
+ * library loads, every cudaMalloc carries a 4 KB guard zone on each side;
+ * this call synchronises the device, compares the zones of all live
+ * allocations and returns the bytes found overwritten so far (freed
+ * allocations included), the number of zone checks made and the live
+ * allocation count. enabled = 0 and zeros when the mode is off. */
+int fds_debug_redzone_check(int* enabled, long long* overwritten_bytes, long long* checks, long long* live);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

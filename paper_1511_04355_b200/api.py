@@ -154,6 +154,14 @@ def profile_read(kind: int):
     return c.value, ms.value, wk.value
 
 
+def redzone_check() -> dict:
+    """Debug (fds_debug_redzone_check): with FDSWEEP_REDZONE set before the library loads, compares the
+    guard zones around every device allocation of the library; `overwritten_bytes` must be 0."""
+    on, bad, chk, live = ctypes.c_int(), ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
+    _check(lib().fds_debug_redzone_check(ctypes.byref(on), ctypes.byref(bad), ctypes.byref(chk), ctypes.byref(live)))
+    return {"enabled": bool(on.value), "overwritten_bytes": bad.value, "checks": chk.value, "live": live.value}
+
+
 def kernel_launches() -> int:
     return int(lib().fds_kernel_launches())
 

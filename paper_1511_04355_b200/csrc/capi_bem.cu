@@ -303,6 +303,27 @@ int fds_profile_enable(int on) {
     });
 }
 
+int fds_debug_redzone_check(int* enabled, long long* overwritten_bytes, long long* checks, long long* live) {
+    return fds_guard([&] {
+        const bool on = RedzoneRegistry::enabled();
+        long long bad = 0, chk = 0, nlive = 0;
+        if (on) {
+            FDS_CUDA(cudaDeviceSynchronize());
+            auto& rz = RedzoneRegistry::get();
+            std::lock_guard<std::mutex> lk(rz.mu);
+            long long now = 0;
+            for (auto& kv : rz.live) now += rz.check_one(kv.first, kv.second);
+            bad = rz.violations + now;  // live zones are re-counted on every call, freed ones once
+            chk = rz.checked;
+            nlive = static_cast<long long>(rz.live.size());
+        }
+        if (enabled) *enabled = on ? 1 : 0;
+        if (overwritten_bytes) *overwritten_bytes = bad;
+        if (checks) *checks = chk;
+        if (live) *live = nlive;
+    });
+}
+
 int fds_profile_read(int kind, int* count, double* total_ms, double* total_work) {
     return fds_guard([&] {
         auto& p = profiler();
