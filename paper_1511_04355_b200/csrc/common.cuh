@@ -41,7 +41,7 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // cudaMalloc of the library is widened by a 4 KB zone on each side filled with
 // 0xA5, the back zone starting at the first byte past the requested size; the
 // zones are compared on cudaFree and by fds_debug_redzone_check (all live
-// allocations). Off by default: the macros below then forward unchanged.
+// allocations). The allocation itself is pre-filled with 0xFF (NaN / -1). Off by default: the macros below then forward unchanged.
 struct RedzoneRegistry {
     struct Rec { void* base; size_t bytes; };
     std::mutex mu;
@@ -87,6 +87,12 @@ inline cudaError_t rz_malloc(T** out, size_t bytes) {
     char* user = static_cast<char*>(base) + RedzoneRegistry::kZone;
     ::cudaMemset(base, RedzoneRegistry::kFill, RedzoneRegistry::kZone);
     ::cudaMemset(user + bytes, RedzoneRegistry::kFill, back);
+    // initcheck stand-in: fresh memory reads as NaN doubles / -1 ints, so a result that
+    // depends on bytes the library never wrote fails the parity tests run in this mode
+    ::cudaMemset(user, 0xFF, bytes);
+    // the fills run on the legacy stream; the library's streams are non-blocking, so
+    // finish them before the allocation is handed out
+    ::cudaDeviceSynchronize();
     std::lock_guard<std::mutex> lk(rz.mu);
     rz.live[user] = {base, bytes};
     *out = reinterpret_cast<T*>(user);
@@ -140,11 +146,18 @@ inline void once_per_device(const void* key, F init) {
 }
 // Every kernel launch of the library goes through this (launch accounting +
 // immediate launch-error check).
+// FDSWEEP_SYNC_LAUNCH (debug): synchronise after every launch so a faulting kernel is named
+inline bool sync_launches() {
+    static const bool on = std::getenv("FDSWEEP_SYNC_LAUNCH") != nullptr;
+    return on;
+}
 #define FDS_LAUNCH(kernel, grid, block, smem, stream, ...)                        \
     do {                                                                           \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);               \
         ::fdsb::g_launches.fetch_add(1, std::memory_order_relaxed);               \
         ::fdsb::cuda_check(cudaGetLastError(), #kernel);                           \
+        if (::fdsb::sync_launches())                                               \
+            ::fdsb::cuda_check(cudaStreamSynchronize(stream), #kernel " (FDSWEEP_SYNC_LAUNCH)"); \
     } while (0)
 
 // ---------------------------------------------------------------- complex

@@ -2,7 +2,8 @@
 this GPU pool, profiles/r02_compute_sanitizer_closed.log). A child pytest process runs the functional
 GPU suites with FDSWEEP_REDZONE=1: every cudaMalloc of the library then carries a 4 KB guard zone on
 each side (csrc/common.cuh), compared on every free and, for the allocations still live, at session
-end (tests/conftest.py). The suites cover the odd sizes where an overrun would show: LU n = 1 ... 3001
+end (tests/conftest.py); fresh allocations are pre-filled with 0xFF (NaN / -1), so the suites' parity
+assertions also fail on any dependence on memory the library never wrote. The suites cover the odd sizes where an overrun would show: LU n = 1 ... 3001
 with forced pivoting and every 64/128/256 boundary, ragged VF / FSM tiles, batches that do not fill a
 chunk, GMRES restarts, the AFS driver."""
 import os
